@@ -1,0 +1,223 @@
+/*
+ * amrb.h -- C ABI of libamrb.so, the B200 (sm_100a) MultiFab / FillBoundary /
+ * MLMG hot path.
+ *
+ * The reference (/root/reference/pkg, package `amrkit`) is pure Python and has
+ * no FFI; its drop-in surface is the module API.  Each entry point below names
+ * the reference function whose work it takes over; the Python layer in
+ * paper_2009_12009_b200/ keeps the reference's signatures and calls these
+ * through ctypes.
+ *
+ * Conventions
+ *   - every call returns AMRB_OK (0) or a negative status; amrb_last_error()
+ *     gives a thread-local message.  The Python wrapper maps AMRB_EINVAL to
+ *     ValueError, AMRB_ENCCL to TransportError(src, dst, why) and AMRB_ECUDA to
+ *     RuntimeError.
+ *   - plain pointers and sizes only; device buffers are owned by the caller
+ *     (PyTorch).  Plans and programs own their host/device descriptor tables.
+ *   - `stream` is a cudaStream_t passed as void*; every device call is
+ *     asynchronous on it.  `nccl_comm` is an ncclComm_t passed as void*.
+ *   - All boxes are described in 3-D: a D-dimensional box's axis d maps to
+ *     axis (3 - D + d); padding axes have lo = hi = 0.  Storage is C-order
+ *     (comp, i, j, k) with k unit-stride, like the reference's Fab
+ *     (fabarray.py:33-38), but every k-row is padded so valid rows start on a
+ *     32-byte sector.
+ *
+ * Fab table ("fabtab"): int64[nboxes][AMRB_FABTAB_W] describing one
+ * FabArray's storage on one device:
+ *     [0] element offset of the grown box's lo cell, comp 0
+ *     [1] comp stride   [2] axis-0 stride   [3] axis-1 stride  (axis-2 stride 1)
+ *     [4..6] grown-box lo (3-D padded)
+ *     [7] 1 if the box is resident on this device, else 0
+ */
+#ifndef AMRB_H
+#define AMRB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMRB_OK 0
+#define AMRB_EINVAL (-1)
+#define AMRB_ECUDA (-2)
+#define AMRB_ENCCL (-3)
+#define AMRB_ENOMEM (-4)
+
+#define AMRB_FABTAB_W 8
+#define AMRB_REC_W 11 /* src, dst, src_lo[3], src_hi[3], shift[3] (3-D padded) */
+
+const char* amrb_last_error(void);
+int amrb_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Communication plans (host).  Records are CopyRecord(src, dst, src_box,    */
+/* dst_box = src_box + shift, shift) sorted by (dst, dst_box.lo, src, shift) */
+/* -- the reference's CommPlan order (fabarray.py:169-197).                  */
+/* ------------------------------------------------------------------------ */
+typedef struct amrb_plan amrb_plan;
+
+/* C++ twin of _build_fill (fabarray.py:262-277) incl. _periodic_shifts
+ * (:235-243), box_diff slabs (index_space.py:320-345) and the BoxHash query
+ * (boxarray.py:169-180, 216-278).  lohi: nboxes x 2*dim (lo then hi). */
+int amrb_plan_fill_create(int dim, int nboxes, const int32_t* lohi, int ngrow,
+                          const int32_t* domain_lohi, const uint8_t* periodic,
+                          amrb_plan** out);
+
+/* _build_copy (fabarray.py:291-302) when dst_ngrow == 0, and
+ * build_plan_copy_grown (coarse_fine.py:201-220) otherwise.  domain_lohi may be
+ * NULL (no periodic images). */
+int amrb_plan_copy_create(int dim, int ndst, const int32_t* dst_lohi, int nsrc,
+                          const int32_t* src_lohi, int dst_ngrow,
+                          const int32_t* domain_lohi, const uint8_t* periodic,
+                          amrb_plan** out);
+
+/* Transpose of the fill plan (build_plan_sum_boundary, fabarray.py:305-318). */
+int amrb_plan_sum_create(int dim, int nboxes, const int32_t* lohi, int ngrow,
+                         const int32_t* domain_lohi, const uint8_t* periodic,
+                         amrb_plan** out);
+
+/* Number of records and total cells (one component). */
+int amrb_plan_size(const amrb_plan* p, int64_t* nrecords, int64_t* ncells);
+/* Export records: out = int32[nrecords][AMRB_REC_W] (parity checks). */
+int amrb_plan_records(const amrb_plan* p, int32_t* out);
+int amrb_plan_destroy(amrb_plan* p);
+
+/* ------------------------------------------------------------------------ */
+/* Copy programs (device): a plan bound to concrete storage.  Replaces the   */
+/* two-phase executor _execute_plan (fabarray.py:326-361).                   */
+/* mode 1 (sim): every rank's boxes live on this device (the reference's    */
+/*     simulated ranks); remote records are packed into one staging buffer,  */
+/*     one segment per ordered (src,dst) rank pair, and unpacked from it.    */
+/* mode 0 (nccl): one process per GPU; this device is rank `my_rank`.        */
+/*     Remote records ride one NCCL send/recv per ordered peer pair.         */
+/* mode 2 (local): keep only records with src and dst owned by my_rank      */
+/*     (copies between a distributed FabArray and a per-rank replica).      */
+/* op: 0 = dst = src (fill / parallel_copy), 1 = dst += src (sum_boundary;   */
+/*     overlapping records are applied in plan order, in waves).             */
+/* Message payloads are C-order (ncomp, e0, e1, e2) record slices           */
+/* concatenated in plan order -- the reference's message layout (:341-347). */
+/* ------------------------------------------------------------------------ */
+typedef struct amrb_prog amrb_prog;
+
+int amrb_prog_create(const amrb_plan* plan, int ncomp,
+                     const int64_t* src_fabtab, int nsrc, const int32_t* src_owner,
+                     const int64_t* dst_fabtab, int ndst, const int32_t* dst_owner,
+                     int nranks, int my_rank, int mode, int op,
+                     amrb_prog** out);
+/* Elements of staging needed: send (and recv, which is the same buffer in
+ * sim mode).  Per-pair message table: int64[npairs][4] = src_rank, dst_rank,
+ * element offset, element count, in (src,dst) order. */
+int amrb_prog_info(const amrb_prog* g, int64_t* send_elems, int64_t* recv_elems,
+                   int64_t* npairs, int64_t* local_records);
+int amrb_prog_pairs(const amrb_prog* g, int64_t* out);
+int amrb_prog_run(amrb_prog* g, const double* src_base, double* dst_base,
+                  double* sendbuf, double* recvbuf, void* nccl_comm, void* stream);
+int amrb_prog_destroy(amrb_prog* g);
+
+/* ------------------------------------------------------------------------ */
+/* Level descriptors for the ParallelFor box loop (advect.py:143-178 is the  */
+/* reference's per-box loop pattern).  A level = one BoxArray on one device: */
+/* per-box valid lo / extents (3-D padded) and, per operand, the fab table.  */
+/* ------------------------------------------------------------------------ */
+typedef struct amrb_level amrb_level;
+
+/* boxes: int32[nboxes][6] valid lo, hi (3-D padded); resident: uint8[nboxes]
+ * (1 = box on this device).  Builds the device tile tables. */
+int amrb_level_create(int nboxes, const int32_t* boxes, const uint8_t* resident,
+                      amrb_level** out);
+int amrb_level_destroy(amrb_level* lv);
+
+/* A bound operand: fab table for one FabArray on a level. */
+typedef struct amrb_field amrb_field;
+int amrb_field_create(const amrb_level* lv, const int64_t* fabtab, int ngrow,
+                      amrb_field** out);
+int amrb_field_destroy(amrb_field* f);
+
+/* out = L(phi) on valid cells, 7-point, ((phi[-1] - 2 phi) + phi[+1]) * dh
+ * per axis, summed x, y, z left to right.  phi ghosts (width 1) must be
+ * filled.  dh = 1/dx^2 per axis. */
+int amrb_lap_apply(const amrb_level* lv, amrb_field* out, double* out_base,
+                   const amrb_field* phi, const double* phi_base,
+                   const double dh[3], void* stream);
+
+/* r = rhs - L(phi). */
+int amrb_residual(const amrb_level* lv, amrb_field* r, double* r_base,
+                  const amrb_field* rhs, const double* rhs_base,
+                  const amrb_field* phi, const double* phi_base,
+                  const double dh[3], void* stream);
+
+/* One GSRB colour: cells with (i+j+k+color) % 2 == 0 (global indices) get
+ * phi += (rhs - L(phi)) / gamma, gamma = -2 (dh0+dh1+dh2). */
+int amrb_gsrb_color(const amrb_level* lv, amrb_field* phi, double* phi_base,
+                    const amrb_field* rhs, const double* rhs_base,
+                    const double dh[3], int color, void* stream);
+
+/* One fused red+black sweep, out of place: b = GSRB(a) (bit-identical to
+ * colour 0 then colour 1 in place with a width-1 fill in between).  Needs the
+ * ghosts of `a` filled to width 2 and of `rhs` to width 1; the red update of
+ * the first ghost ring is recomputed locally, so no second exchange is needed.
+ * fixed_lohi (nullable) = int32[6] global lo, hi: cells outside it in any axis
+ * are never relaxed (non-periodic physical boundaries). */
+int amrb_gsrb_sweep(const amrb_level* lv, const amrb_field* a, const double* a_base,
+                    amrb_field* b, double* b_base, const amrb_field* rhs,
+                    const double* rhs_base, const double dh[3],
+                    const int32_t* fixed_lohi, void* stream);
+
+/* average_down (coarse_fine.py:136-163) on the box-local coarsened layout
+ * (crse box b = fine box b coarsened).  ratio = int32[3] per 3-D axis, each 1
+ * or 2 (NULL = 2,2,2).  mode 0 "average": crse = mean of the children summed
+ * in numpy's reshape-mean order, e.g. in 3-D ((((c000+c001)+(c010+c011))
+ * +(c100+c101))+(c110+c111))/8; mode 1 "injection": the child at offset 0. */
+int amrb_restrict(const amrb_level* crse_lv, amrb_field* crse, double* crse_base,
+                  const amrb_field* fine, const double* fine_base, int ncomp,
+                  const int32_t* ratio, int mode, void* stream);
+
+/* Fused residual + restriction (3-D, ratio 2): crse = average_down of
+ * (rhs - L(phi)), bit-identical to residual then amrb_restrict. */
+int amrb_residual_restrict(const amrb_level* crse_lv, amrb_field* crse,
+                           double* crse_base, const amrb_field* rhs,
+                           const double* rhs_base, const amrb_field* phi,
+                           const double* phi_base, const double dh[3],
+                           void* stream);
+
+/* interp_to_fine "pc" (coarse_fine.py:166-185, interp_block :60-72),
+ * optionally followed by an add: fine(c) (+)= crse(c / ratio), crse on the
+ * box-local coarsened layout.  add = 0 is plain pc interpolation. */
+int amrb_prolong(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
+                 const amrb_field* crse, const double* crse_base, int ncomp,
+                 const int32_t* ratio, int add, void* stream);
+
+/* reduce (fabarray.py:409-440) over valid cells of one component on this
+ * device: kind 0 sum, 1 min, 2 max, 3 max|x| (inf-norm).  Deterministic:
+ * fixed-shape per-tile partials then one ordered pass.  Result (one double)
+ * is written to dev_out. */
+int amrb_reduce(const amrb_level* lv, const amrb_field* x, const double* x_base,
+                int comp, int kind, double* dev_out, void* stream);
+
+/* Fill ghost cells outside the physical domain (apply_domain_boundary,
+ * amr_core.py:111-146).  bc: int32[3][2] per (axis, side) 0 periodic/skip,
+ * 1 external (value), 2 extrap.  domain: int32[6] lo, hi (3-D padded). */
+int amrb_domain_bc(const amrb_level* lv, amrb_field* f, double* base, int ncomp,
+                   const int32_t* domain, const int32_t* bc, double value,
+                   void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* NCCL plumbing (multi-GPU).  The unique id is exchanged by the caller      */
+/* (torch.distributed); the communicator is owned by the Transport.          */
+/* ------------------------------------------------------------------------ */
+int amrb_nccl_unique_id(uint8_t* out128);
+int amrb_nccl_comm_create(const uint8_t* id128, int nranks, int rank, void** comm);
+int amrb_nccl_comm_destroy(void* comm);
+/* In-place all-reduce of n doubles: op 0 sum, 1 min, 2 max. */
+int amrb_nccl_allreduce(double* buf, int64_t n, int op, void* comm, void* stream);
+/* All-gather: each rank contributes n doubles. */
+int amrb_nccl_allgather(const double* send, double* recv, int64_t n, void* comm,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMRB_H */

@@ -1,0 +1,198 @@
+"""numpy restatement of the MLMG Poisson V-cycle (definitions for the device path).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PARITY UNPINNED: the reference package has no linear solver (SPEC.md:13,
+SPEC.md:532); the Laplacian, GSRB smoother, residual and V-cycle are DEFINED
+here on top of the reference-pinned primitives in oracle.mesh_ref
+(fill_boundary, average_down, interp_to_fine 'pc', reduce), following
+SURVEY.md section 8(c):
+
+* operator  L(phi) = (dh0*((phi[i-1]-2phi)+phi[i+1]) + dh1*(...)) + dh2*(...),
+  dh_d = 1/dx_d^2, dx from Geometry.cell_size (amr_core.py:37-40);
+* residual  r = rhs - L(phi);
+* GSRB      per colour c in (0, 1), cells with (i+j+k+c) % 2 == 0 in GLOBAL
+  index space: phi <- phi + (rhs - L(phi)) / gamma, gamma = -2*(dh0+dh1+dh2);
+  one sweep = fill; colour 0; fill; colour 1 (width-1 fills);
+* hierarchy coarsen box-locally by 2 while every box extent is even and >= 8;
+  then, if several boxes remain and the domain is still coarsenable (even,
+  >= 8), agglomerate onto one box covering the coarsened domain; keep
+  coarsening that box while it is even and >= 8.  Restriction = average_down,
+  prolongation = phi_f += interp_to_fine(phi_c, 'pc');
+* cycle     V(nu1, nu2); coarse-level phi starts at 0; bottom = a fixed number
+  of GSRB sweeps; stop when ||r||_inf <= rtol * ||rhs||_inf (phi0 = 0) or
+  after max_iter cycles.
+
+Known-answer tests (tests/test_oracle_mlmg.py) pin the discretisation:
+discrete periodic eigenmodes, a dense 8^3 solve and the per-cycle
+convergence factor.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import mesh_ref as M
+
+__all__ = ["mg_levels", "level_dh", "laplacian", "gsrb_color", "OracleMLMG", "coarsenable_extent"]
+
+
+def coarsenable_extent(e):
+    return e % 2 == 0 and e >= 8
+
+
+def mg_levels(domain, boxes):
+    """[(domain, boxes, kind)] from fine to coarse; kind in base/boxlocal/agglom/single."""
+    two = tuple(2 for _ in domain[0])
+    levels = [(domain, list(boxes), "base")]
+    while all(coarsenable_extent(e) for b in boxes for e in M.ext(b)):
+        boxes = [M.coarsen_box(b, two) for b in boxes]
+        domain = M.coarsen_box(domain, two)
+        levels.append((domain, boxes, "boxlocal"))
+    if len(boxes) > 1 and all(coarsenable_extent(e) for e in M.ext(domain)):
+        domain = M.coarsen_box(domain, two)
+        boxes = [domain]
+        levels.append((domain, boxes, "agglom"))
+    while len(boxes) == 1 and all(coarsenable_extent(e) for e in M.ext(domain)):
+        domain = M.coarsen_box(domain, two)
+        boxes = [domain]
+        levels.append((domain, boxes, "single"))
+    return levels
+
+
+def level_dh(domain, prob_lo, prob_hi):
+    """1/dx^2 per axis from Geometry.cell_size = (hi - lo)/extent (amr_core.py:37-40)."""
+    out = []
+    for l, h, e in zip(prob_lo, prob_hi, M.ext(domain)):
+        cs = (h - l) / e
+        out.append(1.0 / (cs * cs))
+    return tuple(out)
+
+
+def gamma_of(dh):
+    return -2.0 * (dh[0] + dh[1] + dh[2])
+
+
+def laplacian(p, dh):
+    """L(phi) over the valid region of a ghost-1 array p of shape (n0+2, n1+2, n2+2)."""
+    c = p[1:-1, 1:-1, 1:-1]
+    c2 = 2.0 * c
+    tx = dh[0] * ((p[:-2, 1:-1, 1:-1] - c2) + p[2:, 1:-1, 1:-1])
+    ty = dh[1] * ((p[1:-1, :-2, 1:-1] - c2) + p[1:-1, 2:, 1:-1])
+    tz = dh[2] * ((p[1:-1, 1:-1, :-2] - c2) + p[1:-1, 1:-1, 2:])
+    return (tx + ty) + tz
+
+
+_masks = {}
+
+
+def color_mask(lo, shape, color):
+    key = ((lo[0] + lo[1] + lo[2] + color) & 1, shape)
+    m = _masks.get(key)
+    if m is None:
+        i, j, k = np.indices(shape, sparse=True)
+        m = ((i + j + k + key[0]) % 2) == 0
+        _masks[key] = m
+    return m
+
+
+def gsrb_color(box, p, rhs_valid, dh, color):
+    """One colour of GSRB on one box in place (p: ghost-1 array, no comp axis).
+
+    Red cells read only black neighbours, so evaluating L on all cells and
+    keeping the coloured ones equals the sequential definition."""
+    c = p[1:-1, 1:-1, 1:-1]
+    new = c + (rhs_valid - laplacian(p, dh)) / gamma_of(dh)
+    np.copyto(c, new, where=color_mask(box[0], c.shape, color))
+
+
+class OracleMLMG:
+    """CPU V-cycle solver; data per level as mesh_ref dicts (ncomp = 1)."""
+
+    def __init__(self, domain, boxes, prob_lo=(0.0, 0.0, 0.0), prob_hi=(1.0, 1.0, 1.0), nu1=2, nu2=2,
+                 bottom_sweeps=32):
+        self.periodic = (True, True, True)
+        self.nu1, self.nu2, self.bottom_sweeps = nu1, nu2, bottom_sweeps
+        self.levels = []
+        for dom, bxs, kind in mg_levels(domain, boxes):
+            self.levels.append(
+                {
+                    "domain": dom,
+                    "boxes": bxs,
+                    "kind": kind,
+                    "dh": level_dh(dom, prob_lo, prob_hi),
+                    "phi": M.make_fabs(bxs, 1, 1),
+                    "rhs": M.make_fabs(bxs, 1, 0),
+                    "fill": M.fill_records(bxs, 1, dom, self.periodic),
+                }
+            )
+        self.sweeps = 0  # GSRB sweeps performed (all levels)
+        self.cell_updates = 0
+
+    # -- primitives ------------------------------------------------------------
+    def fill(self, lv):
+        M.execute(lv["fill"], lv["boxes"], lv["phi"], 1, lv["boxes"], lv["phi"], 1)
+
+    def smooth(self, lv, n):
+        for _ in range(n):
+            for color in (0, 1):
+                self.fill(lv)
+                for i, b in enumerate(lv["boxes"]):
+                    gsrb_color(b, lv["phi"][i][0], lv["rhs"][i][0], lv["dh"], color)
+            self.sweeps += 1
+            self.cell_updates += sum(int(np.prod(M.ext(b))) for b in lv["boxes"])
+
+    def residual(self, lv):
+        self.fill(lv)
+        return {i: (lv["rhs"][i][0] - laplacian(lv["phi"][i][0], lv["dh"]))[None] for i in range(len(lv["boxes"]))}
+
+    def norm_inf(self, fabs, boxes):
+        mx = M.reduce(boxes, fabs, 0, "max", 0)
+        mn = M.reduce(boxes, fabs, 0, "min", 0)
+        return max(mx, -mn)
+
+    # -- cycle -------------------------------------------------------------------
+    def vcycle(self):
+        L = self.levels
+        two = (2, 2, 2)
+        for l in range(len(L) - 1):
+            lv, nx = L[l], L[l + 1]
+            if l > 0:
+                for f in lv["phi"].values():
+                    f[...] = 0.0
+            self.smooth(lv, self.nu1)
+            r = self.residual(lv)
+            M.average_down(lv["boxes"], r, 0, nx["boxes"], nx["rhs"], 0, two)
+        bot = L[-1]
+        for f in bot["phi"].values():
+            f[...] = 0.0
+        self.smooth(bot, self.bottom_sweeps)
+        for l in range(len(L) - 2, -1, -1):
+            lv, nx = L[l], L[l + 1]
+            M.interp_pc(lv["boxes"], lv["phi"], 1, nx["boxes"], nx["phi"], 1, two, add=True)
+            self.smooth(lv, self.nu2)
+
+    def solve(self, rhs_global, phi_global=None, rtol=1e-10, max_iter=200, max_cycles=None):
+        """Returns dict(phi, iterations, history, r0).  max_cycles bounds the work
+        (CPU-baseline samples) without the convergence test."""
+        top = self.levels[0]
+        dom = top["domain"]
+        M.load_global(top["boxes"], top["rhs"], 0, dom, np.asarray(rhs_global)[None])
+        if phi_global is None:
+            for f in top["phi"].values():
+                f[...] = 0.0
+        else:
+            M.load_global(top["boxes"], top["phi"], 1, dom, np.asarray(phi_global)[None])
+        r0 = self.norm_inf(top["rhs"], top["boxes"])
+        hist = []
+        it = 0
+        limit = max_iter if max_cycles is None else max_cycles
+        while it < limit:
+            self.vcycle()
+            it += 1
+            rn = self.norm_inf(self.residual(top), top["boxes"])
+            hist.append(rn)
+            if max_cycles is None and rn <= rtol * r0:
+                break
+        phi = M.gather(top["boxes"], top["phi"], 1, dom)
+        return {"phi": phi, "iterations": it, "history": hist, "r0": r0}

@@ -1,0 +1,145 @@
+"""ctypes binding of libamrb.so (include/amrb.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or ``make -C
+paper_2009_12009_b200/csrc``).  There is no fallback: if the shared object is
+missing, every device operation raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+__all__ = ["lib", "check", "LIB_PATH", "AmrbError", "ptr", "i32p", "i64p", "u8p", "f64p"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libamrb.so")
+
+AMRB_OK, AMRB_EINVAL, AMRB_ECUDA, AMRB_ENCCL, AMRB_ENOMEM = 0, -1, -2, -3, -4
+FABTAB_W = 8
+REC_W = 11
+
+
+class AmrbError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+vp = C.c_void_p
+i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
+P = C.POINTER
+
+_SIGS = {
+    "amrb_last_error": (C.c_char_p, []),
+    "amrb_version": (C.c_int, []),
+    "amrb_plan_fill_create": (C.c_int, [C.c_int, C.c_int, P(i32), C.c_int, P(i32), P(C.c_uint8), P(vp)]),
+    "amrb_plan_copy_create": (
+        C.c_int,
+        [C.c_int, C.c_int, P(i32), C.c_int, P(i32), C.c_int, P(i32), P(C.c_uint8), P(vp)],
+    ),
+    "amrb_plan_sum_create": (C.c_int, [C.c_int, C.c_int, P(i32), C.c_int, P(i32), P(C.c_uint8), P(vp)]),
+    "amrb_plan_size": (C.c_int, [vp, P(i64), P(i64)]),
+    "amrb_plan_records": (C.c_int, [vp, P(i32)]),
+    "amrb_plan_destroy": (C.c_int, [vp]),
+    "amrb_prog_create": (
+        C.c_int,
+        [vp, C.c_int, P(i64), C.c_int, P(i32), P(i64), C.c_int, P(i32), C.c_int, C.c_int, C.c_int, C.c_int, P(vp)],
+    ),
+    "amrb_prog_info": (C.c_int, [vp, P(i64), P(i64), P(i64), P(i64)]),
+    "amrb_prog_pairs": (C.c_int, [vp, P(i64)]),
+    "amrb_prog_run": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "amrb_prog_destroy": (C.c_int, [vp]),
+    "amrb_level_create": (C.c_int, [C.c_int, P(i32), P(C.c_uint8), P(vp)]),
+    "amrb_level_destroy": (C.c_int, [vp]),
+    "amrb_field_create": (C.c_int, [vp, P(i64), C.c_int, P(vp)]),
+    "amrb_field_destroy": (C.c_int, [vp]),
+    "amrb_lap_apply": (C.c_int, [vp, vp, vp, vp, vp, P(f64), vp]),
+    "amrb_residual": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
+    "amrb_gsrb_color": (C.c_int, [vp, vp, vp, vp, vp, P(f64), C.c_int, vp]),
+    "amrb_gsrb_sweep": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp]),
+    "amrb_restrict": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
+    "amrb_residual_restrict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
+    "amrb_prolong": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
+    "amrb_reduce": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
+    "amrb_domain_bc": (C.c_int, [vp, vp, vp, C.c_int, P(i32), P(i32), f64, vp]),
+    "amrb_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
+    "amrb_nccl_comm_create": (C.c_int, [P(C.c_uint8), C.c_int, C.c_int, P(vp)]),
+    "amrb_nccl_comm_destroy": (C.c_int, [vp]),
+    "amrb_nccl_allreduce": (C.c_int, [vp, i64, C.c_int, vp, vp]),
+    "amrb_nccl_allgather": (C.c_int, [vp, vp, i64, vp, vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """The loaded library; raises if it was never built (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"libamrb.so not built ({LIB_PATH}); run __graft_entry__.build() "
+                        "or `make -C paper_2009_12009_b200/csrc` -- there is no CPU fallback"
+                    )
+                handle = C.CDLL(LIB_PATH)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(handle, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = handle
+    return _lib
+
+
+def check(status, *, src=None, dst=None):
+    """Map a status code to the reference's exception types."""
+    if status == AMRB_OK:
+        return
+    msg = lib().amrb_last_error().decode(errors="replace")
+    if status == AMRB_EINVAL:
+        raise ValueError(msg)
+    if status == AMRB_ENCCL:
+        from .comm import TransportError
+
+        raise TransportError(src if src is not None else -1, dst if dst is not None else -1, msg)
+    raise AmrbError(status, msg)
+
+
+def ptr(x):
+    """Raw address of a torch tensor / numpy array (None -> NULL)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def _np_ptr(a, ctype):
+    return a.ctypes.data_as(P(ctype))
+
+
+def i32p(a):
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a, _np_ptr(a, i32)
+
+
+def i64p(a):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a, _np_ptr(a, i64)
+
+
+def u8p(a):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    return a, _np_ptr(a, C.c_uint8)
+
+
+def f64p(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, _np_ptr(a, f64)

@@ -1,0 +1,313 @@
+"""Ghost exchange, inter-layout copy, boundary folding and reductions.
+
+Drop-in for the reference's FabArray communication API
+(/root/reference/pkg/src/amrkit/fabarray.py:364-455) and its Transport
+(transport.py:20-58):
+
+    fill_boundary(fa, transport, domain, periodic=None)      fabarray.py:364
+    parallel_copy(dst, src, transport, domain=None, periodic=None)  :377
+    sum_boundary(fa, transport, domain, periodic=None)       :391
+    reduce(fa, kind, comp, transport)                        :409
+    gather_global(fa, region, comp=0, default=0.0)           :443
+
+Execution is a libamrb copy program (csrc/comm.cu) running on the current
+torch CUDA stream: one kernel launch for all local records, pack/unpack
+kernels around one message per ordered rank pair for remote ones.  A
+``Transport(nranks)`` simulates ranks inside one process exactly like the
+reference (all boxes on one GPU, messages counted); ``Transport.distributed()``
+is the real thing -- one process per GPU, messages are NCCL send/recv.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import deque
+
+import numpy as np
+import torch
+
+from . import counters
+from ._native import check, i32p, i64p, lib, ptr
+from .boxes import box_diff
+from .device import field_of, level_of, stream_ptr
+from .plans import (
+    build_plan_copy,
+    build_plan_copy_grown,
+    build_plan_fill_boundary,
+    build_plan_sum_boundary,
+)
+
+__all__ = [
+    "Transport",
+    "TransportError",
+    "fill_boundary",
+    "parallel_copy",
+    "sum_boundary",
+    "reduce",
+    "gather_global",
+    "copy_into",
+]
+
+
+class TransportError(RuntimeError):
+    def __init__(self, src, dst, why):
+        super().__init__(f"transport failure {src} -> {dst}: {why}")
+        self.src = src
+        self.dst = dst
+
+
+class Transport:
+    """Message layer between ranks.
+
+    ``Transport(nranks)``: the reference's simulated ranks (transport.py:27-58)
+    -- every rank lives in this process; device messages are segments of one
+    staging buffer on the GPU; host messages use FIFO mailboxes.
+    ``Transport.distributed()``: one process per GPU under torch.distributed;
+    device messages travel by NCCL send/recv over NVLink.
+    """
+
+    def __init__(self, nranks):
+        nranks = int(nranks)
+        if nranks < 1:
+            raise ValueError("nranks must be >= 1")
+        self.nranks = nranks
+        self.rank = 0
+        self.mode = "sim"
+        self.nccl_comm = None
+        self._queues = {}
+
+    @classmethod
+    def distributed(cls):
+        import torch.distributed as dist
+
+        if not (dist.is_available() and dist.is_initialized()):
+            raise ValueError("Transport.distributed() needs torch.distributed to be initialised")
+        t = cls(dist.get_world_size())
+        t.rank = dist.get_rank()
+        t.mode = "nccl"
+        uid = (C.c_uint8 * 128)()
+        if t.rank == 0:
+            check(lib().amrb_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        comm = C.c_void_p()
+        check(lib().amrb_nccl_comm_create(uid, t.nranks, t.rank, C.byref(comm)), src=t.rank, dst=-1)
+        t.nccl_comm = comm
+        return t
+
+    def close(self):
+        if self.nccl_comm is not None and self.nccl_comm.value:
+            check(lib().amrb_nccl_comm_destroy(self.nccl_comm))
+            self.nccl_comm = None
+
+    # -- host message API (reference-compatible) -------------------------------
+    def send(self, src, dst, tag, payload):
+        if not (0 <= src < self.nranks and 0 <= dst < self.nranks):
+            raise TransportError(src, dst, "rank out of range")
+        self._queues.setdefault((src, dst), deque()).append((tag, payload))
+        self.account(src, dst, int(getattr(payload, "nbytes", len(payload))))
+
+    def drain(self, dst):
+        out = []
+        for src in range(self.nranks):
+            q = self._queues.get((src, dst))
+            while q:
+                tag, payload = q.popleft()
+                out.append((src, tag, payload))
+        return out
+
+    def pending(self):
+        return sum(len(q) for q in self._queues.values())
+
+    def account(self, src, dst, nbytes):
+        counters.incr("transport_messages")
+        counters.incr("transport_bytes", int(nbytes))
+
+
+class _Program:
+    """A plan bound to (src storage, dst storage, transport mode)."""
+
+    def __init__(self, plan, src_fa, dst_fa, transport, op):
+        self.plan = plan  # keep the native plan alive
+        sim = transport.mode == "sim"
+        mode = {"nccl": 0, "sim": 1, "local": 2}[transport.mode]
+        ncomp = src_fa.ncomp
+        st, stp = i64p(src_fa.fabtab)
+        dt, dtp = i64p(dst_fa.fabtab)
+        so, sop = i32p(src_fa.owners())
+        do, dop = i32p(dst_fa.owners())
+        h = C.c_void_p()
+        check(
+            lib().amrb_prog_create(
+                plan.handle,
+                ncomp,
+                stp,
+                len(src_fa.ba),
+                sop,
+                dtp,
+                len(dst_fa.ba),
+                dop,
+                transport.nranks,
+                transport.rank,
+                mode,
+                op,
+                C.byref(h),
+            )
+        )
+        self.handle = h
+        send = C.c_int64()
+        recv = C.c_int64()
+        npairs = C.c_int64()
+        nlocal = C.c_int64()
+        check(lib().amrb_prog_info(h, C.byref(send), C.byref(recv), C.byref(npairs), C.byref(nlocal)))
+        pairs = np.zeros((npairs.value, 4), dtype=np.int64)
+        if npairs.value:
+            check(lib().amrb_prog_pairs(h, pairs.ctypes.data_as(C.POINTER(C.c_int64))))
+        self.pairs = pairs
+        dev = dst_fa.device
+        self.sendbuf = torch.empty(max(send.value, 1), dtype=torch.float64, device=dev) if send.value else None
+        self.recvbuf = (
+            torch.empty(max(recv.value, 1), dtype=torch.float64, device=dev) if (recv.value and not sim) else None
+        )
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                lib().amrb_prog_destroy(h)
+            except Exception:
+                pass
+
+    def run(self, src_fa, dst_fa, transport):
+        comm = transport.nccl_comm if transport.mode == "nccl" else None
+        if transport.mode == "local":
+            comm = None
+        check(
+            lib().amrb_prog_run(
+                self.handle,
+                C.c_void_p(src_fa.storage.data_ptr()),
+                C.c_void_p(dst_fa.storage.data_ptr()),
+                C.c_void_p(ptr(self.sendbuf)),
+                C.c_void_p(ptr(self.recvbuf)),
+                comm,
+                stream_ptr(),
+            ),
+            src=transport.rank,
+        )
+        for s, d, _off, cnt in self.pairs.tolist():
+            transport.account(s, d, 8 * cnt)
+
+
+def _execute(plan, src_fa, dst_fa, transport, op):
+    nranks = transport.nranks
+    if src_fa.dm.nranks != nranks or dst_fa.dm.nranks != nranks:
+        raise ValueError("transport rank count differs from the distribution maps")
+    src_fa.require_cuda("copy")
+    dst_fa.require_cuda("copy")
+    key = (id(plan), src_fa.serial, op, transport.mode, nranks)
+    prog = dst_fa._progs.get(key)
+    if prog is None:
+        prog = _Program(plan, src_fa, dst_fa, transport, op)
+        dst_fa._progs[key] = prog
+    prog.run(src_fa, dst_fa, transport)
+
+
+def fill_boundary(fa, transport, domain, periodic=None, ngrow=None):
+    """Fill every in-domain (or periodic-image) ghost cell from the valid cell it
+    shadows; out-of-domain non-periodic ghosts are untouched (fabarray.py:364).
+
+    ``ngrow`` (<= fa.ngrow) limits the exchange to the first ``ngrow`` ghost
+    layers (AMReX FillBoundary(nghost)); default is all of them.
+    """
+    ng = fa.ngrow if ngrow is None else int(ngrow)
+    if ng > fa.ngrow:
+        raise ValueError("fill width exceeds the FabArray's ghost width")
+    if ng == 0:
+        return
+    plan = build_plan_fill_boundary(fa.ba, ng, domain, periodic)
+    _execute(plan, fa, fa, transport, 0)
+
+
+def parallel_copy(dst_fa, src_fa, transport, domain=None, periodic=None):
+    """Copy src valid data onto dst valid cells wherever layouts overlap (:377)."""
+    if dst_fa.ncomp != src_fa.ncomp:
+        raise ValueError(f"component count mismatch: dst {dst_fa.ncomp} vs src {src_fa.ncomp}")
+    plan = build_plan_copy(dst_fa.ba, src_fa.ba, domain, periodic)
+    _execute(plan, src_fa, dst_fa, transport, 0)
+
+
+def copy_into(dst_fa, src_fa, transport, include_dst_ghosts=False, domain=None, periodic=None):
+    """parallel_copy that may also write dst ghost cells (coarse_fine.py:188-198)."""
+    if dst_fa.ncomp != src_fa.ncomp:
+        raise ValueError("component count mismatch")
+    ng = dst_fa.ngrow if include_dst_ghosts else 0
+    plan = build_plan_copy_grown(dst_fa.ba, src_fa.ba, ng, domain, periodic)
+    _execute(plan, src_fa, dst_fa, transport, 0)
+
+
+def sum_boundary(fa, transport, domain, periodic=None):
+    """Fold every ghost copy back onto its valid cell, in plan order, then zero
+    the ghosts (fabarray.py:391-406)."""
+    if fa.ngrow == 0:
+        return
+    plan = build_plan_sum_boundary(fa.ba, fa.ngrow, domain, periodic)
+    _execute(plan, fa, fa, transport, 1)
+    for f in fa.fabs.values():
+        for piece in box_diff(f.gbox, f.box):
+            f.slice(piece).zero_()
+
+
+_KINDS = {"sum": 0, "min": 1, "max": 2, "absmax": 3}
+
+
+def device_reduce(fa, kind, comp=0, out=None):
+    """Reduce over resident valid cells on this device into a 1-element tensor
+    (no host sync).  kind in sum/min/max/absmax."""
+    fa.require_cuda("reduce")
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=fa.device)
+    lv = level_of(fa)
+    f = field_of(fa)
+    check(
+        lib().amrb_reduce(
+            lv.handle, f.handle, C.c_void_p(fa.storage.data_ptr()), comp, _KINDS[kind], C.c_void_p(out.data_ptr()),
+            stream_ptr(),
+        )
+    )
+    return out
+
+
+def reduce(fa, kind, comp, transport):
+    """Reduce one component over valid cells and combine across ranks (:409)."""
+    if kind not in ("sum", "min", "max"):
+        raise ValueError(f"unknown reduction {kind!r}")
+    if not 0 <= comp < fa.ncomp:
+        raise ValueError("component out of range")
+    out = device_reduce(fa, kind, comp)
+    if transport.mode == "nccl":
+        check(
+            lib().amrb_nccl_allreduce(
+                C.c_void_p(out.data_ptr()), 1, _KINDS[kind], transport.nccl_comm, stream_ptr()
+            ),
+            src=transport.rank,
+        )
+        if transport.rank != 0:
+            transport.account(transport.rank, 0, 8)
+    else:
+        # partials of ranks 1..R-1 travel to rank 0 in the reference
+        for r in range(1, transport.nranks):
+            transport.account(r, 0, 8)
+    return float(out.item())
+
+
+def gather_global(fa, region, comp=0, default=0.0):
+    """Dense numpy array over region from resident valid data (diagnostics)."""
+    out = np.full(tuple(region.extents()), default, dtype=np.float64)
+    for i, f in fa.fabs.items():
+        ov = fa.ba[i].intersect(region)
+        if ov.is_empty():
+            continue
+        idx = tuple(slice(ov.lo[d] - region.lo[d], ov.hi[d] - region.lo[d] + 1) for d in range(fa.dim))
+        out[idx] = f.slice(ov, comp).cpu().numpy()
+    return out

@@ -1,0 +1,444 @@
+// Copy programs: a CommPlan bound to concrete device storage, plus the NCCL
+// plumbing.  Replaces the reference's two-phase executor
+// (/root/reference/pkg/src/amrkit/fabarray.py:326-361) and its in-process
+// Transport (transport.py:27-58).
+//
+// Execution of one program:
+//   1. pack   : records whose source is here and destination is remote are
+//               gathered into the send buffer, one contiguous segment per
+//               destination rank (C-order (ncomp, e0, e1, e2) record slices in
+//               plan order -- byte-identical to the reference's message).
+//   2. NCCL   : one ncclSend / ncclRecv per ordered peer pair inside a group.
+//   3. apply  : records whose destination is here, in waves.  Copy programs
+//               have two waves (local records, then records fed from the
+//               receive buffer); add programs (sum_boundary) put records that
+//               touch the same cells in successive waves so every cell sees its
+//               contributions in plan order, which keeps sums bit-identical to
+//               the reference for any rank count.
+//
+// The kernel walks a flat index space over all records of a wave: each CTA
+// covers CHUNK consecutive cells, knows the first record of its chunk, and
+// binary-searches the record prefix for each cell.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "device.h"
+
+namespace amrb {
+
+namespace {
+
+constexpr int kCopyThreads = 256;
+constexpr int kCopyItems = 4;
+constexpr int kChunk = kCopyThreads * kCopyItems;
+
+struct DevRec {
+  int64_t src;    // element offset of the first source cell (comp 0)
+  int64_t dst;    // element offset of the first destination cell (comp 0)
+  int64_t begin;  // first flat index of this record in its wave
+  int64_t ss0, ss1, scs;
+  int64_t ds0, ds1, dcs;
+  int32_t e0, e1, e2;
+  int32_t from_buf;  // 1: source is the receive/staging buffer
+};
+
+struct Wave {
+  std::vector<DevRec> host;
+  std::vector<int32_t> chunk_first;
+  DevArray<DevRec> recs;
+  DevArray<int32_t> first;
+  int64_t total = 0;
+  void finish(int ncomp) {
+    total = 0;
+    for (auto& r : host) {
+      r.begin = total;
+      total += (int64_t)r.e0 * r.e1 * r.e2 * ncomp;
+    }
+  }
+};
+
+template <bool kAdd>
+__global__ void __launch_bounds__(kCopyThreads)
+    k_copy(const DevRec* __restrict__ recs, const int32_t* __restrict__ first, int64_t total,
+           int ncomp, const double* __restrict__ src, const double* __restrict__ buf,
+           double* __restrict__ dst) {
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int rlo0 = first[blockIdx.x];
+  const int rhi0 = first[blockIdx.x + 1];
+#pragma unroll
+  for (int u = 0; u < kCopyItems; ++u) {
+    const int64_t f = base + u * kCopyThreads + threadIdx.x;
+    if (f >= total) return;
+    int lo = rlo0, hi = rhi0;
+    while (lo < hi) {  // last record with begin <= f
+      int mid = (lo + hi + 1) >> 1;
+      if (recs[mid].begin <= f)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const DevRec& r = recs[lo];
+    const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
+    int64_t loc = f - r.begin;  // in [0, ncomp * cells)
+    const int c = (int)(loc / cells);
+    int t = (int)(loc - (int64_t)c * cells);
+    const int k = t % r.e2;
+    t /= r.e2;
+    const int j = t % r.e1;
+    const int i = t / r.e1;
+    const double* s = r.from_buf ? buf : src;
+    const double v = s[r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k];
+    double* d = dst + r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
+    if (kAdd)
+      *d = *d + v;
+    else
+      *d = v;
+  }
+}
+
+struct Peer {
+  int rank;
+  int64_t off, count;  // elements
+};
+
+}  // namespace
+
+struct Prog {
+  int ncomp = 1;
+  int op = 0;
+  int sim = 1;
+  int my_rank = 0;
+  Wave pack;                // source fab -> send buffer
+  std::vector<Wave*> apply;  // destination fab <- source fab / receive buffer
+  int local_waves = 0;      // copy programs: apply[0] is local-only
+  std::vector<Peer> sends, recvs;
+  int64_t send_elems = 0, recv_elems = 0;
+  std::vector<int64_t> pair_table;  // src, dst, off, count
+  int64_t local_records = 0;
+  ~Prog() {
+    for (auto* w : apply) delete w;
+  }
+};
+
+namespace {
+
+struct Tab {
+  const int64_t* t;
+  int64_t at(int box, int w) const { return t[(int64_t)box * AMRB_FABTAB_W + w]; }
+};
+
+// Element offset of cell `lo` (3-D) in box `b` of a fab table, comp 0.
+int64_t cell_offset(const Tab& tab, int b, const int lo[3]) {
+  return tab.at(b, 0) + (lo[0] - tab.at(b, 4)) * tab.at(b, 2) + (lo[1] - tab.at(b, 5)) * tab.at(b, 3) +
+         (lo[2] - tab.at(b, 6));
+}
+
+void prepare_wave(Wave& w, int ncomp) {
+  w.finish(ncomp);
+  int64_t nchunks = (w.total + kChunk - 1) / kChunk;
+  w.chunk_first.assign((size_t)nchunks + 1, 0);
+  size_t r = 0;
+  for (int64_t c = 0; c <= nchunks; ++c) {
+    int64_t f = std::min<int64_t>(c * kChunk, std::max<int64_t>(w.total - 1, 0));
+    while (r + 1 < w.host.size() && w.host[r + 1].begin <= f) ++r;
+    w.chunk_first[(size_t)c] = (int32_t)r;
+  }
+  w.recs.upload(w.host);
+  w.first.upload(w.chunk_first);
+}
+
+void run_wave(const Wave& w, int ncomp, bool add, const double* src, const double* buf, double* dst,
+              cudaStream_t st) {
+  if (w.total == 0) return;
+  int64_t nchunks = (w.total + kChunk - 1) / kChunk;
+  if (add)
+    k_copy<true><<<(unsigned)nchunks, kCopyThreads, 0, st>>>(w.recs.p, w.first.p, w.total, ncomp, src,
+                                                             buf, dst);
+  else
+    k_copy<false><<<(unsigned)nchunks, kCopyThreads, 0, st>>>(w.recs.p, w.first.p, w.total, ncomp, src,
+                                                              buf, dst);
+  check_launch("k_copy");
+}
+
+bool overlaps(const Record& a, const Record& b) {
+  for (int x = 0; x < 3; ++x) {
+    int alo = a.lo[x] + a.shift[x], ahi = a.hi[x] + a.shift[x];
+    int blo = b.lo[x] + b.shift[x], bhi = b.hi[x] + b.shift[x];
+    if (ahi < blo || bhi < alo) return false;
+  }
+  return true;
+}
+
+}  // namespace
+}  // namespace amrb
+
+using amrb::Error;
+
+extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t* src_fabtab, int nsrc,
+                                const int32_t* src_owner, const int64_t* dst_fabtab, int ndst,
+                                const int32_t* dst_owner, int nranks, int my_rank, int mode, int op,
+                                amrb_prog** out) {
+  return amrb::guarded([&] {
+    using namespace amrb;
+    if (!plan_ || !out || ncomp < 1 || nranks < 1 || my_rank < 0 || my_rank >= nranks || (op != 0 && op != 1) ||
+        mode < 0 || mode > 2)
+      throw Error(AMRB_EINVAL, "amrb_prog_create: bad arguments");
+    const int sim_ranks = mode == 1;
+    const bool local_only = mode == 2;
+    const Plan& plan = *reinterpret_cast<const Plan*>(plan_);
+    Tab st{src_fabtab}, dt{dst_fabtab};
+    auto* g = new Prog;
+    std::unique_ptr<Prog> guard(g);
+    g->ncomp = ncomp;
+    g->op = op;
+    g->sim = sim_ranks;
+    g->my_rank = my_rank;
+
+    const auto& recs = plan.recs;
+    const int64_t n = (int64_t)recs.size();
+    std::vector<int> sr(n), dr(n);
+    for (int64_t r = 0; r < n; ++r) {
+      if (recs[r].src < 0 || recs[r].src >= nsrc || recs[r].dst < 0 || recs[r].dst >= ndst)
+        throw Error(AMRB_EINVAL, "plan record box index out of range for the given layouts");
+      sr[r] = src_owner ? src_owner[recs[r].src] : 0;
+      dr[r] = dst_owner ? dst_owner[recs[r].dst] : 0;
+      if (sr[r] < 0 || sr[r] >= nranks || dr[r] < 0 || dr[r] >= nranks)
+        throw Error(AMRB_EINVAL, "owner rank out of range");
+      if (local_only && !(sr[r] == my_rank && dr[r] == my_rank)) sr[r] = dr[r] = -1;  // dropped
+    }
+    // ---- message segments: ordered (src, dst) pairs, plan order inside ------
+    // buffer offset of each remote record (elements)
+    std::vector<int64_t> buf_off(n, -1);
+    {
+      std::map<std::pair<int, int>, std::vector<int64_t>> pairs;
+      for (int64_t r = 0; r < n; ++r)
+        if (sr[r] >= 0 && sr[r] != dr[r] && (sim_ranks || sr[r] == my_rank || dr[r] == my_rank))
+          pairs[{sr[r], dr[r]}].push_back(r);
+      // sim: one staging buffer holding every pair; dist: separate send/recv
+      int64_t soff = 0, roff = 0;
+      for (auto& kv : pairs) {
+        int s = kv.first.first, d = kv.first.second;
+        int64_t cnt = 0;
+        for (int64_t r : kv.second) cnt += recs[r].cells() * ncomp;
+        if (sim_ranks) {
+          int64_t o = soff;
+          for (int64_t r : kv.second) {
+            buf_off[r] = o;
+            o += recs[r].cells() * ncomp;
+          }
+          g->pair_table.insert(g->pair_table.end(), {s, d, soff, cnt});
+          soff += cnt;
+        } else if (s == my_rank) {
+          int64_t o = soff;
+          for (int64_t r : kv.second) {
+            buf_off[r] = o;
+            o += recs[r].cells() * ncomp;
+          }
+          g->sends.push_back({d, soff, cnt});
+          g->pair_table.insert(g->pair_table.end(), {s, d, soff, cnt});
+          soff += cnt;
+        } else {  // d == my_rank
+          int64_t o = roff;
+          for (int64_t r : kv.second) {
+            buf_off[r] = o;
+            o += recs[r].cells() * ncomp;
+          }
+          g->recvs.push_back({s, roff, cnt});
+          roff += cnt;
+        }
+      }
+      g->send_elems = soff;
+      g->recv_elems = sim_ranks ? soff : roff;
+    }
+    auto fab_side = [&](const Tab& t, int box, const int lo[3], int64_t& off, int64_t& s0, int64_t& s1,
+                        int64_t& cs) {
+      if (!t.at(box, 7)) throw Error(AMRB_EINVAL, "record touches a box that is not resident here");
+      off = cell_offset(t, box, lo);
+      s0 = t.at(box, 2);
+      s1 = t.at(box, 3);
+      cs = t.at(box, 1);
+    };
+    auto buf_side = [&](int64_t r, int64_t& off, int64_t& s0, int64_t& s1, int64_t& cs) {
+      const Record& q = recs[r];
+      int e1 = q.hi[1] - q.lo[1] + 1, e2 = q.hi[2] - q.lo[2] + 1;
+      off = buf_off[r];
+      s1 = e2;
+      s0 = (int64_t)e1 * e2;
+      cs = q.cells();
+    };
+    // ---- pack ---------------------------------------------------------------
+    for (int64_t r = 0; r < n; ++r) {
+      if (sr[r] == dr[r] || buf_off[r] < 0) continue;
+      if (!sim_ranks && sr[r] != my_rank) continue;
+      const Record& q = recs[r];
+      DevRec d{};
+      d.e0 = q.hi[0] - q.lo[0] + 1;
+      d.e1 = q.hi[1] - q.lo[1] + 1;
+      d.e2 = q.hi[2] - q.lo[2] + 1;
+      fab_side(st, q.src, q.lo, d.src, d.ss0, d.ss1, d.scs);
+      buf_side(r, d.dst, d.ds0, d.ds1, d.dcs);
+      g->pack.host.push_back(d);
+    }
+    // ---- apply ---------------------------------------------------------------
+    std::vector<int64_t> mine;
+    for (int64_t r = 0; r < n; ++r)
+      if (sr[r] >= 0 && (sim_ranks || dr[r] == my_rank)) mine.push_back(r);
+    auto make_apply = [&](int64_t r) {
+      const Record& q = recs[r];
+      DevRec d{};
+      d.e0 = q.hi[0] - q.lo[0] + 1;
+      d.e1 = q.hi[1] - q.lo[1] + 1;
+      d.e2 = q.hi[2] - q.lo[2] + 1;
+      int dlo[3] = {q.lo[0] + q.shift[0], q.lo[1] + q.shift[1], q.lo[2] + q.shift[2]};
+      fab_side(dt, q.dst, dlo, d.dst, d.ds0, d.ds1, d.dcs);
+      if (sr[r] == dr[r]) {
+        fab_side(st, q.src, q.lo, d.src, d.ss0, d.ss1, d.scs);
+        d.from_buf = 0;
+      } else {
+        buf_side(r, d.src, d.ss0, d.ss1, d.scs);
+        d.from_buf = 1;
+      }
+      return d;
+    };
+    if (op == 0) {
+      auto* local = new Wave;
+      auto* remote = new Wave;
+      g->apply.push_back(local);
+      g->apply.push_back(remote);
+      for (int64_t r : mine) {
+        (sr[r] == dr[r] ? local : remote)->host.push_back(make_apply(r));
+        if (sr[r] == dr[r]) g->local_records++;
+      }
+      g->local_waves = 1;
+    } else {
+      // wave(r) = 1 + max wave of earlier records into the same box that overlap
+      std::map<int, std::vector<std::pair<int64_t, int>>> by_dst;
+      int nw = 0;
+      std::vector<int> wave_of(mine.size());
+      for (size_t m = 0; m < mine.size(); ++m) {
+        int64_t r = mine[m];
+        int w = 0;
+        for (auto& pr : by_dst[recs[r].dst])
+          if (overlaps(recs[pr.first], recs[r])) w = std::max(w, pr.second + 1);
+        by_dst[recs[r].dst].push_back({r, w});
+        wave_of[m] = w;
+        nw = std::max(nw, w + 1);
+        if (sr[r] == dr[r]) g->local_records++;
+      }
+      for (int w = 0; w < nw; ++w) g->apply.push_back(new Wave);
+      for (size_t m = 0; m < mine.size(); ++m) g->apply[wave_of[m]]->host.push_back(make_apply(mine[m]));
+      g->local_waves = 0;
+    }
+    prepare_wave(g->pack, ncomp);
+    for (auto* w : g->apply) prepare_wave(*w, ncomp);
+    *out = reinterpret_cast<amrb_prog*>(guard.release());
+  });
+}
+
+extern "C" int amrb_prog_info(const amrb_prog* g_, int64_t* send_elems, int64_t* recv_elems, int64_t* npairs,
+                              int64_t* local_records) {
+  return amrb::guarded([&] {
+    if (!g_) throw Error(AMRB_EINVAL, "null program");
+    auto* g = reinterpret_cast<const amrb::Prog*>(g_);
+    if (send_elems) *send_elems = g->send_elems;
+    if (recv_elems) *recv_elems = g->recv_elems;
+    if (npairs) *npairs = (int64_t)g->pair_table.size() / 4;
+    if (local_records) *local_records = g->local_records;
+  });
+}
+
+extern "C" int amrb_prog_pairs(const amrb_prog* g_, int64_t* out) {
+  return amrb::guarded([&] {
+    if (!g_ || !out) throw Error(AMRB_EINVAL, "null argument");
+    auto* g = reinterpret_cast<const amrb::Prog*>(g_);
+    std::memcpy(out, g->pair_table.data(), g->pair_table.size() * sizeof(int64_t));
+  });
+}
+
+extern "C" int amrb_prog_run(amrb_prog* g_, const double* src_base, double* dst_base, double* sendbuf,
+                             double* recvbuf, void* nccl_comm, void* stream) {
+  return amrb::guarded([&] {
+    using namespace amrb;
+    if (!g_) throw Error(AMRB_EINVAL, "null program");
+    auto* g = reinterpret_cast<Prog*>(g_);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if ((g->send_elems && !sendbuf) || (g->recv_elems && !g->sim && !recvbuf))
+      throw Error(AMRB_EINVAL, "missing staging buffer");
+    const double* rbuf = g->sim ? sendbuf : recvbuf;
+    run_wave(g->pack, g->ncomp, false, src_base, nullptr, sendbuf, st);
+    if (!g->sim && (!g->sends.empty() || !g->recvs.empty())) {
+      if (!nccl_comm) throw Error(AMRB_ENCCL, "remote records but no NCCL communicator");
+      ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+      auto nc = [](ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw Error(AMRB_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+      };
+      nc(ncclGroupStart(), "ncclGroupStart");
+      for (const auto& p : g->sends)
+        nc(ncclSend(sendbuf + p.off, (size_t)p.count, ncclFloat64, p.rank, comm, st), "ncclSend");
+      for (const auto& p : g->recvs)
+        nc(ncclRecv(recvbuf + p.off, (size_t)p.count, ncclFloat64, p.rank, comm, st), "ncclRecv");
+      nc(ncclGroupEnd(), "ncclGroupEnd");
+    }
+    for (auto* w : g->apply) run_wave(*w, g->ncomp, g->op == 1, src_base, rbuf, dst_base, st);
+  });
+}
+
+extern "C" int amrb_prog_destroy(amrb_prog* g) {
+  delete reinterpret_cast<amrb::Prog*>(g);
+  return AMRB_OK;
+}
+
+// ----------------------------------------------------------------------------
+// NCCL plumbing
+// ----------------------------------------------------------------------------
+namespace {
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(AMRB_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+}  // namespace
+
+extern "C" int amrb_nccl_unique_id(uint8_t* out128) {
+  return amrb::guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, 128);
+  });
+}
+
+extern "C" int amrb_nccl_comm_create(const uint8_t* id128, int nranks, int rank, void** comm) {
+  return amrb::guarded([&] {
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    ncclComm_t c;
+    nccl_check(ncclCommInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+    *comm = c;
+  });
+}
+
+extern "C" int amrb_nccl_comm_destroy(void* comm) {
+  return amrb::guarded([&] {
+    if (comm) nccl_check(ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+  });
+}
+
+extern "C" int amrb_nccl_allreduce(double* buf, int64_t n, int op, void* comm, void* stream) {
+  return amrb::guarded([&] {
+    ncclRedOp_t o = op == 0 ? ncclSum : op == 1 ? ncclMin : ncclMax;
+    nccl_check(ncclAllReduce(buf, buf, (size_t)n, ncclFloat64, o, reinterpret_cast<ncclComm_t>(comm),
+                             reinterpret_cast<cudaStream_t>(stream)),
+               "ncclAllReduce");
+  });
+}
+
+extern "C" int amrb_nccl_allgather(const double* send, double* recv, int64_t n, void* comm, void* stream) {
+  return amrb::guarded([&] {
+    nccl_check(ncclAllGather(send, recv, (size_t)n, ncclFloat64, reinterpret_cast<ncclComm_t>(comm),
+                             reinterpret_cast<cudaStream_t>(stream)),
+               "ncclAllGather");
+  });
+}

@@ -1,0 +1,97 @@
+// Device-side descriptors shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "amrb_internal.h"
+
+namespace amrb {
+
+#define AMRB_CUDA(call)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      throw ::amrb::Error(AMRB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(AMRB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Valid box of one grid, 3-D padded, global index space.
+struct BoxGeom {
+  int lo[3];
+  int n[3];
+};
+
+// Storage of one box of one FabArray: element offset of the VALID lo cell
+// (comp 0) and strides.  Axis-2 stride is 1.
+struct FabView {
+  int64_t off;
+  int64_t s0, s1, cs;
+};
+
+// Unique device allocation helper.
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  ~DevArray() {
+    if (p) cudaFree(p);
+  }
+  void upload(const std::vector<T>& h) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = h.size();
+    if (n == 0) return;
+    AMRB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    AMRB_CUDA(cudaMemcpy(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (n) AMRB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  }
+};
+
+// Tiles of the valid region: (box, i0, j0, k0) in box-local valid coords.
+struct TileTable {
+  int ti, tj, tk;
+  std::vector<int4> host;
+  DevArray<int4> dev;
+};
+
+struct Level {
+  int nboxes = 0;
+  std::vector<BoxGeom> geo;
+  std::vector<uint8_t> resident;
+  DevArray<BoxGeom> dgeo;
+  std::map<std::tuple<int, int, int>, TileTable*> tables;
+  DevArray<double> partials;  // reduction scratch
+  ~Level() {
+    for (auto& kv : tables) delete kv.second;
+  }
+  const TileTable& tiles(int ti, int tj, int tk);
+  bool all_even() const;
+};
+
+struct Field {
+  const Level* lv = nullptr;
+  int ngrow = 0;
+  int ng3[3] = {0, 0, 0};  // ghost width per 3-D axis (0 on padding axes)
+  std::vector<FabView> host;
+  DevArray<FabView> dev;
+};
+
+}  // namespace amrb

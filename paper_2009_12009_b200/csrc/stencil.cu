@@ -1,0 +1,826 @@
+// Box-loop kernels of the MLMG hot path (sm_100a, fp64, HBM-bound).
+//
+// The reference runs these as Python loops over boxes with numpy slicing
+// (advect.py:143-178 is its ParallelFor pattern; average_down coarse_fine.py:
+// 136-163; interp_to_fine "pc" :166-185; reduce fabarray.py:409-440).  The
+// Laplacian / GSRB / residual have no reference code; their definitions are
+// the oracle's (oracle/mlmg_ref.py) and every kernel reproduces its operand
+// order exactly (the library is compiled with --fmad=false), so results are
+// bit-identical, not merely within tolerance.
+//
+// Work decomposition: a level's valid region is cut into tiles
+// (box, i0, j0, k0); one CTA per tile; threadIdx.x runs along k (unit
+// stride), threadIdx.y along j, and each thread marches along i.
+#include <cfloat>
+#include <cstring>
+#include <memory>
+
+#include "device.h"
+
+namespace amrb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+const TileTable& Level::tiles(int ti, int tj, int tk) {
+  auto key = std::make_tuple(ti, tj, tk);
+  auto it = tables.find(key);
+  if (it != tables.end()) return *it->second;
+  auto* t = new TileTable;
+  t->ti = ti;
+  t->tj = tj;
+  t->tk = tk;
+  for (int b = 0; b < nboxes; ++b) {
+    if (!resident[b]) continue;
+    const BoxGeom& g = geo[b];
+    for (int i = 0; i < g.n[0]; i += ti)
+      for (int j = 0; j < g.n[1]; j += tj)
+        for (int k = 0; k < g.n[2]; k += tk) t->host.push_back(make_int4(b, i, j, k));
+  }
+  t->dev.upload(t->host);
+  tables[key] = t;
+  return *t;
+}
+
+bool Level::all_even() const {
+  for (int b = 0; b < nboxes; ++b)
+    for (int x = 0; x < 3; ++x)
+      if (geo[b].n[x] % 2) return false;
+  return true;
+}
+
+namespace {
+
+struct Coef {
+  double dh0, dh1, dh2, gamma;
+};
+
+// 7-point operator, fixed operand order:
+//   ((dh0*((xm - 2c) + xp) + dh1*((ym - 2c) + yp)) + dh2*((zm - 2c) + zp))
+__device__ __forceinline__ double lap7(double c, double xm, double xp, double ym, double yp, double zm,
+                                       double zp, const Coef& k) {
+  const double c2 = 2.0 * c;
+  const double tx = k.dh0 * ((xm - c2) + xp);
+  const double ty = k.dh1 * ((ym - c2) + yp);
+  const double tz = k.dh2 * ((zm - c2) + zp);
+  return (tx + ty) + tz;
+}
+
+__device__ __forceinline__ double relax(double c, double rhs, double lap, double gamma) {
+  return c + (rhs - lap) / gamma;
+}
+
+template <class T>
+__device__ __forceinline__ T ldg(const T* p) {
+  return __ldg(p);
+}
+
+// ---------------------------------------------------------------------------
+// Simple tiles: TI x 8 x 32, block (32, 8); thread = one k, one j, march i.
+// ---------------------------------------------------------------------------
+constexpr int kTI = 8, kTJ = 8, kTK = 32;
+
+enum class Op { kLap, kResid };
+
+template <Op op>
+__global__ void __launch_bounds__(256)
+    k_stencil(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fo,
+              double* __restrict__ out, const FabView* __restrict__ fr, const double* __restrict__ rhs,
+              const FabView* __restrict__ fp, const double* __restrict__ phi, Coef cf) {
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = geo[t.x];
+  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
+  if (j >= g.n[1] || k >= g.n[2]) return;
+  const FabView P = fp[t.x], O = fo[t.x];
+  const double* p = phi + P.off + (int64_t)j * P.s1 + k;
+  double* o = out + O.off + (int64_t)j * O.s1 + k;
+  const double* r = nullptr;
+  int64_t rs0 = 0;
+  if (op == Op::kResid) {
+    const FabView R = fr[t.x];
+    r = rhs + R.off + (int64_t)j * R.s1 + k;
+    rs0 = R.s0;
+  }
+  const int iend = min(t.y + kTI, g.n[0]);
+  int i = t.y;
+  double xm = ldg(p + (int64_t)(i - 1) * P.s0);
+  double c = ldg(p + (int64_t)i * P.s0);
+  for (; i < iend; ++i) {
+    const double* pc = p + (int64_t)i * P.s0;
+    const double xp = ldg(pc + P.s0);
+    const double lap = lap7(c, xm, xp, ldg(pc - P.s1), ldg(pc + P.s1), ldg(pc - 1), ldg(pc + 1), cf);
+    double v = lap;
+    if (op == Op::kResid) v = ldg(r + (int64_t)i * rs0) - lap;
+    o[(int64_t)i * O.s0] = v;
+    xm = c;
+    c = xp;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One GSRB colour, in place.  Tile TI x 8 x 64; thread = a k-pair (exactly one
+// cell of the pair has the colour), so no lane idles on parity.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_gsrb_color(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fp,
+                 double* __restrict__ phi, const FabView* __restrict__ fr, const double* __restrict__ rhs,
+                 Coef cf, int color) {
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = geo[t.x];
+  const int j = t.z + threadIdx.y;
+  const int kp = t.w + 2 * threadIdx.x;
+  if (j >= g.n[1] || kp >= g.n[2]) return;
+  const FabView P = fp[t.x], R = fr[t.x];
+  const int iend = min(t.y + kTI, g.n[0]);
+  for (int i = t.y; i < iend; ++i) {
+    // global parity of (i, j, kp): pick the member of the pair with the colour
+    const int par = (g.lo[0] + i + g.lo[1] + j + g.lo[2] + kp + color) & 1;
+    const int k = kp + par;
+    if (k >= g.n[2]) continue;
+    double* pc = phi + P.off + (int64_t)i * P.s0 + (int64_t)j * P.s1 + k;
+    const double c = *pc;
+    const double lap = lap7(c, pc[-P.s0], pc[P.s0], pc[-P.s1], pc[P.s1], pc[-1], pc[1], cf);
+    const double b = rhs[R.off + (int64_t)i * R.s0 + (int64_t)j * R.s1 + k];
+    *pc = relax(c, b, lap, cf.gamma);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused red+black sweep, out of place (A -> B), marching along i.
+//
+// A CTA owns a TJ x TK column of one box over i in [i0, i0 + CI).  It keeps
+// four planes of A (grown by 2 in j and k) and two planes of rhs (grown by 1)
+// in shared memory.  At step p it relaxes the red cells of plane p+1 over the
+// tile grown by one ring (reading only black, i.e. old, values), then the
+// black cells of plane p over the tile (reading the new red values), then
+// streams plane p to B and prefetches plane p+3 / rhs p+2 with cp.async.
+// Because A is never written, neighbouring tiles and boxes read consistent
+// old values; the red update of ring cells is recomputed from the same
+// operands as its owner computes it, hence bit-identical to "fill; red; fill;
+// black" with a width-1 fill in between.  Cells outside the domain in a
+// non-periodic direction are never relaxed (they hold boundary values).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+struct SweepArgs {
+  const int4* tiles;
+  const BoxGeom* geo;
+  const FabView* fa;  // phi in (ngrow >= 2)
+  const FabView* fb;  // phi out
+  const FabView* fr;  // rhs (ngrow >= 1)
+  const double* a;
+  double* b;
+  const double* rhs;
+  Coef cf;
+  int ci;
+  int fixed_lo[3], fixed_hi[3];  // cells outside [lo, hi] (global) are not relaxed
+};
+
+template <int TJ, int TK>
+struct SweepSmem {
+  static constexpr int PJ = TJ + 4, PK = TK + 4;  // phi plane (grown by 2)
+  static constexpr int RJ = TJ + 2;               // rhs plane rows (grown by 1), PK cols
+  double phi[4][PJ][PK];
+  double rhs[2][RJ][PK];
+};
+
+template <int TJ, int TK>
+__device__ __forceinline__ void load_phi_plane(SweepSmem<TJ, TK>& sm, int slot, const double* a,
+                                               const FabView& A, int i, int j0, int jn, int k0, int kn) {
+  // rows j0-2 .. j0+jn+1, 16-byte chunks covering k0-2 .. k0+kn+1
+  const int rows = jn + 4, chunks = (kn + 4 + 1) / 2;
+  const double* base = a + A.off + (int64_t)i * A.s0 + (int64_t)(j0 - 2) * A.s1 + (k0 - 2);
+  for (int e = threadIdx.x + threadIdx.y * blockDim.x; e < rows * chunks; e += blockDim.x * blockDim.y) {
+    const int r = e / chunks, q = e - r * chunks;
+    cp_async16(&sm.phi[slot][r][2 * q], base + (int64_t)r * A.s1 + 2 * q);
+  }
+}
+
+template <int TJ, int TK>
+__device__ __forceinline__ void load_rhs_plane(SweepSmem<TJ, TK>& sm, int slot, const double* rhs,
+                                               const FabView& R, int i, int j0, int jn, int k0, int kn) {
+  const int rows = jn + 2, chunks = (kn + 4 + 1) / 2;
+  const double* base = rhs + R.off + (int64_t)i * R.s0 + (int64_t)(j0 - 1) * R.s1 + (k0 - 2);
+  for (int e = threadIdx.x + threadIdx.y * blockDim.x; e < rows * chunks; e += blockDim.x * blockDim.y) {
+    const int r = e / chunks, q = e - r * chunks;
+    cp_async16(&sm.rhs[slot][r][2 * q], base + (int64_t)r * R.s1 + 2 * q);
+  }
+}
+
+template <int TJ, int TK>
+__global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SweepSmem<TJ, TK>*>(smem_raw);
+  const int4 t = args.tiles[blockIdx.x];
+  const BoxGeom g = args.geo[t.x];
+  const FabView A = args.fa[t.x], B = args.fb[t.x], R = args.fr[t.x];
+  const Coef cf = args.cf;
+  const int i0 = t.y, j0 = t.z, k0 = t.w;
+  const int i1 = min(i0 + args.ci, g.n[0]);
+  const int jn = min(TJ, g.n[1] - j0), kn = min(TK, g.n[2] - k0);
+  const int nthreads = blockDim.x * blockDim.y;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+
+  auto slot = [&](int plane) { return (plane - i0 + 8) & 3; };
+  auto rslot = [&](int plane) { return (plane - i0 + 8) & 1; };
+
+  // red relaxation of plane ip over the ring-grown tile
+  auto red = [&](int ip) {
+    const int s = slot(ip), sm1 = slot(ip - 1), sp1 = slot(ip + 1), rs = rslot(ip);
+    const int gi = g.lo[0] + ip;
+    const bool ifix = gi < args.fixed_lo[0] || gi > args.fixed_hi[0];
+    const int rows = jn + 2, pairs = (kn + 2) / 2;
+    for (int e = tid; e < rows * pairs; e += nthreads) {
+      const int rr = e / pairs, q = e - rr * pairs;
+      const int j = j0 - 1 + rr;
+      const int kb = k0 - 1 + 2 * q;
+      const int par = (gi + g.lo[1] + j + g.lo[2] + kb) & 1;  // red: even
+      const int k = kb + par;
+      const int gj = g.lo[1] + j, gk = g.lo[2] + k;
+      if (ifix || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] || gk < args.fixed_lo[2] ||
+          gk > args.fixed_hi[2])
+        continue;
+      const int r = rr + 1, c = k - k0 + 2;
+      const double v = sm.phi[s][r][c];
+      const double lap = lap7(v, sm.phi[sm1][r][c], sm.phi[sp1][r][c], sm.phi[s][r - 1][c],
+                              sm.phi[s][r + 1][c], sm.phi[s][r][c - 1], sm.phi[s][r][c + 1], cf);
+      sm.phi[s][r][c] = relax(v, sm.rhs[rs][rr][c], lap, cf.gamma);
+    }
+  };
+  auto black = [&](int ip) {
+    const int s = slot(ip), sm1 = slot(ip - 1), sp1 = slot(ip + 1), rs = rslot(ip);
+    const int gi = g.lo[0] + ip;
+    const bool ifix = gi < args.fixed_lo[0] || gi > args.fixed_hi[0];
+    const int pairs = kn / 2;
+    for (int e = tid; e < jn * pairs; e += nthreads) {
+      const int jj = e / pairs, q = e - jj * pairs;
+      const int j = j0 + jj;
+      const int kb = k0 + 2 * q;
+      const int par = (gi + g.lo[1] + j + g.lo[2] + kb + 1) & 1;  // black: odd
+      const int k = kb + par;
+      const int gj = g.lo[1] + j, gk = g.lo[2] + k;
+      if (ifix || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] || gk < args.fixed_lo[2] ||
+          gk > args.fixed_hi[2])
+        continue;
+      const int r = jj + 2, c = k - k0 + 2;
+      const double v = sm.phi[s][r][c];
+      const double lap = lap7(v, sm.phi[sm1][r][c], sm.phi[sp1][r][c], sm.phi[s][r - 1][c],
+                              sm.phi[s][r + 1][c], sm.phi[s][r][c - 1], sm.phi[s][r][c + 1], cf);
+      sm.phi[s][r][c] = relax(v, sm.rhs[rs][jj + 1][c], lap, cf.gamma);
+    }
+  };
+  auto store = [&](int ip) {
+    const int s = slot(ip);
+    const int pairs = kn / 2;
+    double* base = args.b + B.off + (int64_t)ip * B.s0 + (int64_t)j0 * B.s1 + k0;
+    for (int e = tid; e < jn * pairs; e += nthreads) {
+      const int jj = e / pairs, q = e - jj * pairs;
+      const double2 v = make_double2(sm.phi[s][jj + 2][2 * q + 2], sm.phi[s][jj + 2][2 * q + 3]);
+      *reinterpret_cast<double2*>(base + (int64_t)jj * B.s1 + 2 * q) = v;
+    }
+  };
+
+  // prologue: planes i0-2 .. i0+1 of phi, i0-1 .. i0 of rhs
+  for (int ip = i0 - 2; ip <= i0 + 1; ++ip) load_phi_plane(sm, slot(ip), args.a, A, ip, j0, jn, k0, kn);
+  for (int ip = i0 - 1; ip <= i0; ++ip) load_rhs_plane(sm, rslot(ip), args.rhs, R, ip, j0, jn, k0, kn);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  red(i0 - 1);
+  __syncthreads();
+  load_phi_plane(sm, slot(i0 + 2), args.a, A, i0 + 2, j0, jn, k0, kn);
+  load_rhs_plane(sm, rslot(i0 + 1), args.rhs, R, i0 + 1, j0, jn, k0, kn);
+  cp_async_commit();
+  for (int p = i0; p < i1; ++p) {
+    cp_async_wait_all();
+    __syncthreads();
+    red(p + 1);
+    __syncthreads();
+    black(p);
+    __syncthreads();
+    // plane p is final; slot of p-1 and rhs slot of p are free
+    if (p + 3 <= i1 + 1) load_phi_plane(sm, slot(p + 3), args.a, A, p + 3, j0, jn, k0, kn);
+    if (p + 2 <= i1) load_rhs_plane(sm, rslot(p + 2), args.rhs, R, p + 2, j0, jn, k0, kn);
+    cp_async_commit();
+    store(p);
+  }
+  cp_async_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// Restriction (ratio 2, box-local coarsened layout) and fused residual-restrict.
+// Tile over coarse boxes: 8 x 8 x 32 coarse cells.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double avg8(double c000, double c001, double c010, double c011, double c100,
+                                       double c101, double c110, double c111) {
+  // numpy reshape(...).mean(axis=(2,4,6)) order (verified bit-for-bit)
+  return ((((c000 + c001) + (c010 + c011)) + (c100 + c101)) + (c110 + c111)) * 0.125;
+}
+
+// Generic restriction with per-axis ratio in {1, 2}.  Sum order = numpy's
+// reshape-mean: pair the last-axis children, then accumulate the pairs
+// sequentially in lexicographic order of the outer child offsets (verified
+// bit-for-bit against numpy 2.3 in 1-D, 2-D and 3-D).  mode 1 = injection
+// (child at offset 0, coarse_fine.py:150-154).
+__global__ void __launch_bounds__(256)
+    k_restrict(const int4* __restrict__ tiles, const BoxGeom* __restrict__ cgeo, const FabView* __restrict__ fc,
+               double* __restrict__ crse, const FabView* __restrict__ ff, const double* __restrict__ fine,
+               int ncomp, int3 rr, int mode, double inv) {
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = cgeo[t.x];
+  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
+  if (j >= g.n[1] || k >= g.n[2]) return;
+  const FabView C = fc[t.x], F = ff[t.x];
+  const int iend = min(t.y + kTI, g.n[0]);
+  for (int n = 0; n < ncomp; ++n)
+    for (int i = t.y; i < iend; ++i) {
+      const double* f0 = fine + F.off + n * F.cs + (int64_t)(rr.x * i) * F.s0 + (int64_t)(rr.y * j) * F.s1 + rr.z * k;
+      double acc;
+      if (mode == 1) {
+        acc = f0[0];
+      } else {
+        acc = 0.0;
+        bool first = true;
+        for (int a = 0; a < rr.x; ++a)
+          for (int b = 0; b < rr.y; ++b) {
+            const double* f = f0 + (int64_t)a * F.s0 + (int64_t)b * F.s1;
+            const double p = rr.z == 2 ? f[0] + f[1] : f[0];
+            acc = first ? p : acc + p;
+            first = false;
+          }
+        acc = acc * inv;
+      }
+      crse[C.off + n * C.cs + (int64_t)i * C.s0 + (int64_t)j * C.s1 + k] = acc;
+    }
+}
+
+__device__ __forceinline__ double resid_at(const double* p, int64_t s0, int64_t s1, double b, const Coef& cf) {
+  const double c = *p;
+  return b - lap7(c, p[-s0], p[s0], p[-s1], p[s1], p[-1], p[1], cf);
+}
+
+__global__ void __launch_bounds__(256)
+    k_resid_restrict(const int4* __restrict__ tiles, const BoxGeom* __restrict__ cgeo,
+                     const FabView* __restrict__ fc, double* __restrict__ crse, const FabView* __restrict__ fr,
+                     const double* __restrict__ rhs, const FabView* __restrict__ fp,
+                     const double* __restrict__ phi, Coef cf) {
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = cgeo[t.x];
+  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
+  if (j >= g.n[1] || k >= g.n[2]) return;
+  const FabView C = fc[t.x], R = fr[t.x], P = fp[t.x];
+  const int iend = min(t.y + kTI, g.n[0]);
+  for (int i = t.y; i < iend; ++i) {
+    double v[8];
+#pragma unroll
+    for (int di = 0; di < 2; ++di)
+#pragma unroll
+      for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk) {
+          const int fi = 2 * i + di, fj = 2 * j + dj, fk = 2 * k + dk;
+          const double* p = phi + P.off + (int64_t)fi * P.s0 + (int64_t)fj * P.s1 + fk;
+          const double b = rhs[R.off + (int64_t)fi * R.s0 + (int64_t)fj * R.s1 + fk];
+          v[di * 4 + dj * 2 + dk] = resid_at(p, P.s0, P.s1, b, cf);
+        }
+    crse[C.off + (int64_t)i * C.s0 + (int64_t)j * C.s1 + k] = avg8(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+  }
+}
+
+// Prolongation (pc), optionally added: fine(c) (+)= crse(c / 2).
+__global__ void __launch_bounds__(256)
+    k_prolong(const int4* __restrict__ tiles, const BoxGeom* __restrict__ fgeo, const FabView* __restrict__ ff,
+              double* __restrict__ fine, const FabView* __restrict__ fc, const double* __restrict__ crse,
+              int ncomp, int add, int3 sh) {
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = fgeo[t.x];
+  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
+  if (j >= g.n[1] || k >= g.n[2]) return;
+  const FabView F = ff[t.x], C = fc[t.x];
+  const int iend = min(t.y + kTI, g.n[0]);
+  // coarse local index: floor((lo + x)/2) - floor(lo/2); lo is even on coarsenable layouts
+  for (int n = 0; n < ncomp; ++n)
+    for (int i = t.y; i < iend; ++i) {
+      const double c = crse[C.off + n * C.cs + (int64_t)(i >> sh.x) * C.s0 + (int64_t)(j >> sh.y) * C.s1 + (k >> sh.z)];
+      double* f = fine + F.off + n * F.cs + (int64_t)i * F.s0 + (int64_t)j * F.s1 + k;
+      *f = add ? *f + c : c;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Reductions: per-tile partial (fixed tree), then one ordered final pass.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double combine(int kind, double a, double b) {
+  switch (kind) {
+    case 0:
+      return a + b;
+    case 1:
+      return fmin(a, b);
+    default:
+      return fmax(a, b);
+  }
+}
+
+__device__ __forceinline__ double identity(int kind) {
+  return kind == 0 ? 0.0 : kind == 1 ? DBL_MAX * 2.0 : -DBL_MAX * 2.0;
+}
+
+__device__ double block_combine(int kind, double v, double* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v = combine(kind, v, __shfl_down_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x + threadIdx.y * blockDim.x) >> 5;
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  const int nw = (blockDim.x * blockDim.y) >> 5;
+  if (warp == 0) {
+    v = lane < nw ? scratch[lane] : identity(kind);
+    for (int o = 16; o > 0; o >>= 1) v = combine(kind, v, __shfl_down_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+    k_reduce_tiles(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fx,
+                   const double* __restrict__ x, int comp, int kind, double* __restrict__ partial) {
+  __shared__ double scratch[32];
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = geo[t.x];
+  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
+  const int rkind = kind == 3 ? 2 : kind;
+  double acc = identity(rkind);
+  if (j < g.n[1] && k < g.n[2]) {
+    const FabView X = fx[t.x];
+    const int iend = min(t.y + kTI, g.n[0]);
+    for (int i = t.y; i < iend; ++i) {
+      double v = x[X.off + comp * X.cs + (int64_t)i * X.s0 + (int64_t)j * X.s1 + k];
+      if (kind == 3) v = fabs(v);
+      acc = combine(rkind, acc, v);
+    }
+  }
+  acc = block_combine(rkind, acc, scratch);
+  if (threadIdx.x == 0 && threadIdx.y == 0) partial[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(1024) k_reduce_final(const double* __restrict__ partial, int n, int kind,
+                                                       double* __restrict__ out) {
+  __shared__ double scratch[32];
+  const int rkind = kind == 3 ? 2 : kind;
+  double acc = identity(rkind);
+  for (int e = threadIdx.x; e < n; e += blockDim.x) acc = combine(rkind, acc, partial[e]);
+  acc = block_combine(rkind, acc, scratch);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Physical-domain ghost cells (apply_domain_boundary, amr_core.py:111-146):
+// one launch per (axis, side) in the reference's order, over every box whose
+// grown box pokes out of the domain on that side.
+// ---------------------------------------------------------------------------
+__global__ void k_domain_bc(const BoxGeom* __restrict__ geo, const FabView* __restrict__ fv, double* __restrict__ x,
+                            int nboxes, int3 ng, int ncomp, int axis, int side, int dlo, int dhi, int cond,
+                            double value) {
+  const int b = blockIdx.y;
+  if (b >= nboxes) return;
+  const BoxGeom g = geo[b];
+  const FabView F = fv[b];
+  const int gw[3] = {ng.x, ng.y, ng.z};
+  int glo[3], gn[3];
+  for (int a = 0; a < 3; ++a) {
+    glo[a] = g.lo[a] - gw[a];
+    gn[a] = g.n[a] + 2 * gw[a];
+  }
+  int width, first, edge;
+  if (side == 0) {
+    width = dlo - glo[axis];
+    first = glo[axis];
+    edge = dlo;
+  } else {
+    width = glo[axis] + gn[axis] - 1 - dhi;
+    first = dhi + 1;
+    edge = dhi;
+  }
+  if (width <= 0) return;
+  int ext[3] = {gn[0], gn[1], gn[2]};
+  ext[axis] = width;
+  const int64_t cells = (int64_t)ext[0] * ext[1] * ext[2];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cells * ncomp;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(e / cells);
+    int64_t r = e - (int64_t)n * cells;
+    int c[3];
+    c[2] = (int)(r % ext[2]);
+    r /= ext[2];
+    c[1] = (int)(r % ext[1]);
+    c[0] = (int)(r / ext[1]);
+    int gidx[3] = {glo[0] + c[0], glo[1] + c[1], glo[2] + c[2]};
+    gidx[axis] = first + c[axis];
+    auto addr = [&](const int* q) {
+      return F.off + n * F.cs + (int64_t)(q[0] - g.lo[0]) * F.s0 + (int64_t)(q[1] - g.lo[1]) * F.s1 +
+             (q[2] - g.lo[2]);
+    };
+    double v = value;
+    if (cond == 2) {
+      int src[3] = {gidx[0], gidx[1], gidx[2]};
+      src[axis] = edge;
+      v = x[addr(src)];
+    }
+    x[addr(gidx)] = v;
+  }
+}
+
+Coef make_coef(const double dh[3]) {
+  Coef c;
+  c.dh0 = dh[0];
+  c.dh1 = dh[1];
+  c.dh2 = dh[2];
+  c.gamma = -2.0 * ((dh[0] + dh[1]) + dh[2]);
+  return c;
+}
+
+const Level& L(const amrb_level* p) {
+  if (!p) throw Error(AMRB_EINVAL, "null level");
+  return *reinterpret_cast<const Level*>(p);
+}
+Level& Lm(const amrb_level* p) { return const_cast<Level&>(L(p)); }
+const Field& F(const amrb_field* p) {
+  if (!p) throw Error(AMRB_EINVAL, "null field");
+  return *reinterpret_cast<const Field*>(p);
+}
+
+void need_ghost(const Field& f, int g, const char* what) {
+  if (f.ngrow < g) throw Error(AMRB_EINVAL, std::string(what) + ": needs ghost width >= " + std::to_string(g));
+}
+
+void need_same_level(const Field& f, const Level& lv, const char* what) {
+  if (f.lv != &lv) throw Error(AMRB_EINVAL, std::string(what) + ": field bound to another level");
+}
+
+}  // namespace
+}  // namespace amrb
+
+using namespace amrb;
+
+extern "C" const char* amrb_last_error(void) { return amrb::g_last_error.c_str(); }
+extern "C" int amrb_version(void) { return 1; }
+
+extern "C" int amrb_level_create(int nboxes, const int32_t* boxes, const uint8_t* resident, amrb_level** out) {
+  return guarded([&] {
+    if (nboxes < 0 || (nboxes && !boxes) || !out) throw Error(AMRB_EINVAL, "amrb_level_create: bad arguments");
+    auto lv = std::make_unique<Level>();
+    lv->nboxes = nboxes;
+    lv->geo.resize(nboxes);
+    lv->resident.assign(nboxes, 1);
+    for (int b = 0; b < nboxes; ++b) {
+      for (int a = 0; a < 3; ++a) {
+        lv->geo[b].lo[a] = boxes[6 * b + a];
+        lv->geo[b].n[a] = boxes[6 * b + 3 + a] - boxes[6 * b + a] + 1;
+        if (lv->geo[b].n[a] < 1) throw Error(AMRB_EINVAL, "empty box in level");
+      }
+      if (resident) lv->resident[b] = resident[b];
+    }
+    lv->dgeo.upload(lv->geo);
+    *out = reinterpret_cast<amrb_level*>(lv.release());
+  });
+}
+
+extern "C" int amrb_level_destroy(amrb_level* lv) {
+  delete reinterpret_cast<Level*>(lv);
+  return AMRB_OK;
+}
+
+extern "C" int amrb_field_create(const amrb_level* lv_, const int64_t* fabtab, int ngrow, amrb_field** out) {
+  return guarded([&] {
+    const Level& lv = L(lv_);
+    if (!fabtab || !out || ngrow < 0) throw Error(AMRB_EINVAL, "amrb_field_create: bad arguments");
+    auto f = std::make_unique<Field>();
+    f->lv = &lv;
+    f->ngrow = ngrow;
+    f->host.resize(lv.nboxes);
+    for (int b = 0; b < lv.nboxes; ++b) {
+      const int64_t* t = fabtab + (int64_t)b * AMRB_FABTAB_W;
+      FabView v;
+      v.cs = t[1];
+      v.s0 = t[2];
+      v.s1 = t[3];
+      // offset of the valid lo cell = grown lo offset + ngrow in each axis
+      v.off = t[0] + (lv.geo[b].lo[0] - t[4]) * v.s0 + (lv.geo[b].lo[1] - t[5]) * v.s1 + (lv.geo[b].lo[2] - t[6]);
+      f->host[b] = v;
+      if (b == 0)
+        for (int a = 0; a < 3; ++a) f->ng3[a] = (int)(lv.geo[b].lo[a] - t[4 + a]);
+    }
+    f->dev.upload(f->host);
+    *out = reinterpret_cast<amrb_field*>(f.release());
+  });
+}
+
+extern "C" int amrb_field_destroy(amrb_field* f) {
+  delete reinterpret_cast<Field*>(f);
+  return AMRB_OK;
+}
+
+namespace {
+template <class K, class... Args>
+void launch_tiles(const TileTable& tt, K kernel, cudaStream_t st, dim3 block, Args... args) {
+  if (tt.host.empty()) return;
+  kernel<<<(unsigned)tt.host.size(), block, 0, st>>>(tt.dev.p, args...);
+}
+}  // namespace
+
+extern "C" int amrb_lap_apply(const amrb_level* lv_, amrb_field* out, double* out_base, const amrb_field* phi,
+                              const double* phi_base, const double dh[3], void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(phi), 1, "lap_apply");
+    need_same_level(F(out), lv, "lap_apply");
+    need_same_level(F(phi), lv, "lap_apply");
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    launch_tiles(tt, k_stencil<Op::kLap>, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(out).dev.p, out_base,
+                 (const FabView*)nullptr, (const double*)nullptr, F(phi).dev.p, phi_base, make_coef(dh));
+    check_launch("k_stencil<lap>");
+  });
+}
+
+extern "C" int amrb_residual(const amrb_level* lv_, amrb_field* r, double* r_base, const amrb_field* rhs,
+                             const double* rhs_base, const amrb_field* phi, const double* phi_base,
+                             const double dh[3], void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(phi), 1, "residual");
+    for (auto* f : {r, (amrb_field*)rhs, (amrb_field*)phi}) need_same_level(F(f), lv, "residual");
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    launch_tiles(tt, k_stencil<Op::kResid>, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(r).dev.p, r_base,
+                 F(rhs).dev.p, rhs_base, F(phi).dev.p, phi_base, make_coef(dh));
+    check_launch("k_stencil<resid>");
+  });
+}
+
+extern "C" int amrb_gsrb_color(const amrb_level* lv_, amrb_field* phi, double* phi_base, const amrb_field* rhs,
+                               const double* rhs_base, const double dh[3], int color, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(phi), 1, "gsrb_color");
+    need_same_level(F(phi), lv, "gsrb_color");
+    need_same_level(F(rhs), lv, "gsrb_color");
+    if (color != 0 && color != 1) throw Error(AMRB_EINVAL, "color must be 0 or 1");
+    const auto& tt = lv.tiles(kTI, kTJ, 2 * kTK);
+    launch_tiles(tt, k_gsrb_color, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(phi).dev.p, phi_base,
+                 F(rhs).dev.p, rhs_base, make_coef(dh), color);
+    check_launch("k_gsrb_color");
+  });
+}
+
+namespace {
+constexpr int kSweepCI = 16;
+
+template <int TJ, int TK>
+void launch_sweep(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
+                  const double* r_base, const Coef& cf, const int fixed_lo[3], const int fixed_hi[3],
+                  cudaStream_t st) {
+  const auto& tt = lv.tiles(kSweepCI, TJ, TK);
+  if (tt.host.empty()) return;
+  SweepArgs args;
+  args.tiles = tt.dev.p;
+  args.geo = lv.dgeo.p;
+  args.fa = a.dev.p;
+  args.fb = b.dev.p;
+  args.fr = r.dev.p;
+  args.a = a_base;
+  args.b = b_base;
+  args.rhs = r_base;
+  args.cf = cf;
+  args.ci = kSweepCI;
+  for (int x = 0; x < 3; ++x) {
+    args.fixed_lo[x] = fixed_lo[x];
+    args.fixed_hi[x] = fixed_hi[x];
+  }
+  const size_t smem = sizeof(SweepSmem<TJ, TK>);
+  static bool configured = false;
+  if (!configured) {
+    AMRB_CUDA(cudaFuncSetAttribute(k_gsrb_sweep<TJ, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  k_gsrb_sweep<TJ, TK><<<(unsigned)tt.host.size(), dim3(32, 8), smem, st>>>(args);
+  check_launch("k_gsrb_sweep");
+}
+}  // namespace
+
+extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const double* a_base, amrb_field* b,
+                                  double* b_base, const amrb_field* rhs, const double* rhs_base, const double dh[3],
+                                  const int32_t* fixed_lohi, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(a), 2, "gsrb_sweep (phi in)");
+    need_ghost(F(rhs), 1, "gsrb_sweep (rhs)");
+    for (auto* f : {a, (const amrb_field*)b, rhs}) need_same_level(F(f), lv, "gsrb_sweep");
+    if (!lv.all_even()) throw Error(AMRB_EINVAL, "gsrb_sweep needs even box extents");
+    int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
+    if (fixed_lohi)
+      for (int x = 0; x < 3; ++x) {
+        flo[x] = fixed_lohi[x];
+        fhi[x] = fixed_lohi[3 + x];
+      }
+    int maxk = 0;
+    for (auto& g : lv.geo) maxk = std::max(maxk, g.n[2]);
+    if (maxk >= 64)
+      launch_sweep<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
+                           (cudaStream_t)stream);
+    else
+      launch_sweep<16, 32>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
+                           (cudaStream_t)stream);
+  });
+}
+
+namespace {
+int3 ratio3(const int32_t* ratio) {
+  int3 r = make_int3(2, 2, 2);
+  if (ratio) r = make_int3(ratio[0], ratio[1], ratio[2]);
+  if ((r.x != 1 && r.x != 2) || (r.y != 1 && r.y != 2) || (r.z != 1 && r.z != 2))
+    throw Error(AMRB_EINVAL, "device restriction/prolongation supports ratio 1 or 2 per axis");
+  return r;
+}
+}  // namespace
+
+extern "C" int amrb_restrict(const amrb_level* clv_, amrb_field* crse, double* crse_base, const amrb_field* fine,
+                             const double* fine_base, int ncomp, const int32_t* ratio, int mode, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(clv_);
+    need_same_level(F(crse), lv, "restrict");
+    const int3 r = ratio3(ratio);
+    if (mode != 0 && mode != 1) throw Error(AMRB_EINVAL, "restrict mode must be 0 (average) or 1 (injection)");
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    launch_tiles(tt, k_restrict, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(crse).dev.p, crse_base,
+                 F(fine).dev.p, fine_base, ncomp, r, mode, 1.0 / (r.x * r.y * r.z));
+    check_launch("k_restrict");
+  });
+}
+
+extern "C" int amrb_residual_restrict(const amrb_level* clv_, amrb_field* crse, double* crse_base,
+                                      const amrb_field* rhs, const double* rhs_base, const amrb_field* phi,
+                                      const double* phi_base, const double dh[3], void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(clv_);
+    need_same_level(F(crse), lv, "residual_restrict");
+    need_ghost(F(phi), 1, "residual_restrict");
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    launch_tiles(tt, k_resid_restrict, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(crse).dev.p, crse_base,
+                 F(rhs).dev.p, rhs_base, F(phi).dev.p, phi_base, make_coef(dh));
+    check_launch("k_resid_restrict");
+  });
+}
+
+extern "C" int amrb_prolong(const amrb_level* flv_, amrb_field* fine, double* fine_base, const amrb_field* crse,
+                            const double* crse_base, int ncomp, const int32_t* ratio, int add, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(flv_);
+    need_same_level(F(fine), lv, "prolong");
+    const int3 r = ratio3(ratio);
+    const int3 sh = make_int3(r.x == 2, r.y == 2, r.z == 2);
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    launch_tiles(tt, k_prolong, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(fine).dev.p, fine_base,
+                 F(crse).dev.p, crse_base, ncomp, add, sh);
+    check_launch("k_prolong");
+  });
+}
+
+extern "C" int amrb_reduce(const amrb_level* lv_, const amrb_field* x, const double* x_base, int comp, int kind,
+                           double* dev_out, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    if (kind < 0 || kind > 3) throw Error(AMRB_EINVAL, "unknown reduction kind");
+    need_same_level(F(x), lv, "reduce");
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const int n = (int)tt.host.size();
+    if (lv.partials.n < (size_t)std::max(n, 1)) lv.partials.alloc(std::max(n, 1));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n) launch_tiles(tt, k_reduce_tiles, st, dim3(32, 8), lv.dgeo.p, F(x).dev.p, x_base, comp, kind, lv.partials.p);
+    k_reduce_final<<<1, 1024, 0, st>>>(lv.partials.p, n, kind, dev_out);
+    check_launch("k_reduce");
+  });
+}
+
+extern "C" int amrb_domain_bc(const amrb_level* lv_, amrb_field* f, double* base, int ncomp, const int32_t* domain,
+                              const int32_t* bc, double value, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    const Field& fld = F(f);
+    need_same_level(fld, lv, "domain_bc");
+    if (!domain || !bc) throw Error(AMRB_EINVAL, "domain_bc: null argument");
+    if (fld.ngrow == 0 || lv.nboxes == 0) return;
+    for (int axis = 0; axis < 3; ++axis)
+      for (int side = 0; side < 2; ++side) {
+        const int cond = bc[2 * axis + side];
+        if (cond == 0) continue;
+        dim3 grid(64, lv.nboxes);
+        k_domain_bc<<<grid, 256, 0, (cudaStream_t)stream>>>(lv.dgeo.p, fld.dev.p, base, lv.nboxes,
+                                                           make_int3(fld.ng3[0], fld.ng3[1], fld.ng3[2]), ncomp,
+                                                           axis, side, domain[axis], domain[3 + axis], cond, value);
+        check_launch("k_domain_bc");
+      }
+  });
+}

@@ -1,0 +1,268 @@
+"""Device-resident mesh data: Fab, FabArray and MultiFab.
+
+Drop-in for the reference's containers (/root/reference/pkg/src/amrkit/
+fabarray.py:28-131): same constructor ``FabArray(ba, dm, ncomp, ngrow,
+dtype)``, same ``fab(i)`` accessor returning a Fab with ``box / gbox / ncomp
+/ ngrow / data / valid() / slice() / setval()``, and ``data`` keeps the
+reference's logical shape ``(ncomp, *grown extents)`` in C order (last axis
+unit-stride).
+
+What changes is where the bytes live.  A FabArray owns ONE torch CUDA
+allocation per device; box b occupies a contiguous, 256-byte aligned block in
+which every k-row (last axis) is padded so the first VALID cell of each row
+starts on a 32-byte sector and the row pitch is a multiple of 4 doubles.
+``fab(i).data`` is an ``as_strided`` view of that block with the logical
+shape.  ``fabtab`` (int64, nboxes x 8) describes the layout to libamrb.
+
+Ranks: in one process (the reference's simulated ranks, and the 1-GPU case)
+every box is resident on the one device; under torch.distributed with one
+process per GPU and ``dm.nranks == world_size`` only the boxes owned by this
+rank are allocated (owner-computes).  ``replicated=True`` makes
+every box resident on every rank (the agglomerated MLMG bottom levels).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .boxes import Box, IntVect
+from .layout import BoxArray, DistributionMapping
+
+__all__ = ["Fab", "FabArray", "MultiFab", "ArrayView", "current_rank", "world_size"]
+
+import itertools
+
+_serials = itertools.count(1)
+_ALIGN_ROW = 4  # doubles: 32-byte sectors
+_ALIGN_BOX = 32  # doubles: 256 bytes
+
+
+def world_size():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size()
+    return 1
+
+
+def current_rank():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank()
+    return 0
+
+
+def _default_device():
+    if torch.cuda.is_available():
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _round(x, a):
+    return (x + a - 1) // a * a
+
+
+class Fab:
+    """One box's data: a strided view into the owning FabArray's allocation."""
+
+    __slots__ = ("box", "gbox", "ncomp", "ngrow", "data")
+
+    def __init__(self, box, ncomp, ngrow, data):
+        self.box = box
+        self.ngrow = int(ngrow)
+        self.ncomp = int(ncomp)
+        self.gbox = box.grow(self.ngrow)
+        self.data = data
+
+    def _index(self, region):
+        if not self.gbox.contains_box(region):
+            raise ValueError(f"{region!r} not within {self.gbox!r}")
+        return tuple(
+            slice(region.lo[d] - self.gbox.lo[d], region.hi[d] - self.gbox.lo[d] + 1) for d in range(self.box.dim)
+        )
+
+    def slice(self, region, comp=None):
+        idx = self._index(region)
+        if comp is None:
+            return self.data[(slice(None),) + idx]
+        return self.data[(comp,) + idx]
+
+    def valid(self, comp=None):
+        return self.slice(self.box, comp)
+
+    def array(self):
+        return ArrayView(self)
+
+    def setval(self, value, comp=None, ghosts=True):
+        if ghosts:
+            (self.data if comp is None else self.data[comp]).fill_(value)
+        else:
+            self.slice(self.box, comp).fill_(value)
+
+
+class ArrayView:
+    """Global-index window (i, j, k, n) onto a Fab (fabarray.py:68-91)."""
+
+    __slots__ = ("data", "lo", "dim")
+
+    def __init__(self, fab):
+        self.data = fab.data
+        self.lo = fab.gbox.lo
+        self.dim = fab.box.dim
+
+    def _key(self, key):
+        if len(key) != self.dim + 1:
+            raise IndexError(f"expected {self.dim + 1} indices (spatial + component)")
+        return (key[-1],) + tuple(key[d] - self.lo[d] for d in range(self.dim))
+
+    def __getitem__(self, key):
+        return self.data[self._key(key)]
+
+    def __setitem__(self, key, value):
+        self.data[self._key(key)] = value
+
+
+class FabArray:
+    """One Fab per box of ``ba``; boxes resident where ``dm`` puts them."""
+
+    def __init__(self, ba, dm, ncomp=1, ngrow=0, dtype=np.float64, *, device=None, replicated=False, rank=None):
+        if len(ba) != len(dm):
+            raise ValueError("BoxArray and DistributionMapping lengths differ")
+        if np.dtype(dtype) != np.float64:
+            raise ValueError("device FabArrays hold float64 (the reference's MultiFab type)")
+        self.ba = ba
+        self.dm = dm
+        self.ncomp = int(ncomp)
+        self.ngrow = int(ngrow)
+        self.dtype = np.dtype(np.float64)
+        self.device = torch.device(device) if device is not None else _default_device()
+        self.replicated = bool(replicated)
+        ws = world_size()
+        self.distributed = (not replicated) and ws > 1 and dm.nranks == ws
+        self.rank = current_rank() if rank is None else int(rank)
+        if self.distributed:
+            self.resident = np.array([r == self.rank for r in dm.owner], dtype=bool)
+        else:
+            self.resident = np.ones(len(ba), dtype=bool)
+        self._layout()
+        self.storage = torch.zeros(self._nelems, dtype=torch.float64, device=self.device)
+        self.fabs = {}
+        for i in range(len(ba)):
+            if self.resident[i]:
+                self.fabs[i] = Fab(ba[i], self.ncomp, self.ngrow, self._view(i))
+        self._progs = {}
+        self._native = {}
+        self.serial = next(_serials)
+
+    # -- layout ---------------------------------------------------------------
+    def _layout(self):
+        dim = self.ba.dim
+        pad = 3 - dim
+        g = self.ngrow
+        n = len(self.ba)
+        tab = np.zeros((n, 8), dtype=np.int64)
+        ext3 = np.ones((n, 3), dtype=np.int64)
+        front = (_ALIGN_ROW - g % _ALIGN_ROW) % _ALIGN_ROW
+        off = 0
+        for i, b in enumerate(self.ba):
+            e = [1, 1, 1]
+            glo = [0, 0, 0]
+            for d in range(dim):
+                e[pad + d] = b.hi[d] - b.lo[d] + 1 + 2 * g
+                glo[pad + d] = b.lo[d] - g
+            ext3[i] = e
+            pitch = _round(front + e[2] + 2, _ALIGN_ROW)
+            s1 = pitch
+            s0 = e[1] * s1
+            cs = e[0] * s0
+            if self.resident[i]:
+                tab[i] = (off + front, cs, s0, s1, glo[0], glo[1], glo[2], 1)
+                off += _round(self.ncomp * cs, _ALIGN_BOX)
+            else:
+                tab[i, 4:7] = glo
+        self.fabtab = tab
+        self._ext3 = ext3
+        self._nelems = max(off + _ALIGN_BOX, _ALIGN_BOX)
+
+    def _view(self, i):
+        t = self.fabtab[i]
+        dim = self.ba.dim
+        pad = 3 - dim
+        size = (self.ncomp,) + tuple(int(x) for x in self._ext3[i][pad:])
+        all_strides = (int(t[1]), int(t[2]), int(t[3]), 1)
+        stride = (all_strides[0],) + all_strides[1 + pad :]
+        return torch.as_strided(self.storage, size, stride, int(t[0]))
+
+    @property
+    def dim(self):
+        return self.ba.dim
+
+    def fab(self, i):
+        try:
+            return self.fabs[i]
+        except KeyError:
+            raise KeyError(f"box {i} is not resident on rank {self.rank}") from None
+
+    def local_indices(self, rank=None):
+        if rank is None:
+            return [i for i in range(len(self.ba)) if self.resident[i]]
+        return self.dm.owned_indices(rank)
+
+    def setval(self, value, comp=None, ghosts=True):
+        if ghosts and comp is None:
+            self.storage.fill_(value)
+            return self
+        for f in self.fabs.values():
+            f.setval(value, comp, ghosts)
+        return self
+
+    def copy_shape(self, ncomp=None, ngrow=None):
+        return type(self)(
+            self.ba,
+            self.dm,
+            self.ncomp if ncomp is None else ncomp,
+            self.ngrow if ngrow is None else ngrow,
+            self.dtype,
+            device=self.device,
+            replicated=self.replicated,
+            rank=self.rank,
+        )
+
+    def owners(self):
+        """Owner rank per box as seen by copy programs.
+
+        A replicated FabArray is resident everywhere, so under one process per
+        GPU every box counts as owned by this rank (copies from/to it are local).
+        """
+        if self.replicated and world_size() > 1:
+            return np.full(len(self.ba), self.rank, dtype=np.int32)
+        return np.asarray(self.dm.owner, dtype=np.int32)
+
+    # -- host <-> device helpers ----------------------------------------------
+    def load_valid_from(self, domain, global_arr):
+        """Load every resident fab's valid region from one dense array over domain."""
+        g = np.asarray(global_arr)
+        if g.ndim == self.dim:
+            g = g[None]
+        gt = torch.as_tensor(np.ascontiguousarray(g)).to(self.device)
+        for i, f in self.fabs.items():
+            b = self.ba[i]
+            sel = tuple(slice(b.lo[d] - domain.lo[d], b.hi[d] - domain.lo[d] + 1) for d in range(self.dim))
+            f.valid().copy_(gt[(slice(None),) + sel])
+        return self
+
+    def to_global(self, domain, comp=0, default=0.0):
+        """Dense numpy array over domain from resident valid data."""
+        from .comm import gather_global
+
+        return gather_global(self, domain, comp, default)
+
+    def require_cuda(self, what):
+        if self.device.type != "cuda":
+            raise RuntimeError(f"{what}: FabArray storage is on {self.device}; the hot path runs on CUDA only")
+
+
+class MultiFab(FabArray):
+    """float64 FabArray (AMReX's MultiFab)."""

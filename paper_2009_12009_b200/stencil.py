@@ -1,0 +1,84 @@
+"""Box-loop stencil operators on device MultiFabs (the MLMG building blocks).
+
+Each function is one libamrb launch over every resident box of a level
+(the ParallelFor box loop; the reference's per-box numpy loop pattern is
+advect.py:143-178).  Operands are MultiFabs on the same BoxArray; ghost
+cells must already be filled (fill_boundary).  Definitions (operand order,
+colouring) are those of oracle/mlmg_ref.py and the results are bit-identical.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from ._native import check, i32p, lib
+from .device import dh_array, field_of, level_of, stream_ptr
+
+__all__ = ["laplacian", "residual", "gsrb_color", "gsrb_sweep", "residual_restrict", "dh_of"]
+
+
+def dh_of(geom):
+    """1/dx^2 per axis from Geometry.cell_size (amr_core.py:37-40)."""
+    return tuple(1.0 / (c * c) for c in geom.cell_size)
+
+
+def _p(fa):
+    return C.c_void_p(fa.storage.data_ptr())
+
+
+def _same_layout(*fas):
+    ba = fas[0].ba
+    for f in fas:
+        f.require_cuda("stencil")
+        if f.ba is not ba and f.ba != ba:
+            raise ValueError("operands must share one BoxArray")
+        if f.dim != 3:
+            raise ValueError("stencil operators are 3-D")
+
+
+def laplacian(out, phi, dh):
+    """out = L(phi) on valid cells (phi ghosts of width >= 1 filled)."""
+    _same_layout(out, phi)
+    check(lib().amrb_lap_apply(level_of(out).handle, field_of(out).handle, _p(out), field_of(phi).handle, _p(phi),
+                               dh_array(dh), stream_ptr()))
+
+
+def residual(r, rhs, phi, dh):
+    """r = rhs - L(phi)."""
+    _same_layout(r, rhs, phi)
+    check(lib().amrb_residual(level_of(r).handle, field_of(r).handle, _p(r), field_of(rhs).handle, _p(rhs),
+                              field_of(phi).handle, _p(phi), dh_array(dh), stream_ptr()))
+
+
+def gsrb_color(phi, rhs, dh, color):
+    """One in-place GSRB colour ((i+j+k+color) % 2 == 0, global indices)."""
+    _same_layout(phi, rhs)
+    check(lib().amrb_gsrb_color(level_of(phi).handle, field_of(phi).handle, _p(phi), field_of(rhs).handle, _p(rhs),
+                                dh_array(dh), int(color), stream_ptr()))
+
+
+def gsrb_sweep(a, b, rhs, dh, fixed=None):
+    """b = one fused red+black sweep of a (a ghosts width 2, rhs ghosts width 1
+    filled).  ``fixed`` = Box outside which cells are never relaxed."""
+    _same_layout(a, b, rhs)
+    fp = None
+    if fixed is not None:
+        import numpy as np
+
+        pad = 3 - fixed.dim
+        arr = np.array([-(1 << 30)] * 3 + [1 << 30] * 3, dtype=np.int32)
+        for d in range(fixed.dim):
+            arr[pad + d] = fixed.lo[d]
+            arr[3 + pad + d] = fixed.hi[d]
+        _keep, fp = i32p(arr)
+    check(lib().amrb_gsrb_sweep(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
+                                field_of(rhs).handle, _p(rhs), dh_array(dh), fp, stream_ptr()))
+
+
+def residual_restrict(crse, rhs, phi, dh):
+    """crse (on coarsened_layout(phi.ba, 2)) = average_down(rhs - L(phi))."""
+    crse.require_cuda("residual_restrict")
+    if len(crse.ba) != len(phi.ba):
+        raise ValueError("crse must live on the box-local coarsened layout")
+    check(lib().amrb_residual_restrict(level_of(crse).handle, field_of(crse).handle, _p(crse), field_of(rhs).handle,
+                                       _p(rhs), field_of(phi).handle, _p(phi), dh_array(dh), stream_ptr()))
