@@ -293,7 +293,9 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
+  // red of planes i0-1 and i0 (independent: red reads only black cells)
   red(i0 - 1);
+  red(i0);
   __syncthreads();
   load_phi_plane(sm, slot(i0 + 2), args.a, A, i0 + 2, j0, jn, k0, kn);
   load_rhs_plane(sm, rslot(i0 + 1), args.rhs, R, i0 + 1, j0, jn, k0, kn);
