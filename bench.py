@@ -1,0 +1,334 @@
+"""Benchmark: MLMG Poisson solve (C3: 256^3, 64^3 boxes, 1 GPU; C4 weak scaling:
+256^3 per GPU) through the package API, plus the fused GSRB kernel roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full MLMG solve to 1e-10 relative residual on a synthetic,
+host-centred random rhs.  ``value`` = GSRB cell-updates (every smoother
+relaxation of every cell on every level) per second over the K timed solves,
+whole job (all GPUs).  ``ms_per_step`` is the MLMG solve time.  ``e2e`` is the
+same metric through MLMG.solve with the rhs in pinned host memory and the
+solution copied back to pinned host memory inside the timed region.
+``roofline`` is the fine-level fused GSRB sweep kernel, timed with CUDA events
+on its launch stream, against the measured HBM copy bandwidth.
+
+``--impl reference`` times the CPU oracle (numpy restatement of the reference
+path; the reference itself has no MLMG) on rank 0: one V-cycle of the same
+problem per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 cell-updates/s (GSRB, %HBM roofline); MLMG 256^3 solve time @1/2/4/8 GPU"
+UNIT = "cell-updates/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _domain_for(n_gpus):
+    f = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(n_gpus)
+    if f is None:
+        raise SystemExit(f"unsupported --gpus {n_gpus} (1, 2, 4 or 8)")
+    return tuple(256 * x for x in f)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for _, _, flags in rows for n, f in zip(names, flags) if f.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def run_reference(args):
+    """CPU oracle (numpy, 1 thread of compute) on rank 0; one V-cycle per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import mlmg_ref as R
+
+    n, m = 256, 64
+    boxes = [((i, j, k), (i + m - 1, j + m - 1, k + m - 1)) for i in range(0, n, m) for j in range(0, n, m)
+             for k in range(0, n, m)]
+    rng = np.random.default_rng(2)
+    rhs = rng.standard_normal((n, n, n))
+    rhs -= rhs.mean()
+    s = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), boxes)
+    times = []
+    for step in range(args.warmup + args.steps):
+        s.cell_updates = 0
+        t0 = time.perf_counter()
+        s.solve(rhs, max_cycles=1)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append((dt, s.cell_updates))
+    tot_t = sum(t for t, _ in times)
+    tot_u = sum(u for _, u in times)
+    v = tot_u / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3 MLMG Poisson 256^3, 64^3 boxes, periodic; one V(2,2) cycle per step (CPU sample)",
+                   "global_batch": 1, "seq_len": n ** 3, "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": "one full V(2,2) cycle of the C3 solve (7 levels, 32-sweep bottom) in the numpy "
+                                   "oracle; host cores available: %d" % (os.cpu_count() or 0)},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample():
+    """Bounded oracle sample for the cpu_baseline key (one V-cycle of C3)."""
+    from oracle import mlmg_ref as R
+
+    n, m = 256, 64
+    boxes = [((i, j, k), (i + m - 1, j + m - 1, k + m - 1)) for i in range(0, n, m) for j in range(0, n, m)
+             for k in range(0, n, m)]
+    rng = np.random.default_rng(2)
+    rhs = rng.standard_normal((n, n, n))
+    rhs -= rhs.mean()
+    s = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), boxes)
+    t0 = time.perf_counter()
+    s.solve(rhs, max_cycles=1)
+    dt = time.perf_counter() - t0
+    return {"value": s.cell_updates / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"one V(2,2) cycle of C3 in the numpy oracle ({dt:.1f} s, {s.cell_updates} cell-updates); "
+                      f"host has {os.cpu_count()} cores, the oracle uses 1"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2009_12009_b200 as A
+    from paper_2009_12009_b200 import stencil as S
+    from paper_2009_12009_b200._native import lib
+
+    ext = _domain_for(world)
+    dom = A.Box((0, 0, 0), tuple(e - 1 for e in ext))
+    ba = A.BoxArray([dom]).max_size(64)
+    dm = A.sfc_distribute(ba, A.default_costs(ba), world)
+    tr = A.Transport.distributed() if world > 1 else A.Transport(1)
+    geom = A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, True)
+
+    # synthetic rhs: per-box seeded normals on device, centred globally
+    rhs = A.MultiFab(ba, dm, 1, 0)
+    gen = torch.Generator(device="cuda")
+    for i, f in rhs.fabs.items():
+        gen.manual_seed(1000003 * (2 if world == 1 else 3) + i)
+        f.valid().copy_(torch.randn(tuple(f.valid().shape), generator=gen, device="cuda", dtype=torch.float64))
+    tot = torch.tensor([A.device_reduce(rhs, "sum").item()], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    mean = tot.item() / dom.num_cells()
+    for f in rhs.fabs.values():
+        f.valid().sub_(mean)
+    phi = A.MultiFab(ba, dm, 1, 1)
+    mg = A.MLMG(geom, ba, dm, transport=tr)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def maxover(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def one_solve():
+        phi.setval(0.0)
+        return mg.solve(phi, rhs, rtol=1e-10, max_iter=100)
+
+    for _ in range(args.warmup):
+        one_solve()
+    iters = []
+    launches0 = lib().amrb_launch_count()
+    replays0 = mg.graph_replays
+    barrier()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            one_solve()
+            iters.append(mg.iterations)
+        e1.record(st)
+        barrier()
+    t_dev = maxover(e0.elapsed_time(e1) / 1e3)
+    launches = (lib().amrb_launch_count() - launches0) + (mg.graph_replays - replays0) * mg.launches_per_cycle
+    # every level's smoother relaxations, counted once for the whole job (replicated
+    # bottom levels run redundantly on every rank but are counted once)
+    updates_job = mg.cell_updates_per_cycle * sum(iters)
+    value = updates_job / t_dev
+    ms = 1e3 * t_dev / args.steps
+
+    # ---- e2e: pinned host rhs -> solve -> pinned host phi ------------------------
+    host_rhs = {i: f.valid().detach().cpu().pin_memory() for i, f in rhs.fabs.items()}
+    host_phi = {i: torch.empty(tuple(f.valid().shape), dtype=torch.float64).pin_memory() for i, f in phi.fabs.items()}
+    dev_rhs = A.MultiFab(ba, dm, 1, 0)
+    h2d = sum(t.numel() * 8 for t in host_rhs.values())
+    d2h = sum(t.numel() * 8 for t in host_phi.values())
+    e_iters = []
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for i, t in host_rhs.items():
+            dev_rhs.fab(i).valid().copy_(t, non_blocking=True)
+        phi.setval(0.0)
+        mg.solve(phi, dev_rhs, rtol=1e-10, max_iter=100)
+        e_iters.append(mg.iterations)
+        for i, t in host_phi.items():
+            t.copy_(phi.fab(i).valid(), non_blocking=True)
+        torch.cuda.synchronize()
+    barrier()
+    t_e2e = maxover(time.perf_counter() - t0)
+    e2e_value = mg.cell_updates_per_cycle * sum(e_iters) / t_e2e
+
+    # ---- roofline: fine-level fused sweep, events on its launch stream ----------
+    top = mg.levels[0]
+    a, b = top.phi[0], top.phi[1]
+    evs = []
+    for r in range(23):
+        A.fill_boundary(a, tr, top.domain, True, ngrow=2)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(st)
+        S.gsrb_sweep(a, b, top.rhs, top.dh)
+        s1.record(st)
+        evs.append((s0, s1))
+        a, b = b, a
+    torch.cuda.synchronize()
+    t_sweep = float(np.mean([x.elapsed_time(y) for x, y in evs[3:]])) / 1e3
+    t_sweep = maxover(t_sweep)
+    nloc = sum(ba[i].num_cells() for i in range(len(ba)) if dm[i] == rank)
+    floc = sum(2 * (e[0] * e[1] + e[1] * e[2] + e[2] * e[0]) for e in (ba[i].extents() for i in range(len(ba)) if dm[i] == rank))
+    alg_bytes = 24 * nloc + 8 * floc
+    achieved = alg_bytes / t_sweep / 1e9
+    peak, peak_kind = _peaks()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": ("C3 MLMG Poisson 256^3, 64^3 boxes, 1 GPU" if world == 1 else
+                             f"C4 weak-scaling MLMG Poisson {ext[0]}x{ext[1]}x{ext[2]} (256^3 per GPU), 64^3 boxes"),
+                "domain": list(ext), "box": 64, "boxes": len(ba), "levels": len(mg.levels), "cycle": "V(2,2)",
+                "bottom_sweeps": mg.bottom_sweeps, "rtol": 1e-10, "iterations": iters,
+                "mlmg_solve_ms": ms, "global_batch": 1, "seq_len": dom.num_cells(),
+                "parallelism": f"dp{world} (boxes by Morton SFC)",
+                "l2": "working set (phi x2 + rhs, 256^3 fp64 per GPU = 0.4 GB) exceeds the 126 MB L2",
+            },
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": 1e3 * t_e2e / args.steps},
+            "roofline": {"bound": "hbm", "kernel": "k_gsrb_sweep (fine level, fused red+black)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_kind": peak_kind, "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                         "us_per_launch": t_sweep * 1e6,
+                         "kernel_cell_updates_per_s": nloc / t_sweep},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tr.close()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

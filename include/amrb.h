@@ -51,6 +51,9 @@ extern "C" {
 
 const char* amrb_last_error(void);
 int amrb_version(void);
+/* Kernel launches issued so far by this process (host-side count; launches
+ * replayed from a captured CUDA graph are not included). */
+int64_t amrb_launch_count(void);
 
 /* ------------------------------------------------------------------------ */
 /* Communication plans (host).  Records are CopyRecord(src, dst, src_box,    */

@@ -20,7 +20,12 @@ namespace amrb {
       throw ::amrb::Error(AMRB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Host-side tally of kernel launches issued by the library (graph replays are
+// not seen here; callers multiply captured launches by replays).
+void count_launch();
+
 inline void check_launch(const char* what) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error(AMRB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }

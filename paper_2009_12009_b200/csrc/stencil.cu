@@ -11,6 +11,7 @@
 // Work decomposition: a level's valid region is cut into tiles
 // (box, i0, j0, k0); one CTA per tile; threadIdx.x runs along k (unit
 // stride), threadIdx.y along j, and each thread marches along i.
+#include <atomic>
 #include <cfloat>
 #include <cstring>
 #include <memory>
@@ -23,6 +24,11 @@ namespace {
 thread_local std::string g_last_error;
 }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 const TileTable& Level::tiles(int ti, int tj, int tk) {
   auto key = std::make_tuple(ti, tj, tk);
@@ -570,6 +576,7 @@ using namespace amrb;
 
 extern "C" const char* amrb_last_error(void) { return amrb::g_last_error.c_str(); }
 extern "C" int amrb_version(void) { return 1; }
+extern "C" int64_t amrb_launch_count(void) { return (int64_t)amrb::g_launches.load(); }
 
 extern "C" int amrb_level_create(int nboxes, const int32_t* boxes, const uint8_t* resident, amrb_level** out) {
   return guarded([&] {
@@ -800,7 +807,10 @@ extern "C" int amrb_reduce(const amrb_level* lv_, const amrb_field* x, const dou
     const int n = (int)tt.host.size();
     if (lv.partials.n < (size_t)std::max(n, 1)) lv.partials.alloc(std::max(n, 1));
     cudaStream_t st = (cudaStream_t)stream;
-    if (n) launch_tiles(tt, k_reduce_tiles, st, dim3(32, 8), lv.dgeo.p, F(x).dev.p, x_base, comp, kind, lv.partials.p);
+    if (n) {
+      launch_tiles(tt, k_reduce_tiles, st, dim3(32, 8), lv.dgeo.p, F(x).dev.p, x_base, comp, kind, lv.partials.p);
+      check_launch("k_reduce_tiles");
+    }
     k_reduce_final<<<1, 1024, 0, st>>>(lv.partials.p, n, kind, dev_out);
     check_launch("k_reduce");
   });

@@ -117,6 +117,8 @@ class MLMG:
         top.resid = MultiFab(top.ba, top.dm, 1, 0)
         self.norm = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
         self.graph = None
+        self.graph_replays = 0
+        self.launches_per_cycle = 0
         self.iterations = 0
         self.history = []
         self.cell_updates_per_cycle = sum(
@@ -257,8 +259,10 @@ class MLMG:
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
+                self._cap_l0 = int(lib().amrb_launch_count())
                 self._cycle_and_norm()
         torch.cuda.current_stream().wait_stream(s)
+        self.launches_per_cycle = int(lib().amrb_launch_count()) - self._cap_l0
         self._graph_cur = [lv.cur for lv in self.levels]
         for lv, c in zip(self.levels, saved):
             lv.cur = c
@@ -298,6 +302,7 @@ class MLMG:
         while self.iterations < max_iter:
             if self.graph is not None:
                 self.graph.replay()
+                self.graph_replays += 1
                 for lv, c in zip(self.levels, self._graph_cur):
                     lv.cur = c
             else:
