@@ -323,6 +323,144 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
 }
 
 // ---------------------------------------------------------------------------
+// Fused sweep, full-tile fast path.  Same algorithm as k_gsrb_sweep, but
+//   * tile geometry is compile-time (every tile full: TJ | n1, TK | n2), so
+//     all index math is shifts / constant divisions and there are no bounds
+//     checks;
+//   * a 2-plane-deep cp.async pipeline: 6 phi slots, 4 rhs slots; at step p
+//     the loads of phi(p+4) and rhs(p+3) are issued while red(p+1) / black(p)
+//     compute, and only 2 barriers separate the phases of a plane.
+// Slot reuse (phi mod 6, rhs mod 4): phi(p+4) overwrites phi(p-2), last read
+// by black(p-1); rhs(p+3) overwrites rhs(p-1), last read by black(p-1); both
+// readers finish before the barrier that opens step p.
+// ---------------------------------------------------------------------------
+template <int TJ, int TK>
+struct Sweep2Smem {
+  static constexpr int PJ = TJ + 4, PK = TK + 4, RJ = TJ + 2;
+  double phi[6][PJ][PK];
+  double rhs[4][RJ][PK];
+};
+
+template <int TJ, int TK, bool FIXED>
+__global__ void __launch_bounds__(256, 2) k_gsrb_sweep_full(SweepArgs args) {
+  using SM = Sweep2Smem<TJ, TK>;
+  constexpr int PK = SM::PK;
+  constexpr int NT = 256;
+  constexpr int CH = PK / 2;                // 16-byte chunks per smem row
+  constexpr int RQ = TK / 2 + 1;            // red pairs per ring row
+  constexpr int RROWS = TJ + 2;             // ring rows
+  constexpr int BQ = TK / 2;                // black pairs per row
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int4 t = args.tiles[blockIdx.x];
+  const BoxGeom g = args.geo[t.x];
+  const FabView A = args.fa[t.x], B = args.fb[t.x], R = args.fr[t.x];
+  const Coef cf = args.cf;
+  const int i0 = t.y, j0 = t.z, k0 = t.w;
+  const int i1 = min(i0 + args.ci, g.n[0]);
+  const int tid = threadIdx.x + threadIdx.y * 32;
+  // global parity offset of (j0, k0): cell (ip, j0 + r, k0 + c) has parity (gi + jk0 + r + c) & 1
+  const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
+  const double* abase = args.a + A.off + (int64_t)(j0 - 2) * A.s1 + (k0 - 2);
+  const double* rbase = args.rhs + R.off + (int64_t)(j0 - 1) * R.s1 + (k0 - 2);
+
+  auto load_phi = [&](int ip) {
+    double* dst = &sm.phi[(ip + 12) % 6][0][0];
+    const double* src = abase + (int64_t)ip * A.s0;
+#pragma unroll 4
+    for (int e = tid; e < SM::PJ * CH; e += NT) {
+      const int r = e / CH, q = e - r * CH;
+      cp_async16(dst + r * PK + 2 * q, src + (int64_t)r * A.s1 + 2 * q);
+    }
+  };
+  auto load_rhs = [&](int ip) {
+    double* dst = &sm.rhs[(ip + 12) & 3][0][0];
+    const double* src = rbase + (int64_t)ip * R.s0;
+#pragma unroll 4
+    for (int e = tid; e < RROWS * CH; e += NT) {
+      const int r = e / CH, q = e - r * CH;
+      cp_async16(dst + r * PK + 2 * q, src + (int64_t)r * R.s1 + 2 * q);
+    }
+  };
+  auto fixed_cell = [&](int gi, int r, int c) {
+    // r, c: smem coordinates (row j0-2+r, col k0-2+c)
+    const int gj = g.lo[1] + j0 - 2 + r, gk = g.lo[2] + k0 - 2 + c;
+    return gi < args.fixed_lo[0] || gi > args.fixed_hi[0] || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] ||
+           gk < args.fixed_lo[2] || gk > args.fixed_hi[2];
+  };
+  auto red = [&](int ip) {
+    double(*P)[PK] = sm.phi[(ip + 12) % 6];
+    const double(*Pm)[PK] = sm.phi[(ip + 11) % 6];
+    const double(*Pp)[PK] = sm.phi[(ip + 13) % 6];
+    const double(*Rh)[PK] = sm.rhs[(ip + 12) & 3];
+    const int gi = g.lo[0] + ip;
+    const int base_par = (gi + jk0) & 1;
+    for (int e = tid; e < RROWS * RQ; e += NT) {
+      const int rr = e / RQ, q = e - rr * RQ;  // ring row rr <-> smem row rr+1
+      // ring pair q covers smem cols 2q+1, 2q+2 (k0-1+2q, k0+2q); cell (r, c)
+      // has parity (base_par + r + c) & 1 and red is even
+      const int r = rr + 1;
+      const int c = 2 * q + 1 + ((base_par + rr) & 1);
+      if (FIXED && fixed_cell(gi, r, c)) continue;
+      const double v = P[r][c];
+      const double lap = lap7(v, Pm[r][c], Pp[r][c], P[r - 1][c], P[r + 1][c], P[r][c - 1], P[r][c + 1], cf);
+      P[r][c] = relax(v, Rh[rr][c], lap, cf.gamma);
+    }
+  };
+  auto black_store = [&](int ip) {
+    double(*P)[PK] = sm.phi[(ip + 12) % 6];
+    const double(*Pm)[PK] = sm.phi[(ip + 11) % 6];
+    const double(*Pp)[PK] = sm.phi[(ip + 13) % 6];
+    const double(*Rh)[PK] = sm.rhs[(ip + 12) & 3];
+    const int gi = g.lo[0] + ip;
+    const int base_par = (gi + jk0) & 1;
+    double* out = args.b + B.off + (int64_t)ip * B.s0 + (int64_t)j0 * B.s1 + k0;
+#pragma unroll
+    for (int m = 0; m < (TJ * BQ + NT - 1) / NT; ++m) {
+      const int e = tid + m * NT;
+      if (TJ * BQ % NT != 0 && e >= TJ * BQ) break;
+      const int jj = e / BQ, q = e - jj * BQ;
+      const int r = jj + 2;
+      // pair cols 2q+2, 2q+3; black = odd parity: (base_par + jj + 2q + par) odd
+      const int par = (base_par + jj + 1) & 1;
+      const int c = 2 * q + 2 + par;
+      double bv = P[r][c];
+      if (!(FIXED && fixed_cell(gi, r, c))) {
+        const double lap = lap7(bv, Pm[r][c], Pp[r][c], P[r - 1][c], P[r + 1][c], P[r][c - 1], P[r][c + 1], cf);
+        bv = relax(bv, Rh[jj + 1][c], lap, cf.gamma);
+      }
+      // the pair's red member (already final) + the new black value
+      const double rv = P[r][par ? c - 1 : c + 1];
+      const double2 w = par ? make_double2(rv, bv) : make_double2(bv, rv);
+      *reinterpret_cast<double2*>(out + (int64_t)jj * B.s1 + 2 * q) = w;
+    }
+  };
+
+  // prologue
+  for (int ip = i0 - 2; ip <= i0 + 2; ++ip) load_phi(ip);
+  for (int ip = i0 - 1; ip <= i0 + 1; ++ip) load_rhs(ip);
+  cp_async_commit();
+  if (i0 + 3 <= i1 + 1) load_phi(i0 + 3);
+  if (i0 + 2 <= i1) load_rhs(i0 + 2);
+  cp_async_commit();
+  asm volatile("cp.async.wait_group 1;\n" ::);
+  __syncthreads();
+  red(i0 - 1);
+  red(i0);
+  for (int p = i0; p < i1; ++p) {
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    if (p + 4 <= i1 + 1) load_phi(p + 4);
+    if (p + 3 <= i1) load_rhs(p + 3);
+    cp_async_commit();
+    red(p + 1);
+    __syncthreads();
+    black_store(p);
+  }
+  cp_async_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // Restriction (ratio 2, box-local coarsened layout) and fused residual-restrict.
 // Tile over coarse boxes: 8 x 8 x 32 coarse cells.
 // ---------------------------------------------------------------------------
@@ -717,6 +855,37 @@ void launch_sweep(Level& lv, const Field& a, const double* a_base, const Field& 
   k_gsrb_sweep<TJ, TK><<<(unsigned)tt.host.size(), dim3(32, 8), smem, st>>>(args);
   check_launch("k_gsrb_sweep");
 }
+template <int TJ, int TK>
+void launch_sweep_full(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
+                       const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
+                       const int fixed_hi[3], bool fixed, cudaStream_t st) {
+  const auto& tt = lv.tiles(kSweepCI, TJ, TK);
+  if (tt.host.empty()) return;
+  SweepArgs args;
+  args.tiles = tt.dev.p;
+  args.geo = lv.dgeo.p;
+  args.fa = a.dev.p;
+  args.fb = b.dev.p;
+  args.fr = r.dev.p;
+  args.a = a_base;
+  args.b = b_base;
+  args.rhs = r_base;
+  args.cf = cf;
+  args.ci = kSweepCI;
+  for (int x = 0; x < 3; ++x) {
+    args.fixed_lo[x] = fixed_lo[x];
+    args.fixed_hi[x] = fixed_hi[x];
+  }
+  const size_t smem = sizeof(Sweep2Smem<TJ, TK>);
+  auto kern = fixed ? k_gsrb_sweep_full<TJ, TK, true> : k_gsrb_sweep_full<TJ, TK, false>;
+  static bool configured[2] = {false, false};
+  if (!configured[fixed]) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[fixed] = true;
+  }
+  kern<<<(unsigned)tt.host.size(), dim3(32, 8), smem, st>>>(args);
+  check_launch("k_gsrb_sweep_full");
+}
 }  // namespace
 
 extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const double* a_base, amrb_field* b,
@@ -734,14 +903,37 @@ extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const
         flo[x] = fixed_lohi[x];
         fhi[x] = fixed_lohi[3 + x];
       }
-    int maxk = 0;
-    for (auto& g : lv.geo) maxk = std::max(maxk, g.n[2]);
-    if (maxk >= 64)
-      launch_sweep<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
-                           (cudaStream_t)stream);
+    // full-tile fast path when every box is a multiple of the tile
+    int minj = 1 << 30, mink = 1 << 30, maxk = 0;
+    for (auto& g : lv.geo) {
+      minj = std::min(minj, g.n[1]);
+      mink = std::min(mink, g.n[2]);
+      maxk = std::max(maxk, g.n[2]);
+    }
+    auto divides = [&](int tj, int tk) {
+      for (auto& g : lv.geo)
+        if (g.n[1] % tj || g.n[2] % tk) return false;
+      return true;
+    };
+    const bool fixed = fixed_lohi != nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Coef cf = make_coef(dh);
+    if (divides(16, 64))
+      launch_sweep_full<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
+    else if (divides(16, 32))
+      launch_sweep_full<16, 32>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
+    else if (divides(16, 16))
+      launch_sweep_full<16, 16>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
+    else if (divides(8, 8))
+      launch_sweep_full<8, 8>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
+    else if (divides(4, 4))
+      launch_sweep_full<4, 4>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
+    else if (maxk >= 64)
+      launch_sweep<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, st);
     else
-      launch_sweep<16, 32>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
-                           (cudaStream_t)stream);
+      launch_sweep<16, 32>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, st);
+    (void)minj;
+    (void)mink;
   });
 }
 

@@ -69,7 +69,7 @@ def test_gsrb_color_bitexact(rng, n, m, lo):
             assert np.array_equal(got[i], pf[i])
 
 
-@pytest.mark.parametrize("n,m", [(16, 8), (32, 16), (64, 32), (128, 64), (8, 4), (8, 8)])
+@pytest.mark.parametrize("n,m", [(16, 8), (32, 16), (64, 32), (128, 64), (8, 4), (8, 8), (12, 6), (40, 20)])
 def test_fused_sweep_equals_fill_red_fill_black(rng, n, m):
     dom, ba, dm = _layout(n, m)
     tr = A.Transport(1)
