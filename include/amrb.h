@@ -153,7 +153,7 @@ int amrb_residual(const amrb_level* lv, amrb_field* r, double* r_base,
                   const double dh[3], void* stream);
 
 /* One GSRB colour: cells with (i+j+k+color) % 2 == 0 (global indices) get
- * phi += (rhs - L(phi)) / gamma, gamma = -2 (dh0+dh1+dh2). */
+ * phi += (rhs - L(phi)) * rgamma, rgamma = 1 / (-2 (dh0+dh1+dh2)). */
 int amrb_gsrb_color(const amrb_level* lv, amrb_field* phi, double* phi_base,
                     const amrb_field* rhs, const double* rhs_base,
                     const double dh[3], int color, void* stream);

@@ -12,7 +12,9 @@ SURVEY.md section 8(c):
   dh_d = 1/dx_d^2, dx from Geometry.cell_size (amr_core.py:37-40);
 * residual  r = rhs - L(phi);
 * GSRB      per colour c in (0, 1), cells with (i+j+k+c) % 2 == 0 in GLOBAL
-  index space: phi <- phi + (rhs - L(phi)) / gamma, gamma = -2*(dh0+dh1+dh2);
+  index space: phi <- phi + (rhs - L(phi)) * rgamma with rgamma = 1/gamma,
+  gamma = -2*(dh0+dh1+dh2) (the reciprocal is formed once, as upstream AMReX's
+  gsrb does with omega/gamma);
   one sweep = fill; colour 0; fill; colour 1 (width-1 fills);
 * hierarchy coarsen box-locally by 2 while every box extent is even and >= 8;
   then, if several boxes remain and the domain is still coarsenable (even,
@@ -73,6 +75,10 @@ def gamma_of(dh):
     return -2.0 * (dh[0] + dh[1] + dh[2])
 
 
+def rgamma_of(dh):
+    return 1.0 / gamma_of(dh)
+
+
 def laplacian(p, dh):
     """L(phi) over the valid region of a ghost-1 array p of shape (n0+2, n1+2, n2+2)."""
     c = p[1:-1, 1:-1, 1:-1]
@@ -102,7 +108,7 @@ def gsrb_color(box, p, rhs_valid, dh, color):
     Red cells read only black neighbours, so evaluating L on all cells and
     keeping the coloured ones equals the sequential definition."""
     c = p[1:-1, 1:-1, 1:-1]
-    new = c + (rhs_valid - laplacian(p, dh)) / gamma_of(dh)
+    new = c + (rhs_valid - laplacian(p, dh)) * rgamma_of(dh)
     np.copyto(c, new, where=color_mask(box[0], c.shape, color))
 
 

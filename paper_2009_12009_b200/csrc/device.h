@@ -73,6 +73,7 @@ struct DevArray {
 // Tiles of the valid region: (box, i0, j0, k0) in box-local valid coords.
 struct TileTable {
   int ti, tj, tk;
+  long long total = 0;  // column tables: plane-steps over all columns
   std::vector<int4> host;
   DevArray<int4> dev;
 };
@@ -88,6 +89,8 @@ struct Level {
     for (auto& kv : tables) delete kv.second;
   }
   const TileTable& tiles(int ti, int tj, int tk);
+  // (box, j0, k0, first plane-step) per TJ x TK column of the valid region
+  const TileTable& columns(int tj, int tk);
   bool all_even() const;
 };
 
@@ -98,5 +101,7 @@ struct Field {
   std::vector<FabView> host;
   DevArray<FabView> dev;
 };
+
+int num_sms();
 
 }  // namespace amrb

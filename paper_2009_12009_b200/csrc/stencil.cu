@@ -50,6 +50,40 @@ const TileTable& Level::tiles(int ti, int tj, int tk) {
   return *t;
 }
 
+const TileTable& Level::columns(int tj, int tk) {
+  auto key = std::make_tuple(-1, tj, tk);
+  auto it = tables.find(key);
+  if (it != tables.end()) return *it->second;
+  auto* t = new TileTable;
+  t->ti = -1;
+  t->tj = tj;
+  t->tk = tk;
+  long long acc = 0;
+  for (int b = 0; b < nboxes; ++b) {
+    if (!resident[b]) continue;
+    const BoxGeom& g = geo[b];
+    for (int j = 0; j < g.n[1]; j += tj)
+      for (int k = 0; k < g.n[2]; k += tk) {
+        t->host.push_back(make_int4(b, j, k, (int)acc));
+        acc += g.n[0];
+      }
+  }
+  t->total = acc;
+  t->dev.upload(t->host);
+  tables[key] = t;
+  return *t;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    AMRB_CUDA(cudaGetDevice(&dev));
+    AMRB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 bool Level::all_even() const {
   for (int b = 0; b < nboxes; ++b)
     for (int x = 0; x < 3; ++x)
@@ -60,7 +94,7 @@ bool Level::all_even() const {
 namespace {
 
 struct Coef {
-  double dh0, dh1, dh2, gamma;
+  double dh0, dh1, dh2, rgamma;  // rgamma = 1 / (-2 (dh0 + dh1 + dh2))
 };
 
 // 7-point operator, fixed operand order:
@@ -74,8 +108,8 @@ __device__ __forceinline__ double lap7(double c, double xm, double xp, double ym
   return (tx + ty) + tz;
 }
 
-__device__ __forceinline__ double relax(double c, double rhs, double lap, double gamma) {
-  return c + (rhs - lap) / gamma;
+__device__ __forceinline__ double relax(double c, double rhs, double lap, double rgamma) {
+  return c + (rhs - lap) * rgamma;
 }
 
 template <class T>
@@ -149,7 +183,7 @@ __global__ void __launch_bounds__(256)
     const double c = *pc;
     const double lap = lap7(c, pc[-P.s0], pc[P.s0], pc[-P.s1], pc[P.s1], pc[-1], pc[1], cf);
     const double b = rhs[R.off + (int64_t)i * R.s0 + (int64_t)j * R.s1 + k];
-    *pc = relax(c, b, lap, cf.gamma);
+    *pc = relax(c, b, lap, cf.rgamma);
   }
 }
 
@@ -257,7 +291,7 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
       const double v = sm.phi[s][r][c];
       const double lap = lap7(v, sm.phi[sm1][r][c], sm.phi[sp1][r][c], sm.phi[s][r - 1][c],
                               sm.phi[s][r + 1][c], sm.phi[s][r][c - 1], sm.phi[s][r][c + 1], cf);
-      sm.phi[s][r][c] = relax(v, sm.rhs[rs][rr][c], lap, cf.gamma);
+      sm.phi[s][r][c] = relax(v, sm.rhs[rs][rr][c], lap, cf.rgamma);
     }
   };
   auto black = [&](int ip) {
@@ -279,7 +313,7 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
       const double v = sm.phi[s][r][c];
       const double lap = lap7(v, sm.phi[sm1][r][c], sm.phi[sp1][r][c], sm.phi[s][r - 1][c],
                               sm.phi[s][r + 1][c], sm.phi[s][r][c - 1], sm.phi[s][r][c + 1], cf);
-      sm.phi[s][r][c] = relax(v, sm.rhs[rs][jj + 1][c], lap, cf.gamma);
+      sm.phi[s][r][c] = relax(v, sm.rhs[rs][jj + 1][c], lap, cf.rgamma);
     }
   };
   auto store = [&](int ip) {
@@ -323,141 +357,196 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused sweep, full-tile fast path.  Same algorithm as k_gsrb_sweep, but
-//   * tile geometry is compile-time (every tile full: TJ | n1, TK | n2), so
-//     all index math is shifts / constant divisions and there are no bounds
-//     checks;
-//   * a 2-plane-deep cp.async pipeline: 6 phi slots, 4 rhs slots; at step p
-//     the loads of phi(p+4) and rhs(p+3) are issued while red(p+1) / black(p)
-//     compute, and only 2 barriers separate the phases of a plane.
-// Slot reuse (phi mod 6, rhs mod 4): phi(p+4) overwrites phi(p-2), last read
-// by black(p-1); rhs(p+3) overwrites rhs(p-1), last read by black(p-1); both
-// readers finish before the barrier that opens step p.
+// Fused sweep, full-tile fast path (every box a multiple of TJ x TK in j, k).
+//
+// Persistent and balanced: the level's (box, j0, k0) columns are laid end to
+// end as one sequence of plane-steps; CTA b of G marches the contiguous range
+// [T*b/G, T*(b+1)/G), restarting its pipeline only where it crosses into the
+// next column.  Per step p:
+//   wait(phi p+2, rhs p+1); barrier; prefetch phi(p+4), rhs(p+3) (cp.async);
+//   red(p+1) over the ring-grown tile; barrier; black(p) + stream plane p out.
+// Shared planes are stored parity-split: cell (r, c) lives at [r][c & 1][c >> 1],
+// so the red (or black) cells of a row and their k-neighbours are unit-stride
+// across lanes (no bank conflicts).  phi slots rotate mod 6, rhs mod 4:
+// phi(p+4) overwrites phi(p-2) and rhs(p+3) overwrites rhs(p-1), whose last
+// readers (black(p-1)) finish before the barrier that opens step p.
 // ---------------------------------------------------------------------------
 template <int TJ, int TK>
-struct Sweep2Smem {
-  static constexpr int PJ = TJ + 4, PK = TK + 4, RJ = TJ + 2;
-  double phi[6][PJ][PK];
-  double rhs[4][RJ][PK];
+struct Sweep3Smem {
+  static constexpr int PJ = TJ + 4, RJ = TJ + 2, H = TK / 2 + 2;  // H: cells per parity half-row
+  double phi[6][PJ][2][H];
+  double rhs[4][RJ][2][H];
 };
 
+struct Sweep3Args {
+  const int4* cols;  // (box, j0, k0, first plane-step of the column)
+  int ncols;
+  long long total;  // plane-steps over all columns
+  const BoxGeom* geo;
+  const FabView* fa;
+  const FabView* fb;
+  const FabView* fr;
+  const double* a;
+  double* b;
+  const double* rhs;
+  Coef cf;
+  int fixed_lo[3], fixed_hi[3];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
 template <int TJ, int TK, bool FIXED>
-__global__ void __launch_bounds__(256, 2) k_gsrb_sweep_full(SweepArgs args) {
-  using SM = Sweep2Smem<TJ, TK>;
-  constexpr int PK = SM::PK;
+__global__ void __launch_bounds__(256, 2) k_gsrb_sweep3(Sweep3Args args) {
+  using SM = Sweep3Smem<TJ, TK>;
   constexpr int NT = 256;
-  constexpr int CH = PK / 2;                // 16-byte chunks per smem row
-  constexpr int RQ = TK / 2 + 1;            // red pairs per ring row
-  constexpr int RROWS = TJ + 2;             // ring rows
-  constexpr int BQ = TK / 2;                // black pairs per row
+  constexpr int PK = TK + 4;       // cells per smem row (k0-2 .. k0+TK+1)
+  constexpr int H = SM::H;
+  constexpr int LPR = TK / 2;      // lanes per row (one k-pair each)
+  constexpr int RPP = NT / LPR;    // rows per pass
+  static_assert(NT % LPR == 0, "tile width");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
-  const int4 t = args.tiles[blockIdx.x];
-  const BoxGeom g = args.geo[t.x];
-  const FabView A = args.fa[t.x], B = args.fb[t.x], R = args.fr[t.x];
+  const int tid = threadIdx.x;
+  const int q = tid % LPR;         // pair index inside a row
+  const int rsub = tid / LPR;      // row inside a pass
   const Coef cf = args.cf;
-  const int i0 = t.y, j0 = t.z, k0 = t.w;
-  const int i1 = min(i0 + args.ci, g.n[0]);
-  const int tid = threadIdx.x + threadIdx.y * 32;
-  // global parity offset of (j0, k0): cell (ip, j0 + r, k0 + c) has parity (gi + jk0 + r + c) & 1
-  const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
-  const double* abase = args.a + A.off + (int64_t)(j0 - 2) * A.s1 + (k0 - 2);
-  const double* rbase = args.rhs + R.off + (int64_t)(j0 - 1) * R.s1 + (k0 - 2);
 
-  auto load_phi = [&](int ip) {
-    double* dst = &sm.phi[(ip + 12) % 6][0][0];
-    const double* src = abase + (int64_t)ip * A.s0;
-#pragma unroll 4
-    for (int e = tid; e < SM::PJ * CH; e += NT) {
-      const int r = e / CH, q = e - r * CH;
-      cp_async16(dst + r * PK + 2 * q, src + (int64_t)r * A.s1 + 2 * q);
+  const long long G = gridDim.x;
+  long long s = args.total * blockIdx.x / G;
+  const long long e = args.total * (blockIdx.x + 1) / G;
+  if (s >= e) return;
+  int col = 0;
+  {
+    int lo = 0, hi = args.ncols - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (args.cols[mid].w <= s)
+        lo = mid;
+      else
+        hi = mid - 1;
     }
-  };
-  auto load_rhs = [&](int ip) {
-    double* dst = &sm.rhs[(ip + 12) & 3][0][0];
-    const double* src = rbase + (int64_t)ip * R.s0;
-#pragma unroll 4
-    for (int e = tid; e < RROWS * CH; e += NT) {
-      const int r = e / CH, q = e - r * CH;
-      cp_async16(dst + r * PK + 2 * q, src + (int64_t)r * R.s1 + 2 * q);
-    }
-  };
-  auto fixed_cell = [&](int gi, int r, int c) {
-    // r, c: smem coordinates (row j0-2+r, col k0-2+c)
-    const int gj = g.lo[1] + j0 - 2 + r, gk = g.lo[2] + k0 - 2 + c;
-    return gi < args.fixed_lo[0] || gi > args.fixed_hi[0] || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] ||
-           gk < args.fixed_lo[2] || gk > args.fixed_hi[2];
-  };
-  auto red = [&](int ip) {
-    double(*P)[PK] = sm.phi[(ip + 12) % 6];
-    const double(*Pm)[PK] = sm.phi[(ip + 11) % 6];
-    const double(*Pp)[PK] = sm.phi[(ip + 13) % 6];
-    const double(*Rh)[PK] = sm.rhs[(ip + 12) & 3];
-    const int gi = g.lo[0] + ip;
-    const int base_par = (gi + jk0) & 1;
-    for (int e = tid; e < RROWS * RQ; e += NT) {
-      const int rr = e / RQ, q = e - rr * RQ;  // ring row rr <-> smem row rr+1
-      // ring pair q covers smem cols 2q+1, 2q+2 (k0-1+2q, k0+2q); cell (r, c)
-      // has parity (base_par + r + c) & 1 and red is even
-      const int r = rr + 1;
-      const int c = 2 * q + 1 + ((base_par + rr) & 1);
-      if (FIXED && fixed_cell(gi, r, c)) continue;
-      const double v = P[r][c];
-      const double lap = lap7(v, Pm[r][c], Pp[r][c], P[r - 1][c], P[r + 1][c], P[r][c - 1], P[r][c + 1], cf);
-      P[r][c] = relax(v, Rh[rr][c], lap, cf.gamma);
-    }
-  };
-  auto black_store = [&](int ip) {
-    double(*P)[PK] = sm.phi[(ip + 12) % 6];
-    const double(*Pm)[PK] = sm.phi[(ip + 11) % 6];
-    const double(*Pp)[PK] = sm.phi[(ip + 13) % 6];
-    const double(*Rh)[PK] = sm.rhs[(ip + 12) & 3];
-    const int gi = g.lo[0] + ip;
-    const int base_par = (gi + jk0) & 1;
-    double* out = args.b + B.off + (int64_t)ip * B.s0 + (int64_t)j0 * B.s1 + k0;
-#pragma unroll
-    for (int m = 0; m < (TJ * BQ + NT - 1) / NT; ++m) {
-      const int e = tid + m * NT;
-      if (TJ * BQ % NT != 0 && e >= TJ * BQ) break;
-      const int jj = e / BQ, q = e - jj * BQ;
-      const int r = jj + 2;
-      // pair cols 2q+2, 2q+3; black = odd parity: (base_par + jj + 2q + par) odd
-      const int par = (base_par + jj + 1) & 1;
-      const int c = 2 * q + 2 + par;
-      double bv = P[r][c];
-      if (!(FIXED && fixed_cell(gi, r, c))) {
-        const double lap = lap7(bv, Pm[r][c], Pp[r][c], P[r - 1][c], P[r + 1][c], P[r][c - 1], P[r][c + 1], cf);
-        bv = relax(bv, Rh[jj + 1][c], lap, cf.gamma);
+    col = lo;
+  }
+  while (s < e) {
+    const int4 cd = args.cols[col];
+    const BoxGeom g = args.geo[cd.x];
+    const FabView A = args.fa[cd.x], B = args.fb[cd.x], R = args.fr[cd.x];
+    const int j0 = cd.y, k0 = cd.z;
+    const int i0 = (int)(s - cd.w);
+    const int i1 = (int)min((long long)g.n[0], e - cd.w);
+    s += i1 - i0;
+    ++col;
+    const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
+    const double* abase = args.a + A.off + (int64_t)(j0 - 2) * A.s1 + (k0 - 2);
+    const double* rbase = args.rhs + R.off + (int64_t)(j0 - 1) * R.s1 + (k0 - 2);
+    double* obase = args.b + B.off + (int64_t)j0 * B.s1 + k0;
+
+    auto load_phi = [&](int ip) {
+      double(*dst)[2][H] = sm.phi[(ip + 12) % 6];
+      const double* src = abase + (int64_t)ip * A.s0;
+#pragma unroll 2
+      for (int x = tid; x < SM::PJ * PK; x += NT) {
+        const int r = x / PK, c = x - r * PK;
+        cp_async8(&dst[r][c & 1][c >> 1], src + (int64_t)r * A.s1 + c);
       }
-      // the pair's red member (already final) + the new black value
-      const double rv = P[r][par ? c - 1 : c + 1];
-      const double2 w = par ? make_double2(rv, bv) : make_double2(bv, rv);
-      *reinterpret_cast<double2*>(out + (int64_t)jj * B.s1 + 2 * q) = w;
-    }
-  };
+    };
+    auto load_rhs = [&](int ip) {
+      double(*dst)[2][H] = sm.rhs[(ip + 12) & 3];
+      const double* src = rbase + (int64_t)ip * R.s0;
+#pragma unroll 2
+      for (int x = tid; x < SM::RJ * PK; x += NT) {
+        const int r = x / PK, c = x - r * PK;
+        cp_async8(&dst[r][c & 1][c >> 1], src + (int64_t)r * R.s1 + c);
+      }
+    };
+    auto is_fixed = [&](int gi, int r, int c) {
+      const int gj = g.lo[1] + j0 - 2 + r, gk = g.lo[2] + k0 - 2 + c;
+      return gi < args.fixed_lo[0] || gi > args.fixed_hi[0] || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] ||
+             gk < args.fixed_lo[2] || gk > args.fixed_hi[2];
+    };
+    // relax cell (r, c) of plane ip (smem coords); c's half h = c & 1, x = c >> 1
+    auto relax_cell = [&](double(*P)[2][H], const double(*Pm)[2][H], const double(*Pp)[2][H],
+                          const double(*Rh)[2][H], int r, int h, int x, int xl, int xr) {
+      const double v = P[r][h][x];
+      const double lap = lap7(v, Pm[r][h][x], Pp[r][h][x], P[r - 1][h][x], P[r + 1][h][x], P[r][h ^ 1][xl],
+                              P[r][h ^ 1][xr], cf);
+      return relax(v, Rh[r - 1][h][x], lap, cf.rgamma);
+    };
+    auto red = [&](int ip) {
+      double(*P)[2][H] = sm.phi[(ip + 12) % 6];
+      const double(*Pm)[2][H] = sm.phi[(ip + 11) % 6];
+      const double(*Pp)[2][H] = sm.phi[(ip + 13) % 6];
+      const double(*Rh)[2][H] = sm.rhs[(ip + 12) & 3];
+      const int gi = g.lo[0] + ip;
+      const int bp = (gi + jk0) & 1;  // parity of smem cell (r, c) = (bp + r + c) & 1
+      // interior pairs: cols 2q+2, 2q+3; red member c = 2q+2+off, off = (bp + r) & 1
+#pragma unroll
+      for (int m = 0; m < (TJ + 2 + RPP - 1) / RPP; ++m) {
+        const int r = 1 + rsub + m * RPP;  // ring rows 1 .. TJ+2
+        if ((TJ + 2) % RPP != 0 && r > TJ + 2) break;
+        const int off = (bp + r) & 1;
+        if (FIXED && is_fixed(gi, r, 2 * q + 2 + off)) continue;
+        P[r][off][q + 1] = relax_cell(P, Pm, Pp, Rh, r, off, q + 1, q + off, q + 1 + off);
+      }
+      // ring columns c = 1 (k0-1) and c = TK+2 (k0+TK)
+      if (tid < 2 * (TJ + 2)) {
+        const int r = 1 + (tid >> 1);
+        const int c = (tid & 1) ? TK + 2 : 1;
+        if (((bp + r + c) & 1) == 0 && !(FIXED && is_fixed(gi, r, c))) {
+          const int h = c & 1, x = c >> 1;
+          const int xl = (c - 1) >> 1, xr = (c + 1) >> 1;
+          P[r][h][x] = relax_cell(P, Pm, Pp, Rh, r, h, x, xl, xr);
+        }
+      }
+    };
+    auto black_store = [&](int ip) {
+      double(*P)[2][H] = sm.phi[(ip + 12) % 6];
+      const double(*Pm)[2][H] = sm.phi[(ip + 11) % 6];
+      const double(*Pp)[2][H] = sm.phi[(ip + 13) % 6];
+      const double(*Rh)[2][H] = sm.rhs[(ip + 12) & 3];
+      const int gi = g.lo[0] + ip;
+      const int bp = (gi + jk0) & 1;
+      double* out = obase + (int64_t)ip * B.s0;
+#pragma unroll
+      for (int m = 0; m < (TJ + RPP - 1) / RPP; ++m) {
+        const int r = 2 + rsub + m * RPP;  // rows 2 .. TJ+1
+        if (TJ % RPP != 0 && r > TJ + 1) break;
+        const int off = ((bp + r) & 1) ^ 1;  // black member of the pair
+        double bv = P[r][off][q + 1];
+        if (!(FIXED && is_fixed(gi, r, 2 * q + 2 + off))) bv = relax_cell(P, Pm, Pp, Rh, r, off, q + 1, q + off, q + 1 + off);
+        const double rv = P[r][off ^ 1][q + 1];
+        const double2 w = off ? make_double2(rv, bv) : make_double2(bv, rv);
+        *reinterpret_cast<double2*>(out + (int64_t)(r - 2) * B.s1 + 2 * q) = w;
+      }
+    };
 
-  // prologue
-  for (int ip = i0 - 2; ip <= i0 + 2; ++ip) load_phi(ip);
-  for (int ip = i0 - 1; ip <= i0 + 1; ++ip) load_rhs(ip);
-  cp_async_commit();
-  if (i0 + 3 <= i1 + 1) load_phi(i0 + 3);
-  if (i0 + 2 <= i1) load_rhs(i0 + 2);
-  cp_async_commit();
-  asm volatile("cp.async.wait_group 1;\n" ::);
-  __syncthreads();
-  red(i0 - 1);
-  red(i0);
-  for (int p = i0; p < i1; ++p) {
+    // prologue for this column segment
+    __syncthreads();  // previous segment's smem readers are done
+    for (int ip = i0 - 2; ip <= i0 + 2; ++ip) load_phi(ip);
+    for (int ip = i0 - 1; ip <= i0 + 1; ++ip) load_rhs(ip);
+    cp_async_commit();
+    if (i0 + 3 <= i1 + 1) load_phi(i0 + 3);
+    if (i0 + 2 <= i1) load_rhs(i0 + 2);
+    cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
-    if (p + 4 <= i1 + 1) load_phi(p + 4);
-    if (p + 3 <= i1) load_rhs(p + 3);
-    cp_async_commit();
-    red(p + 1);
-    __syncthreads();
-    black_store(p);
+    red(i0 - 1);
+    red(i0);
+    for (int p = i0; p < i1; ++p) {
+      asm volatile("cp.async.wait_group 1;\n" ::);
+      __syncthreads();
+      if (p + 4 <= i1 + 1) load_phi(p + 4);
+      if (p + 3 <= i1) load_rhs(p + 3);
+      cp_async_commit();
+      red(p + 1);
+      __syncthreads();
+      black_store(p);
+    }
+    cp_async_wait_all();
   }
-  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -685,7 +774,7 @@ Coef make_coef(const double dh[3]) {
   c.dh0 = dh[0];
   c.dh1 = dh[1];
   c.dh2 = dh[2];
-  c.gamma = -2.0 * ((dh[0] + dh[1]) + dh[2]);
+  c.rgamma = 1.0 / (-2.0 * ((dh[0] + dh[1]) + dh[2]));
   return c;
 }
 
@@ -859,10 +948,12 @@ template <int TJ, int TK>
 void launch_sweep_full(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                        const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
                        const int fixed_hi[3], bool fixed, cudaStream_t st) {
-  const auto& tt = lv.tiles(kSweepCI, TJ, TK);
-  if (tt.host.empty()) return;
-  SweepArgs args;
-  args.tiles = tt.dev.p;
+  const auto& cols = lv.columns(TJ, TK);
+  if (cols.host.empty()) return;
+  Sweep3Args args;
+  args.cols = cols.dev.p;
+  args.ncols = (int)cols.host.size();
+  args.total = cols.total;
   args.geo = lv.dgeo.p;
   args.fa = a.dev.p;
   args.fb = b.dev.p;
@@ -871,20 +962,23 @@ void launch_sweep_full(Level& lv, const Field& a, const double* a_base, const Fi
   args.b = b_base;
   args.rhs = r_base;
   args.cf = cf;
-  args.ci = kSweepCI;
   for (int x = 0; x < 3; ++x) {
     args.fixed_lo[x] = fixed_lo[x];
     args.fixed_hi[x] = fixed_hi[x];
   }
-  const size_t smem = sizeof(Sweep2Smem<TJ, TK>);
-  auto kern = fixed ? k_gsrb_sweep_full<TJ, TK, true> : k_gsrb_sweep_full<TJ, TK, false>;
-  static bool configured[2] = {false, false};
-  if (!configured[fixed]) {
+  const size_t smem = sizeof(Sweep3Smem<TJ, TK>);
+  auto kern = fixed ? k_gsrb_sweep3<TJ, TK, true> : k_gsrb_sweep3<TJ, TK, false>;
+  static int per_sm[2] = {0, 0};
+  if (!per_sm[fixed]) {
     AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[fixed] = true;
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[fixed], kern, 256, smem));
+    per_sm[fixed] = std::max(per_sm[fixed], 1);
   }
-  kern<<<(unsigned)tt.host.size(), dim3(32, 8), smem, st>>>(args);
-  check_launch("k_gsrb_sweep_full");
+  // enough CTAs to fill the chip, but >= 16 planes (or a whole column) each
+  long long want = std::max<long long>((long long)cols.host.size(), cols.total / 16);
+  long long grid = std::min<long long>((long long)per_sm[fixed] * num_sms(), want);
+  kern<<<(unsigned)std::max<long long>(grid, 1), 256, smem, st>>>(args);
+  check_launch("k_gsrb_sweep3");
 }
 }  // namespace
 
