@@ -402,17 +402,31 @@ template <int TJ, int TK, bool FIXED>
 __global__ void __launch_bounds__(256, 2) k_gsrb_sweep3(Sweep3Args args) {
   using SM = Sweep3Smem<TJ, TK>;
   constexpr int NT = 256;
-  constexpr int PK = TK + 4;       // cells per smem row (k0-2 .. k0+TK+1)
-  constexpr int H = SM::H;
-  constexpr int LPR = TK / 2;      // lanes per row (one k-pair each)
-  constexpr int RPP = NT / LPR;    // rows per pass
+  constexpr int PK = TK + 4;        // cells per smem row (k0-2 .. k0+TK+1)
+  constexpr int H = SM::H;          // cells per parity half-row
+  constexpr int ROW = 2 * H;        // doubles per smem row
+  constexpr int PSLOT = SM::PJ * ROW;
+  constexpr int RSLOT = SM::RJ * ROW;
+  constexpr int LPR = TK / 2;       // lanes per row (one k-pair each)
+  constexpr int RPP = NT / LPR;     // rows per pass
+  constexpr int NCP = (PK + 31) / 32;  // copies per lane per row
   static_assert(NT % LPR == 0, "tile width");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  double* const phi_s = &sm.phi[0][0][0][0];
+  double* const rhs_s = &sm.rhs[0][0][0][0];
   const int tid = threadIdx.x;
-  const int q = tid % LPR;         // pair index inside a row
-  const int rsub = tid / LPR;      // row inside a pass
+  const int lane = tid & 31, warp = tid >> 5;
+  const int q = tid % LPR;          // pair index inside a row
+  const int rsub = tid / LPR;       // row inside a pass
   const Coef cf = args.cf;
+  // per-lane split-parity smem offsets of the row elements this lane copies
+  int soff[NCP];
+#pragma unroll
+  for (int u = 0; u < NCP; ++u) {
+    const int c = lane + 32 * u;
+    soff[u] = (c & 1) * H + (c >> 1);
+  }
 
   const long long G = gridDim.x;
   long long s = args.total * blockIdx.x / G;
@@ -442,71 +456,67 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep3(Sweep3Args args) {
     const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
     const double* abase = args.a + A.off + (int64_t)(j0 - 2) * A.s1 + (k0 - 2);
     const double* rbase = args.rhs + R.off + (int64_t)(j0 - 1) * R.s1 + (k0 - 2);
-    double* obase = args.b + B.off + (int64_t)j0 * B.s1 + k0;
+    double* obase = args.b + B.off + (int64_t)j0 * B.s1 + k0 + 2 * q;
 
-    auto load_phi = [&](int ip) {
-      double(*dst)[2][H] = sm.phi[(ip + 12) % 6];
-      const double* src = abase + (int64_t)ip * A.s0;
-#pragma unroll 2
-      for (int x = tid; x < SM::PJ * PK; x += NT) {
-        const int r = x / PK, c = x - r * PK;
-        cp_async8(&dst[r][c & 1][c >> 1], src + (int64_t)r * A.s1 + c);
+    auto phi_slot = [&](int ip) { return phi_s + ((ip + 12) % 6) * PSLOT; };
+    auto rhs_slot = [&](int ip) { return rhs_s + ((ip + 12) & 3) * RSLOT; };
+    auto load_rows = [&](double* dst, const double* src, int64_t s1, int nrows) {
+      for (int r = warp; r < nrows; r += NT / 32) {
+        const double* gs = src + (int64_t)r * s1 + lane;
+        double* sd = dst + r * ROW;
+#pragma unroll
+        for (int u = 0; u < NCP; ++u)
+          if (lane + 32 * u < PK) cp_async8(sd + soff[u], gs + 32 * u);
       }
     };
-    auto load_rhs = [&](int ip) {
-      double(*dst)[2][H] = sm.rhs[(ip + 12) & 3];
-      const double* src = rbase + (int64_t)ip * R.s0;
-#pragma unroll 2
-      for (int x = tid; x < SM::RJ * PK; x += NT) {
-        const int r = x / PK, c = x - r * PK;
-        cp_async8(&dst[r][c & 1][c >> 1], src + (int64_t)r * R.s1 + c);
-      }
-    };
+    auto load_phi = [&](int ip) { load_rows(phi_slot(ip), abase + (int64_t)ip * A.s0, A.s1, SM::PJ); };
+    auto load_rhs = [&](int ip) { load_rows(rhs_slot(ip), rbase + (int64_t)ip * R.s0, R.s1, SM::RJ); };
     auto is_fixed = [&](int gi, int r, int c) {
       const int gj = g.lo[1] + j0 - 2 + r, gk = g.lo[2] + k0 - 2 + c;
       return gi < args.fixed_lo[0] || gi > args.fixed_hi[0] || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] ||
              gk < args.fixed_lo[2] || gk > args.fixed_hi[2];
     };
-    // relax cell (r, c) of plane ip (smem coords); c's half h = c & 1, x = c >> 1
-    auto relax_cell = [&](double(*P)[2][H], const double(*Pm)[2][H], const double(*Pp)[2][H],
-                          const double(*Rh)[2][H], int r, int h, int x, int xl, int xr) {
-      const double v = P[r][h][x];
-      const double lap = lap7(v, Pm[r][h][x], Pp[r][h][x], P[r - 1][h][x], P[r + 1][h][x], P[r][h ^ 1][xl],
-                              P[r][h ^ 1][xr], cf);
-      return relax(v, Rh[r - 1][h][x], lap, cf.rgamma);
+    // relax the cell at smem offset o (its half known through kl: the offset of
+    // its k-1 neighbour; k+1 is kl + 1).  rhs row = phi row - 1.
+    auto relax_at = [&](const double* P, const double* Pm, const double* Pp, const double* Rh, int o, int kl) {
+      const double v = P[o];
+      const double lap = lap7(v, Pm[o], Pp[o], P[o - ROW], P[o + ROW], P[kl], P[kl + 1], cf);
+      return relax(v, Rh[o - ROW], lap, cf.rgamma);
     };
     auto red = [&](int ip) {
-      double(*P)[2][H] = sm.phi[(ip + 12) % 6];
-      const double(*Pm)[2][H] = sm.phi[(ip + 11) % 6];
-      const double(*Pp)[2][H] = sm.phi[(ip + 13) % 6];
-      const double(*Rh)[2][H] = sm.rhs[(ip + 12) & 3];
+      double* P = phi_slot(ip);
+      const double* Pm = phi_slot(ip - 1);
+      const double* Pp = phi_slot(ip + 1);
+      const double* Rh = rhs_slot(ip);
       const int gi = g.lo[0] + ip;
       const int bp = (gi + jk0) & 1;  // parity of smem cell (r, c) = (bp + r + c) & 1
-      // interior pairs: cols 2q+2, 2q+3; red member c = 2q+2+off, off = (bp + r) & 1
+      // interior pairs: cols 2q+2, 2q+3 (half x = q+1); red member off = (bp + r) & 1
 #pragma unroll
       for (int m = 0; m < (TJ + 2 + RPP - 1) / RPP; ++m) {
         const int r = 1 + rsub + m * RPP;  // ring rows 1 .. TJ+2
         if ((TJ + 2) % RPP != 0 && r > TJ + 2) break;
         const int off = (bp + r) & 1;
         if (FIXED && is_fixed(gi, r, 2 * q + 2 + off)) continue;
-        P[r][off][q + 1] = relax_cell(P, Pm, Pp, Rh, r, off, q + 1, q + off, q + 1 + off);
+        const int o = r * ROW + off * H + q + 1;
+        const int kl = off ? o - H : o + H - 1;
+        P[o] = relax_at(P, Pm, Pp, Rh, o, kl);
       }
       // ring columns c = 1 (k0-1) and c = TK+2 (k0+TK)
       if (tid < 2 * (TJ + 2)) {
         const int r = 1 + (tid >> 1);
         const int c = (tid & 1) ? TK + 2 : 1;
         if (((bp + r + c) & 1) == 0 && !(FIXED && is_fixed(gi, r, c))) {
-          const int h = c & 1, x = c >> 1;
-          const int xl = (c - 1) >> 1, xr = (c + 1) >> 1;
-          P[r][h][x] = relax_cell(P, Pm, Pp, Rh, r, h, x, xl, xr);
+          const int o = r * ROW + (c & 1) * H + (c >> 1);
+          const int kl = r * ROW + ((c - 1) & 1) * H + ((c - 1) >> 1);
+          P[o] = relax_at(P, Pm, Pp, Rh, o, kl);
         }
       }
     };
     auto black_store = [&](int ip) {
-      double(*P)[2][H] = sm.phi[(ip + 12) % 6];
-      const double(*Pm)[2][H] = sm.phi[(ip + 11) % 6];
-      const double(*Pp)[2][H] = sm.phi[(ip + 13) % 6];
-      const double(*Rh)[2][H] = sm.rhs[(ip + 12) & 3];
+      const double* P = phi_slot(ip);
+      const double* Pm = phi_slot(ip - 1);
+      const double* Pp = phi_slot(ip + 1);
+      const double* Rh = rhs_slot(ip);
       const int gi = g.lo[0] + ip;
       const int bp = (gi + jk0) & 1;
       double* out = obase + (int64_t)ip * B.s0;
@@ -515,11 +525,13 @@ __global__ void __launch_bounds__(256, 2) k_gsrb_sweep3(Sweep3Args args) {
         const int r = 2 + rsub + m * RPP;  // rows 2 .. TJ+1
         if (TJ % RPP != 0 && r > TJ + 1) break;
         const int off = ((bp + r) & 1) ^ 1;  // black member of the pair
-        double bv = P[r][off][q + 1];
-        if (!(FIXED && is_fixed(gi, r, 2 * q + 2 + off))) bv = relax_cell(P, Pm, Pp, Rh, r, off, q + 1, q + off, q + 1 + off);
-        const double rv = P[r][off ^ 1][q + 1];
+        const int o = r * ROW + off * H + q + 1;
+        const int kl = off ? o - H : o + H - 1;
+        double bv = P[o];
+        if (!(FIXED && is_fixed(gi, r, 2 * q + 2 + off))) bv = relax_at(P, Pm, Pp, Rh, o, kl);
+        const double rv = off ? P[o - H] : P[o + H];
         const double2 w = off ? make_double2(rv, bv) : make_double2(bv, rv);
-        *reinterpret_cast<double2*>(out + (int64_t)(r - 2) * B.s1 + 2 * q) = w;
+        *reinterpret_cast<double2*>(out + (int64_t)(r - 2) * B.s1) = w;
       }
     };
 
