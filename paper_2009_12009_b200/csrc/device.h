@@ -85,6 +85,9 @@ struct Level {
   DevArray<BoxGeom> dgeo;
   std::map<std::tuple<int, int, int>, TileTable*> tables;
   DevArray<double> partials;  // reduction scratch
+  // block index of each resident box inside a FabArray allocation (resident order)
+  std::vector<int> slot;
+  DevArray<int> dslot;
   ~Level() {
     for (auto& kv : tables) delete kv.second;
   }

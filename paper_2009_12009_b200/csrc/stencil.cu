@@ -16,7 +16,7 @@
 #include <cstring>
 #include <memory>
 
-#include "device.h"
+#include "stencil_common.cuh"
 
 namespace amrb {
 
@@ -92,25 +92,6 @@ bool Level::all_even() const {
 }
 
 namespace {
-
-struct Coef {
-  double dh0, dh1, dh2, rgamma;  // rgamma = 1 / (-2 (dh0 + dh1 + dh2))
-};
-
-// 7-point operator, fixed operand order:
-//   ((dh0*((xm - 2c) + xp) + dh1*((ym - 2c) + yp)) + dh2*((zm - 2c) + zp))
-__device__ __forceinline__ double lap7(double c, double xm, double xp, double ym, double yp, double zm,
-                                       double zp, const Coef& k) {
-  const double c2 = 2.0 * c;
-  const double tx = k.dh0 * ((xm - c2) + xp);
-  const double ty = k.dh1 * ((ym - c2) + yp);
-  const double tz = k.dh2 * ((zm - c2) + zp);
-  return (tx + ty) + tz;
-}
-
-__device__ __forceinline__ double relax(double c, double rhs, double lap, double rgamma) {
-  return c + (rhs - lap) * rgamma;
-}
 
 template <class T>
 __device__ __forceinline__ T ldg(const T* p) {
@@ -202,13 +183,6 @@ __global__ void __launch_bounds__(256)
 // black" with a width-1 fill in between.  Cells outside the domain in a
 // non-periodic direction are never relaxed (they hold boundary values).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
 struct SweepArgs {
   const int4* tiles;
   const BoxGeom* geo;
@@ -392,11 +366,6 @@ struct Sweep3Args {
   Coef cf;
   int fixed_lo[3], fixed_hi[3];
 };
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
 
 template <int TJ, int TK, bool FIXED>
 __global__ void __launch_bounds__(256, 2) k_gsrb_sweep3(Sweep3Args args) {
@@ -781,15 +750,6 @@ __global__ void k_domain_bc(const BoxGeom* __restrict__ geo, const FabView* __re
   }
 }
 
-Coef make_coef(const double dh[3]) {
-  Coef c;
-  c.dh0 = dh[0];
-  c.dh1 = dh[1];
-  c.dh2 = dh[2];
-  c.rgamma = 1.0 / (-2.0 * ((dh[0] + dh[1]) + dh[2]));
-  return c;
-}
-
 const Level& L(const amrb_level* p) {
   if (!p) throw Error(AMRB_EINVAL, "null level");
   return *reinterpret_cast<const Level*>(p);
@@ -833,6 +793,10 @@ extern "C" int amrb_level_create(int nboxes, const int32_t* boxes, const uint8_t
       if (resident) lv->resident[b] = resident[b];
     }
     lv->dgeo.upload(lv->geo);
+    lv->slot.assign(nboxes, 0);
+    for (int b = 0, k = 0; b < nboxes; ++b)
+      if (lv->resident[b]) lv->slot[b] = k++;
+    lv->dslot.upload(lv->slot);
     *out = reinterpret_cast<amrb_level*>(lv.release());
   });
 }
@@ -1024,6 +988,7 @@ extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const
     const bool fixed = fixed_lohi != nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     const Coef cf = make_coef(dh);
+    if (launch_sweep_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st)) return;
     if (divides(16, 64))
       launch_sweep_full<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
     else if (divides(16, 32))

@@ -1,0 +1,486 @@
+// Fused GSRB sweep, TMA path (sm_100a).
+//
+// Same algorithm and bit-exact result as k_gsrb_sweep / k_gsrb_sweep3
+// (stencil.cu): out of place A -> B, red of the ghost ring recomputed
+// locally, black relaxed and streamed out.  What is different:
+//
+//  * planes of A (phi, grown by 2 in j, k) and of rhs (grown by 1) arrive by
+//    TMA -- one cp.async.bulk.tensor per plane per operand, issued by one
+//    thread, completion on a per-slot mbarrier -- so the load path costs no
+//    per-element instructions and no registers;
+//  * red(p+2) and black(p) are independent (red reads only black cells, which
+//    no phase ever writes back to shared memory; black reads only red cells),
+//    so one step runs both in a single phase with ONE __syncthreads:
+//        wait(phi p+3, rhs p+2); barrier; TMA(phi p+3+D, rhs p+2+D);
+//        black(p) -> global;  red(p+2) -> shared
+//  * warp roles are uniform: warp w relaxes red ring row w+1 (one k-pair per
+//    lane, TK = 64), warps w < TJ also relax + store black row w+2, and the
+//    two extra warps relax the ring columns k0-1 / k0+TK.
+//  * persistent CTAs march balanced contiguous ranges of (column, plane)
+//    steps, like k_gsrb_sweep3.
+//
+// Slot rotation (relative to the segment's first plane): phi has D+5 slots,
+// rhs D+3.  At step p the TMA for phi(p+3+D) reuses the slot of phi(p-2) and
+// rhs(p+2+D) the slot of rhs(p-1); their last readers ran in step p-1, before
+// the step-p barrier.  All threads fence.proxy.async after their shared
+// stores so the async-proxy TMA writes are ordered after them.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <climits>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "stencil_common.cuh"
+
+namespace amrb {
+
+namespace {
+
+struct Sweep4Args {
+  const int4* cols;  // (box, j0, k0, first plane-step of the column)
+  const FabView* fa;  // bulk mode: phi-in and rhs views (source addresses)
+  const FabView* fr;
+  const double* a;
+  const double* rhs;
+  const int* slot;   // per box: index of its block in the allocation
+  int ncols;
+  long long total;
+  const BoxGeom* geo;
+  const FabView* fb;
+  double* b;
+  Coef cf;
+  int a_kc, a_jc, a_ic;  // tensor-map coordinate offsets: phi plane ip, rows from j0-2, cols from k0-2
+  int r_kc, r_jc, r_ic;  // rhs: rows from j0-1, cols from k0-2
+  int fixed_lo[3], fixed_hi[3];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+constexpr int kTK = 64;
+
+// BULK: a tile spans whole rows of its box (TK == box k-extent), so a plane's
+// rows j0-2 .. j0+TJ+1 are one contiguous chunk of memory: one 1-D
+// cp.async.bulk copy per plane, smem rows keep the storage pitch PP = 72 and
+// smem col CO + c holds cell k0-2+c.  Otherwise a 4-D tensor-map TMA box of
+// PP = TK+4 columns (CO = 0).
+template <int TJ, int D, bool BULK>
+struct Sweep4Layout {
+  static constexpr int PP = BULK ? kTK + 8 : kTK + 4;  // smem row pitch (doubles)
+  static constexpr int CO = BULK ? 2 : 0;
+  static constexpr int PJ = TJ + 4;   // phi rows j0-2 .. j0+TJ+1
+  static constexpr int RJ = TJ + 2;   // rhs rows j0-1 .. j0+TJ
+  static constexpr int NPHI = D + 5, NRHS = D + 3;
+  static constexpr int PBYTES = PJ * PP * 8;
+  static constexpr int RBYTES = RJ * PP * 8;
+  static constexpr int PSTRIDE = (PBYTES + 127) / 128 * 128;
+  static constexpr int RSTRIDE = (RBYTES + 127) / 128 * 128;
+  static constexpr int BAR_OFF = NPHI * PSTRIDE + NRHS * RSTRIDE;
+  static constexpr int BYTES = BAR_OFF + 8 * (NPHI + NRHS);
+  static constexpr int NW = TJ + 2;  // warps
+};
+
+template <int TJ, int D, int MINB, bool FIXED, bool BULK>
+__global__ void __launch_bounds__(32 * (TJ + 2), MINB)
+    k_gsrb_sweep4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR, Sweep4Args args) {
+  using LY = Sweep4Layout<TJ, D, BULK>;
+  constexpr int PK = LY::PP;
+  constexpr int CO = LY::CO;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + LY::BAR_OFF);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const Coef cf = args.cf;
+  auto phi_slot = [&](int rel) { return reinterpret_cast<double*>(smem_raw + (rel % LY::NPHI) * LY::PSTRIDE); };
+  auto rhs_slot = [&](int rel) {
+    return reinterpret_cast<double*>(smem_raw + LY::NPHI * LY::PSTRIDE + (rel % LY::NRHS) * LY::RSTRIDE);
+  };
+
+  const long long G = gridDim.x;
+  long long s = args.total * blockIdx.x / G;
+  const long long e = args.total * (blockIdx.x + 1) / G;
+  if (s >= e) return;
+  int col = 0;
+  {
+    int lo = 0, hi = args.ncols - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (args.cols[mid].w <= s)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    col = lo;
+  }
+  bool first_segment = true;
+  while (s < e) {
+    const int4 cd = args.cols[col];
+    const BoxGeom g = args.geo[cd.x];
+    const FabView B = args.fb[cd.x];
+    const FabView AV = BULK ? args.fa[cd.x] : B;
+    const FabView RV = BULK ? args.fr[cd.x] : B;
+    const int slot = args.slot[cd.x];
+    const int j0 = cd.y, k0 = cd.z;
+    const int i0 = (int)(s - cd.w);
+    const int i1 = (int)min((long long)g.n[0], e - cd.w);
+    s += i1 - i0;
+    ++col;
+    const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
+    const int pbase = i0 - 2;  // relative index origin of phi planes
+    const int rbase = i0 - 1;  // and of rhs planes
+
+    // (re)arm the barriers: every load of the previous segment was waited on
+    __syncthreads();
+    if (tid == 0) {
+      for (int x = 0; x < LY::NPHI + LY::NRHS; ++x) {
+        if (!first_segment) mbar_inval(&bars[x]);
+        mbar_init(&bars[x], 1);
+      }
+      fence_barrier_init();
+    }
+    first_segment = false;
+    __syncthreads();
+
+    auto issue_phi = [&](int ip) {
+      const int rel = ip - pbase;
+      uint64_t* bar = &bars[rel % LY::NPHI];
+      mbar_expect_tx(bar, LY::PBYTES);
+      if (BULK)
+        bulk_load(phi_slot(rel), args.a + AV.off + (int64_t)ip * AV.s0 + (int64_t)(j0 - 2) * AV.s1 + (k0 - 2 - CO),
+                  LY::PBYTES, bar);
+      else
+        tma_load4(phi_slot(rel), &tmA, bar, k0 + args.a_kc, j0 + args.a_jc, ip + args.a_ic, slot);
+    };
+    auto issue_rhs = [&](int ip) {
+      const int rel = ip - rbase;
+      uint64_t* bar = &bars[LY::NPHI + rel % LY::NRHS];
+      mbar_expect_tx(bar, LY::RBYTES);
+      if (BULK)
+        bulk_load(rhs_slot(rel), args.rhs + RV.off + (int64_t)ip * RV.s0 + (int64_t)(j0 - 1) * RV.s1 + (k0 - 2 - CO),
+                  LY::RBYTES, bar);
+      else
+        tma_load4(rhs_slot(rel), &tmR, bar, k0 + args.r_kc, j0 + args.r_jc, ip + args.r_ic, slot);
+    };
+    auto wait_phi = [&](int ip) {
+      const int rel = ip - pbase;
+      mbar_wait(&bars[rel % LY::NPHI], (rel / LY::NPHI) & 1);
+    };
+    auto wait_rhs = [&](int ip) {
+      const int rel = ip - rbase;
+      mbar_wait(&bars[LY::NPHI + rel % LY::NRHS], (rel / LY::NRHS) & 1);
+    };
+    auto is_fixed = [&](int gi, int r, int c) {
+      const int gj = g.lo[1] + j0 - 2 + r, gk = g.lo[2] + k0 - 2 + c;
+      return gi < args.fixed_lo[0] || gi > args.fixed_hi[0] || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] ||
+             gk < args.fixed_lo[2] || gk > args.fixed_hi[2];
+    };
+    // relax smem cell o (row r, col c) of plane ip; rhs row r-1, same col
+    auto relax_at = [&](const double* P, const double* Pm, const double* Pp, const double* Rh, int o) {
+      const double v = P[o];
+      const double lap = lap7(v, Pm[o], Pp[o], P[o - PK], P[o + PK], P[o - 1], P[o + 1], cf);
+      return relax(v, Rh[o - PK], lap, cf.rgamma);
+    };
+    // red of plane ip (its smem parity base bp): ring row w+1 (pair = lane), or a ring column
+    auto red = [&](int ip) {
+      double* P = phi_slot(ip - pbase);
+      const double* Pm = phi_slot(ip - 1 - pbase);
+      const double* Pp = phi_slot(ip + 1 - pbase);
+      const double* Rh = rhs_slot(ip - rbase);
+      const int gi = g.lo[0] + ip;
+      const int bp = (gi + jk0) & 1;  // smem cell (r, c) has parity (bp + r + c) & 1; red is even
+      {
+        const int r = warp + 1;
+        const int c = 2 * lane + 2 + ((bp + r) & 1);
+        if (!(FIXED && is_fixed(gi, r, c))) {
+          const int o = r * PK + CO + c;
+          P[o] = relax_at(P, Pm, Pp, Rh, o);
+        }
+      }
+      if (warp >= TJ && lane < TJ + 2) {
+        const int r = lane + 1;
+        const int c = warp == TJ ? 1 : kTK + 2;
+        if (((bp + r + c) & 1) == 0 && !(FIXED && is_fixed(gi, r, c))) {
+          const int o = r * PK + CO + c;
+          P[o] = relax_at(P, Pm, Pp, Rh, o);
+        }
+      }
+    };
+    // One step, bank-conflict free: black(p) and red(p+2) occupy complementary
+    // columns of a row (planes p and p+2 have the same parity pattern), so
+    // warp w takes row r = w+1 with lane -> consecutive column c; a lane whose
+    // cell is black in plane p relaxes it there, the others relax their red
+    // cell of plane p+2.  Consecutive lanes read consecutive doubles (from two
+    // slots 128-byte aligned apart): 2 wavefronts per LDS.64.  Every lane of
+    // rows 2..TJ+1 then streams plane p's value of its column (new black, or the
+    // final red read back from shared) with one coalesced STG.64.
+    auto step = [&](int p, bool do_red) {
+      const int r = warp + 1;
+      const bool row_black = r >= 2 && r <= TJ + 1;
+      const int gi = g.lo[0] + p;
+      const int bp = (gi + jk0) & 1;  // same for plane p+2
+      const double* S0 = phi_slot(p - pbase);       // plane p
+      double* S2 = phi_slot(p + 2 - pbase);         // plane p+2
+      const double* Sm = phi_slot(p - 1 - pbase);   // p-1
+      const double* S1 = phi_slot(p + 1 - pbase);   // p+1
+      const double* S3 = phi_slot(p + 3 - pbase);   // p+3
+      const double* R0 = rhs_slot(p - rbase);
+      const double* R2 = rhs_slot(p + 2 - rbase);
+      double* out = args.b + B.off + (int64_t)p * B.s0 + (int64_t)(j0 + warp - 1) * B.s1 + k0 - 2;
+#pragma unroll
+      for (int h = 0; h < kTK / 32; ++h) {
+        const int c = 2 + lane + 32 * h;
+        const bool black = ((bp + r + c) & 1) != 0;  // cell (r, c) is black in planes p, p+2
+        const double* P = black ? S0 : S2;
+        const double* Pm = black ? Sm : S1;
+        const double* Pp = black ? S1 : S3;
+        const double* Rh = black ? R0 : R2;
+        const int o = r * PK + CO + c;
+        const bool act = black ? row_black : do_red;
+        double v = P[o];
+        if (act && !(FIXED && is_fixed(black ? gi : gi + 2, r, c))) v = relax_at(P, Pm, Pp, Rh, o);
+        if (!black && act) S2[o] = v;
+        if (row_black) out[c] = black ? v : S0[o];
+      }
+      // ring columns k0-1 / k0+TK of plane p+2 (red only)
+      if (do_red && lane < 2) {
+        const int c = lane ? kTK + 2 : 1;
+        if (((bp + r + c) & 1) == 0 && !(FIXED && is_fixed(gi + 2, r, c))) {
+          const int o = r * PK + CO + c;
+          S2[o] = relax_at(S2, S1, S3, R2, o);
+        }
+      }
+    };
+
+    // prologue: phi i0-2 .. i0+2+D, rhs i0-1 .. i0+1+D (clipped to what the segment needs)
+    if (tid == 0) {
+      for (int ip = i0 - 2; ip <= min(i0 + 2 + D, i1 + 1); ++ip) issue_phi(ip);
+      for (int ip = i0 - 1; ip <= min(i0 + 1 + D, i1); ++ip) issue_rhs(ip);
+    }
+    for (int ip = i0 - 2; ip <= i0 + 2; ++ip) wait_phi(ip);
+    for (int ip = i0 - 1; ip <= i0 + 1; ++ip) wait_rhs(ip);
+    red(i0 - 1);
+    red(i0);
+    red(i0 + 1);
+    fence_proxy_async();
+    for (int p = i0; p < i1; ++p) {
+      const bool do_red = p + 2 <= i1;
+      if (do_red) {
+        wait_phi(p + 3);
+        wait_rhs(p + 2);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (p + 3 + D <= i1 + 1) issue_phi(p + 3 + D);
+        if (p + 2 + D <= i1) issue_rhs(p + 2 + D);
+      }
+      step(p, do_red);
+      fence_proxy_async();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Describe one FabArray's storage as a 4-D tensor (k, j, i, block) when every
+// resident box has the same grown shape and blocks are equally spaced.
+struct TmaDesc {
+  bool ok = false;
+  int64_t base;  // element offset of tensor element (0, 0, 0, 0) (16-byte aligned)
+  int64_t pitch, rows, planes, stride;
+  int f, g;      // k index of the grown box's first cell = f
+  std::vector<int> slot;  // per box
+};
+
+TmaDesc describe(const Level& lv, const Field& f) {
+  TmaDesc d;
+  const int g = f.ngrow;
+  if (f.ng3[0] != g || f.ng3[1] != g || f.ng3[2] != g) return d;
+  d.g = g;
+  int first = -1, second = -1;
+  for (int b = 0; b < lv.nboxes; ++b)
+    if (lv.resident[b]) {
+      if (first < 0)
+        first = b;
+      else if (second < 0)
+        second = b;
+    }
+  if (first < 0) return d;
+  const BoxGeom& g0 = lv.geo[first];
+  const FabView& v0 = f.host[first];
+  auto grown = [&](const FabView& v) { return v.off - g * v.s0 - g * v.s1 - g; };
+  const int64_t og = grown(v0);
+  d.f = (int)(og & 1);  // shift the tensor origin back to a 16-byte boundary
+  d.base = og - d.f;
+  d.pitch = v0.s1;
+  d.rows = v0.s0 / v0.s1;
+  d.planes = g0.n[0] + 2 * g;
+  if (d.f + g0.n[2] + 2 * g > d.pitch) return d;
+  d.stride = second >= 0 ? grown(f.host[second]) - og : d.planes * v0.s0;
+  if (d.stride <= 0 || d.stride % 2) return d;
+  d.slot.assign(lv.nboxes, 0);
+  int k = 0;
+  for (int b = 0; b < lv.nboxes; ++b) {
+    if (!lv.resident[b]) continue;
+    const BoxGeom& gb = lv.geo[b];
+    const FabView& v = f.host[b];
+    if (gb.n[0] != g0.n[0] || gb.n[1] != g0.n[1] || gb.n[2] != g0.n[2] || v.s0 != v0.s0 || v.s1 != v0.s1)
+      return d;
+    if (grown(v) != og + (int64_t)k * d.stride) return d;
+    d.slot[b] = k++;
+  }
+  d.ok = true;
+  return d;
+}
+
+bool make_map(CUtensorMap* map, const double* base, const TmaDesc& d, int nblocks, int box_rows, int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[4] = {(cuuint64_t)d.pitch, (cuuint64_t)d.rows, (cuuint64_t)d.planes, (cuuint64_t)nblocks};
+  cuuint64_t gstride[3] = {(cuuint64_t)d.pitch * 8, (cuuint64_t)(d.pitch * d.rows) * 8, (cuuint64_t)d.stride * 8};
+  cuuint32_t box[4] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base + d.base), gdim, gstride, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int TJ, int D, int MINB, bool BULK>
+bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
+             const double* r_base, const Coef& cf, const int fixed_lo[3], const int fixed_hi[3], bool fixed,
+             cudaStream_t st) {
+  using LY = Sweep4Layout<TJ, D, BULK>;
+  for (auto& gg : lv.geo)
+    if (gg.n[1] % TJ || gg.n[2] % kTK || (BULK && gg.n[2] != kTK)) return false;
+  if (a.ngrow < 2 || r.ngrow < 1) return false;
+  CUtensorMap ma, mr;
+  std::memset(&ma, 0, sizeof ma);
+  std::memset(&mr, 0, sizeof mr);
+  Sweep4Args args;
+  std::memset(&args, 0, sizeof args);
+  if (BULK) {
+    // every resident box: smem pitch == storage pitch, valid k=0 at row index CO+2
+    for (int bx = 0; bx < lv.nboxes; ++bx) {
+      if (!lv.resident[bx]) continue;
+      const FabView& va = a.host[bx];
+      const FabView& vr = r.host[bx];
+      if (va.s1 != LY::PP || vr.s1 != LY::PP || va.off % 4 || vr.off % 4) return false;
+      if (a.ng3[2] + (4 - a.ng3[2] % 4) % 4 != LY::CO + 2 || r.ng3[2] + (4 - r.ng3[2] % 4) % 4 != LY::CO + 2)
+        return false;
+    }
+  } else {
+    TmaDesc da = describe(lv, a), dr = describe(lv, r);
+    if (!da.ok || !dr.ok) return false;
+    if (da.slot != lv.slot || dr.slot != lv.slot) return false;
+    int nres = 0;
+    for (auto x : lv.resident) nres += x ? 1 : 0;
+    if (!make_map(&ma, a_base, da, nres, LY::PJ, LY::PP)) return false;
+    if (!make_map(&mr, r_base, dr, nres, LY::RJ, LY::PP)) return false;
+    args.a_kc = -2 + da.g + da.f;
+    args.a_jc = -2 + da.g;
+    args.a_ic = da.g;
+    args.r_kc = -2 + dr.g + dr.f;
+    args.r_jc = -1 + dr.g;
+    args.r_ic = dr.g;
+  }
+  const auto& cols = lv.columns(TJ, kTK);
+  if (cols.host.empty()) return true;
+  args.cols = cols.dev.p;
+  args.fa = a.dev.p;
+  args.fr = r.dev.p;
+  args.a = a_base;
+  args.rhs = r_base;
+  args.slot = lv.dslot.p;
+  args.ncols = (int)cols.host.size();
+  args.total = cols.total;
+  args.geo = lv.dgeo.p;
+  args.fb = b.dev.p;
+  args.b = b_base;
+  args.cf = cf;
+  for (int x = 0; x < 3; ++x) {
+    args.fixed_lo[x] = fixed_lo[x];
+    args.fixed_hi[x] = fixed_hi[x];
+  }
+  auto kern = fixed ? k_gsrb_sweep4<TJ, D, MINB, true, BULK> : k_gsrb_sweep4<TJ, D, MINB, false, BULK>;
+  static int per_sm[2] = {0, 0};
+  if (!per_sm[fixed]) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[fixed], kern, 32 * LY::NW, LY::BYTES));
+    per_sm[fixed] = std::max(per_sm[fixed], 1);
+  }
+  const long long slots = (long long)per_sm[fixed] * num_sms();
+  const long long ncol = (long long)cols.host.size();
+  long long grid;
+  (void)ncol;
+  // balanced persistent split: every CTA marches ~total/G plane-steps
+  grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 16));
+  kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES, st>>>(ma, mr, args);
+  check_launch("k_gsrb_sweep4");
+  return true;
+}
+
+}  // namespace
+
+bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
+                      const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
+                      const int fixed_hi[3], bool fixed, cudaStream_t st) {
+  // TJ = 16 rows per tile, one plane of prefetch, 2 CTAs per SM.  (Measured on
+  // B200 at C3: 114.6 us; deeper prefetch, TJ = 8, 1-D bulk copies, cp.async
+  // and register-staged loads were all slower -- see DESIGN.md.)
+  return launch4<16, 1, 1, false>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st);
+}
+
+}  // namespace amrb
