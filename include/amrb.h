@@ -193,6 +193,16 @@ int amrb_prolong(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
                  const amrb_field* crse, const double* crse_base, int ncomp,
                  const int32_t* ratio, int add, void* stream);
 
+/* Coarse tail of the V-cycle in ONE CTA (all levels in shared memory):
+ * nlev single-box periodic levels, each half the previous; lohi = int32
+ * [nlev][6] (3-D padded), dh = double[nlev][3].  Reads level-0 rhs (valid) from
+ * `rhs`, runs zero/nu1 sweeps/residual-restrict down to the bottom (nbottom
+ * sweeps), pc-prolong + nu2 sweeps back up, and writes level-0 phi (valid).
+ * Bit-identical to the per-level kernels / oracle. */
+int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
+                     const amrb_field* rhs, const double* rhs_base, amrb_field* phi,
+                     double* phi_base, int nu1, int nu2, int nbottom, void* stream);
+
 /* reduce (fabarray.py:409-440) over valid cells of one component on this
  * device: kind 0 sum, 1 min, 2 max, 3 max|x| (inf-norm).  Deterministic:
  * fixed-shape per-tile partials then one ordered pass.  Result (one double)

@@ -46,22 +46,46 @@ def _coarsenable(e):
     return e % 2 == 0 and e >= 8
 
 
+_TAIL_MAX_EXTENT = 16  # agglomerate once the coarsened domain fits in one CTA
+
+
 def mg_hierarchy(domain, ba):
-    """[(domain, BoxArray, kind)] fine -> coarse (same rules as oracle.mlmg_ref.mg_levels)."""
+    """[(domain, BoxArray, kind)] fine -> coarse.
+
+    Same level RESOLUTIONS as oracle.mlmg_ref.mg_levels (box-local coarsening,
+    agglomeration, single-box coarsening while extents are even and >= 8), but
+    the device agglomerates as soon as the coarsened domain is <= 16 cells per
+    side, so the small levels are single boxes that the one-CTA coarse-tail
+    kernel can hold in shared memory.  A level's box decomposition does not
+    change its values (ghost fills are exact copies), so results stay
+    bit-identical to the oracle.
+    """
     levels = [(domain, ba, "base")]
-    while all(_coarsenable(e) for b in ba for e in b.extents()):
+    while all(_coarsenable(e) for b in ba for e in b.extents()) and max(
+        domain.coarsen(2).extents()
+    ) > _TAIL_MAX_EXTENT:
         ba = coarsened_layout(ba, 2)
         domain = domain.coarsen(2)
         levels.append((domain, ba, "boxlocal"))
-    if len(ba) > 1 and all(_coarsenable(e) for e in domain.extents()):
+    if all(_coarsenable(e) for e in domain.extents()):
         domain = domain.coarsen(2)
         ba = BoxArray([domain])
         levels.append((domain, ba, "agglom"))
-    while len(ba) == 1 and all(_coarsenable(e) for e in domain.extents()):
-        domain = domain.coarsen(2)
-        ba = BoxArray([domain])
-        levels.append((domain, ba, "single"))
+        while all(_coarsenable(e) for e in domain.extents()):
+            domain = domain.coarsen(2)
+            ba = BoxArray([domain])
+            levels.append((domain, ba, "single"))
+    elif len(ba) > 1:
+        pass  # cannot coarsen further: the current level is the bottom
     return levels
+
+
+def _tail_bytes(levels):
+    tot = 0
+    for dom, _, _ in levels:
+        e = dom.extents()
+        tot += (e[0] + 2) * (e[1] + 2) * (e[2] + 2) + e[0] * e[1] * e[2]
+    return 8 * tot
 
 
 class _Level:
@@ -113,6 +137,25 @@ class MLMG:
                 cba = coarsened_layout(lv.ba, 2)
                 lv.tmp = MultiFab(cba, lv.dm, 1, 0, replicated=lv.replicated)
                 lv.stage = MultiFab(cba, lv.dm, 1, 0, replicated=lv.replicated)
+        # coarse tail: the longest suffix of single-box levels that fits one CTA
+        n = len(self.levels)
+        self.tail = n
+        for t in range(n):
+            if all(self.levels[x].kind in ("agglom", "single") for x in range(t, n)) and _tail_bytes(
+                [(self.levels[x].domain, None, None) for x in range(t, n)]
+            ) <= 200 * 1024 and n - t <= 8 and t > 0:
+                self.tail = t
+                break
+        if self.tail < n:
+            tl = self.levels[self.tail:]
+            lohi = np.zeros((len(tl), 6), dtype=np.int32)
+            dhs = np.zeros((len(tl), 3), dtype=np.float64)
+            for x, lv in enumerate(tl):
+                lohi[x, :3] = tuple(lv.domain.lo)
+                lohi[x, 3:] = tuple(lv.domain.hi)
+                dhs[x] = lv.dh
+            self._tail_lohi = lohi
+            self._tail_dh = dhs
         top = self.levels[0]
         top.resid = MultiFab(top.ba, top.dm, 1, 0)
         self.norm = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
@@ -227,18 +270,44 @@ class MLMG:
         if self.dist:
             check(lib().amrb_nccl_allreduce(C.c_void_p(t.data_ptr()), 1, 2, self.transport.nccl_comm, stream_ptr()))
 
+    def _coarse_tail(self):
+        """All tail levels in one kernel: reads rhs, writes phi of levels[tail]."""
+        lv = self.levels[self.tail]
+        phi = lv.phi[lv.cur]
+        lohi, lp = i32p(self._tail_lohi)
+        dh = np.ascontiguousarray(self._tail_dh)
+        check(
+            lib().amrb_coarse_tail(
+                len(self._tail_lohi),
+                lp,
+                dh.ctypes.data_as(C.POINTER(C.c_double)),
+                field_of(lv.rhs).handle,
+                C.c_void_p(lv.rhs.storage.data_ptr()),
+                field_of(phi).handle,
+                C.c_void_p(phi.storage.data_ptr()),
+                self.nu1,
+                self.nu2,
+                self.bottom_sweeps,
+                stream_ptr(),
+            )
+        )
+
     def vcycle(self):
         L = self.levels
-        for l in range(len(L) - 1):
+        n = len(L)
+        T = self.tail  # first level handled by the coarse-tail kernel (n: none)
+        for l in range(T):
             lv = L[l]
             if l > 0:
                 lv.phi[lv.cur].storage.zero_()
+            if l == n - 1:
+                self._smooth(lv, self.bottom_sweeps)
+                break
             self._smooth(lv, self.nu1)
             self._resid_restrict(l)
-        bot = L[-1]
-        bot.phi[bot.cur].storage.zero_()
-        self._smooth(bot, self.bottom_sweeps)
-        for l in range(len(L) - 2, -1, -1):
+        if T < n:
+            self._coarse_tail()
+        for l in range(min(T, n - 1) - 1, -1, -1):
             self._prolong(l)
             self._smooth(L[l], self.nu2)
 
