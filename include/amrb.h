@@ -193,6 +193,13 @@ int amrb_prolong(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
                  const amrb_field* crse, const double* crse_base, int ncomp,
                  const int32_t* ratio, int add, void* stream);
 
+/* ||rhs - L(phi)||_inf over this device's valid cells, without writing the
+ * residual (phi ghosts width 1 filled).  Result (one double) to dev_out. */
+int amrb_residual_norm(const amrb_level* lv, const amrb_field* rhs,
+                       const double* rhs_base, const amrb_field* phi,
+                       const double* phi_base, const double dh[3], double* dev_out,
+                       void* stream);
+
 /* Coarse tail of the V-cycle in ONE CTA (all levels in shared memory):
  * nlev single-box periodic levels, each half the previous; lohi = int32
  * [nlev][6] (3-D padded), dh = double[nlev][3].  Reads level-0 rhs (valid) from

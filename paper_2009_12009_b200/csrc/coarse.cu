@@ -36,6 +36,7 @@ struct TailArgs {
   int nlev;
   TailLevel lv[kMaxTail];
   int nu1, nu2, nbottom;
+  int warp_from;  // first level small enough for one warp
   const double* rhs;  // level 0 rhs (valid lo cell)
   int64_t rs0, rs1;
   double* phi;        // level 0 phi (valid lo cell)
@@ -48,11 +49,19 @@ __device__ __forceinline__ double avg8t(const double* v) {
 
 __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x;
+  // Levels >= a.warp_from are tiny (<= 512 cells): warp 0 runs their whole
+  // sub-cycle with __syncwarp while the other warps wait at one barrier.
+  bool wmode = false;
+  int t = threadIdx.x, nt = kTailThreads;
+  auto sync = [&]() {
+    if (wmode)
+      __syncwarp();
+    else
+      __syncthreads();
+  };
 
   auto P = [&](const TailLevel& L) { return sm + L.phi_off; };
   auto Rr = [&](const TailLevel& L) { return sm + L.rhs_off; };
-  // phi index of valid cell (i, j, k): one ghost layer
   auto pidx = [](const TailLevel& L, int i, int j, int k) {
     return ((i + 1) * (L.n[1] + 2) + (j + 1)) * (L.n[2] + 2) + (k + 1);
   };
@@ -63,35 +72,28 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
     const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
     const int f0 = n1 * n2, f1 = n0 * n2, f2 = n0 * n1;
     const int tot = 2 * (f0 + f1 + f2);
-    for (int e = tid; e < tot; e += kTailThreads) {
-      int x = e, axis, side;
+    for (int e = t; e < tot; e += nt) {
+      int x = e;
       if (x < 2 * f0) {
-        axis = 0;
-        side = x / f0;
+        const int side = x / f0;
         x -= side * f0;
         const int j = x / n2, k = x - j * n2;
-        const int i = side ? n0 : -1, si = side ? 0 : n0 - 1;
-        p[pidx(L, i, j, k)] = p[pidx(L, si, j, k)];
+        p[pidx(L, side ? n0 : -1, j, k)] = p[pidx(L, side ? 0 : n0 - 1, j, k)];
         continue;
       }
       x -= 2 * f0;
       if (x < 2 * f1) {
-        axis = 1;
-        side = x / f1;
+        const int side = x / f1;
         x -= side * f1;
         const int i = x / n2, k = x - i * n2;
-        const int j = side ? n1 : -1, sj = side ? 0 : n1 - 1;
-        p[pidx(L, i, j, k)] = p[pidx(L, i, sj, k)];
+        p[pidx(L, i, side ? n1 : -1, k)] = p[pidx(L, i, side ? 0 : n1 - 1, k)];
         continue;
       }
       x -= 2 * f1;
-      axis = 2;
-      side = x / f2;
+      const int side = x / f2;
       x -= side * f2;
       const int i = x / n1, j = x - i * n1;
-      const int k = side ? n2 : -1, sk = side ? 0 : n2 - 1;
-      p[pidx(L, i, j, k)] = p[pidx(L, i, j, sk)];
-      (void)axis;
+      p[pidx(L, i, j, side ? n2 : -1)] = p[pidx(L, i, j, side ? 0 : n2 - 1)];
     }
   };
   auto color = [&](const TailLevel& L, int c) {
@@ -99,9 +101,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
     const double* r = Rr(L);
     const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
     const int sj = n2 + 2, si = (n1 + 2) * sj;
-    const int np = n0 * n1 * ((n2 + 1) / 2);
     const int h = (n2 + 1) / 2;
-    for (int e = tid; e < np; e += kTailThreads) {
+    const int np = n0 * n1 * h;
+    for (int e = t; e < np; e += nt) {
       const int ij = e / h, kp = e - ij * h;
       const int i = ij / n1, j = ij - i * n1;
       const int k = 2 * kp + ((L.lo_par + i + j + c) & 1);
@@ -116,94 +118,248 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
     for (int s = 0; s < n; ++s)
       for (int c = 0; c < 2; ++c) {
         fill_faces(L);
-        __syncthreads();
+        sync();
         color(L, c);
-        __syncthreads();
+        sync();
       }
   };
   auto zero_phi = [&](const TailLevel& L) {
     double* p = P(L);
     const int tot = (L.n[0] + 2) * (L.n[1] + 2) * (L.n[2] + 2);
-    for (int e = tid; e < tot; e += kTailThreads) p[e] = 0.0;
+    for (int e = t; e < tot; e += nt) p[e] = 0.0;
   };
-
-  // load level-0 rhs
-  {
-    const TailLevel& L = a.lv[0];
-    double* r = Rr(L);
-    const int tot = L.n[0] * L.n[1] * L.n[2];
-    for (int e = tid; e < tot; e += kTailThreads) {
-      const int ij = e / L.n[2], k = e - ij * L.n[2];
-      const int i = ij / L.n[1], j = ij - i * L.n[1];
-      r[e] = a.rhs[i * a.rs0 + j * a.rs1 + k];
-    }
-  }
-  // down
-  for (int l = 0; l < a.nlev; ++l) {
-    const TailLevel& L = a.lv[l];
-    zero_phi(L);
-    __syncthreads();
-    if (l == a.nlev - 1) {
-      smooth(L, a.nbottom);
-      break;
-    }
-    smooth(L, a.nu1);
-    fill_faces(L);
-    __syncthreads();
-    // residual + restriction into level l+1's rhs
-    const TailLevel& C = a.lv[l + 1];
-    {
-      const double* p = P(L);
-      const double* r = Rr(L);
-      double* rc = Rr(C);
-      const int sj = L.n[2] + 2, si = (L.n[1] + 2) * sj;
-      const int tot = C.n[0] * C.n[1] * C.n[2];
-      for (int e = tid; e < tot; e += kTailThreads) {
-        const int IJ = e / C.n[2], K = e - IJ * C.n[2];
-        const int I = IJ / C.n[1], J = IJ - I * C.n[1];
-        double v[8];
+  auto restrict_resid = [&](const TailLevel& L, const TailLevel& C) {
+    const double* p = P(L);
+    const double* r = Rr(L);
+    double* rc = Rr(C);
+    const int sj = L.n[2] + 2, si = (L.n[1] + 2) * sj;
+    const int tot = C.n[0] * C.n[1] * C.n[2];
+    for (int e = t; e < tot; e += nt) {
+      const int IJ = e / C.n[2], K = e - IJ * C.n[2];
+      const int I = IJ / C.n[1], J = IJ - I * C.n[1];
+      double v[8];
 #pragma unroll
-        for (int di = 0; di < 2; ++di)
+      for (int di = 0; di < 2; ++di)
 #pragma unroll
-          for (int dj = 0; dj < 2; ++dj)
+        for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
-            for (int dk = 0; dk < 2; ++dk) {
-              const int i = 2 * I + di, j = 2 * J + dj, k = 2 * K + dk;
-              const int o = pidx(L, i, j, k);
-              const double c0 = p[o];
-              v[di * 4 + dj * 2 + dk] =
-                  r[ridx(L, i, j, k)] - lap7(c0, p[o - si], p[o + si], p[o - sj], p[o + sj], p[o - 1], p[o + 1], L.cf);
-            }
-        rc[e] = avg8t(v);
-      }
+          for (int dk = 0; dk < 2; ++dk) {
+            const int i = 2 * I + di, j = 2 * J + dj, k = 2 * K + dk;
+            const int o = pidx(L, i, j, k);
+            const double c0 = p[o];
+            v[di * 4 + dj * 2 + dk] =
+                r[ridx(L, i, j, k)] - lap7(c0, p[o - si], p[o + si], p[o - sj], p[o + sj], p[o - 1], p[o + 1], L.cf);
+          }
+      rc[e] = avg8t(v);
     }
-    __syncthreads();
-  }
-  // up
-  for (int l = a.nlev - 2; l >= 0; --l) {
-    const TailLevel& L = a.lv[l];
-    const TailLevel& C = a.lv[l + 1];
+  };
+  auto prolong_add = [&](const TailLevel& L, const TailLevel& C) {
     double* p = P(L);
     const double* pc = P(C);
     const int tot = L.n[0] * L.n[1] * L.n[2];
-    for (int e = tid; e < tot; e += kTailThreads) {
+    for (int e = t; e < tot; e += nt) {
       const int ij = e / L.n[2], k = e - ij * L.n[2];
       const int i = ij / L.n[1], j = ij - i * L.n[1];
       const int o = pidx(L, i, j, k);
       p[o] = p[o] + pc[pidx(C, i >> 1, j >> 1, k >> 1)];
     }
-    __syncthreads();
-    smooth(L, a.nu2);
+  };
+  // down-sweep of levels [l0, nl): level l0's rhs is ready
+  auto down = [&](int l0, int nl) {
+    for (int l = l0; l < nl; ++l) {
+      const TailLevel& L = a.lv[l];
+      zero_phi(L);
+      sync();
+      if (l == a.nlev - 1) {
+        smooth(L, a.nbottom);
+        return;
+      }
+      smooth(L, a.nu1);
+      fill_faces(L);
+      sync();
+      restrict_resid(L, a.lv[l + 1]);
+      sync();
+    }
+  };
+  auto up = [&](int from, int to) {  // levels from .. to (descending), each prolonged from the next
+    for (int l = from; l >= to; --l) {
+      prolong_add(a.lv[l], a.lv[l + 1]);
+      sync();
+      smooth(a.lv[l], a.nu2);
+    }
+  };
+
+  {  // load level-0 rhs
+    const TailLevel& L = a.lv[0];
+    double* r = Rr(L);
+    const int tot = L.n[0] * L.n[1] * L.n[2];
+    for (int e = t; e < tot; e += nt) {
+      const int ij = e / L.n[2], k = e - ij * L.n[2];
+      const int i = ij / L.n[1], j = ij - i * L.n[1];
+      r[e] = a.rhs[i * a.rs0 + j * a.rs1 + k];
+    }
   }
-  // store level-0 phi (valid)
-  {
+  __syncthreads();
+  const int wf = a.warp_from;  // first tiny level (nlev if none)
+  down(0, wf);
+  if (wf < a.nlev) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      wmode = true;
+      nt = 32;
+      down(wf, a.nlev);
+      up(a.nlev - 2, wf);
+      wmode = false;
+      nt = kTailThreads;
+    }
+    __syncthreads();
+  }
+  up(min(wf, a.nlev - 1) - 1, 0);
+  __syncthreads();
+  {  // store level-0 phi (valid)
     const TailLevel& L = a.lv[0];
     const double* p = P(L);
     const int tot = L.n[0] * L.n[1] * L.n[2];
-    for (int e = tid; e < tot; e += kTailThreads) {
+    for (int e = t; e < tot; e += nt) {
       const int ij = e / L.n[2], k = e - ij * L.n[2];
       const int i = ij / L.n[1], j = ij - i * L.n[1];
       a.phi[i * a.ps0 + j * a.ps1 + k] = p[pidx(L, i, j, k)];
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Power-of-two cubic tails (16^3 .. 4^3 in the configs): no ghost cells at
+// all -- the periodic neighbour of (i-1) is ((i-1) & (n-1)), which reads the
+// very value a ghost fill would have copied, so the result is unchanged while
+// every fill phase (and its barrier) disappears.  Each level runs with just
+// enough threads (one per cell of a colour, capped at the block) and syncs on
+// a named barrier sized to them (one warp: __syncwarp).
+// ---------------------------------------------------------------------------
+template <int LOG0>
+__global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  // level l: n = 1 << (LOG0 - l); phi and rhs dense n^3 at smem offsets
+  auto cells = [](int l) { return 1 << (3 * (LOG0 - l)); };
+  auto nact = [&](int l) { return min(kTailThreads, max(32, cells(l) / 2)); };
+  auto lsync = [&](int l) {
+    const int na = nact(l);
+    if (na == 32)
+      __syncwarp();
+    else if (na == kTailThreads)
+      __syncthreads();
+    else
+      asm volatile("bar.sync 1, %0;\n" ::"r"(na) : "memory");
+  };
+  auto PHI = [&](int l) { return sm + a.lv[l].phi_off; };
+  auto RHS = [&](int l) { return sm + a.lv[l].rhs_off; };
+
+  auto color = [&](int l, int c) {
+    const int s = LOG0 - l, n = 1 << s, m = n - 1;
+    double* p = PHI(l);
+    const double* r = RHS(l);
+    const Coef cf = a.lv[l].cf;
+    const int lp = a.lv[l].lo_par;
+    const int np = cells(l) / 2;
+    for (int e = tid; e < np; e += nact(l)) {
+      const int kp = e & ((n >> 1) - 1), ij = e >> (s - 1);
+      const int j = ij & m, i = ij >> s;
+      const int k = 2 * kp + ((lp + i + j + c) & 1);
+      const int o = (i << (2 * s)) | (j << s) | k;
+      const double v = p[o];
+      const double lap = lap7(v, p[(((i - 1) & m) << (2 * s)) | (j << s) | k], p[(((i + 1) & m) << (2 * s)) | (j << s) | k],
+                              p[(i << (2 * s)) | (((j - 1) & m) << s) | k], p[(i << (2 * s)) | (((j + 1) & m) << s) | k],
+                              p[(i << (2 * s)) | (j << s) | ((k - 1) & m)], p[(i << (2 * s)) | (j << s) | ((k + 1) & m)], cf);
+      p[o] = relax(v, r[o], lap, cf.rgamma);
+    }
+  };
+  auto smooth = [&](int l, int nsw) {
+    for (int q = 0; q < nsw; ++q) {
+      color(l, 0);
+      lsync(l);
+      color(l, 1);
+      lsync(l);
+    }
+  };
+  auto restrict_resid = [&](int l) {  // rhs_{l+1} = avg8(rhs_l - L phi_l)
+    const int s = LOG0 - l, m = (1 << s) - 1, cs = s - 1;
+    const double* p = PHI(l);
+    const double* r = RHS(l);
+    double* rc = RHS(l + 1);
+    const Coef cf = a.lv[l].cf;
+    for (int e = tid; e < cells(l + 1); e += nact(l)) {
+      const int K = e & ((1 << cs) - 1), J = (e >> cs) & ((1 << cs) - 1), I = e >> (2 * cs);
+      double v[8];
+#pragma unroll
+      for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+          for (int dk = 0; dk < 2; ++dk) {
+            const int i = 2 * I + di, j = 2 * J + dj, k = 2 * K + dk;
+            const int o = (i << (2 * s)) | (j << s) | k;
+            const double c0 = p[o];
+            v[di * 4 + dj * 2 + dk] =
+                r[o] - lap7(c0, p[(((i - 1) & m) << (2 * s)) | (j << s) | k], p[(((i + 1) & m) << (2 * s)) | (j << s) | k],
+                            p[(i << (2 * s)) | (((j - 1) & m) << s) | k], p[(i << (2 * s)) | (((j + 1) & m) << s) | k],
+                            p[(i << (2 * s)) | (j << s) | ((k - 1) & m)], p[(i << (2 * s)) | (j << s) | ((k + 1) & m)], cf);
+          }
+      rc[e] = avg8t(v);
+    }
+  };
+  auto prolong_add = [&](int l) {  // phi_l += phi_{l+1}(parent)
+    const int s = LOG0 - l, cs = s - 1;
+    double* p = PHI(l);
+    const double* pc = PHI(l + 1);
+    for (int e = tid; e < cells(l); e += nact(l)) {
+      const int k = e & ((1 << s) - 1), j = (e >> s) & ((1 << s) - 1), i = e >> (2 * s);
+      p[e] = p[e] + pc[((i >> 1) << (2 * cs)) | ((j >> 1) << cs) | (k >> 1)];
+    }
+  };
+  auto zero = [&](int l) {
+    double* p = PHI(l);
+    for (int e = tid; e < cells(l); e += nact(l)) p[e] = 0.0;
+  };
+
+  {  // level-0 rhs from global
+    const int s = LOG0, n = 1 << s;
+    double* r = RHS(0);
+    for (int e = tid; e < cells(0); e += kTailThreads) {
+      const int k = e & (n - 1), j = (e >> s) & (n - 1), i = e >> (2 * s);
+      r[e] = a.rhs[i * a.rs0 + j * a.rs1 + k];
+    }
+  }
+  __syncthreads();
+  const int L = a.nlev;
+  for (int l = 0; l < L; ++l) {
+    if (tid < nact(l)) {
+      zero(l);
+      lsync(l);
+      if (l == L - 1) {
+        smooth(l, a.nbottom);
+      } else {
+        smooth(l, a.nu1);
+        restrict_resid(l);
+      }
+    }
+    __syncthreads();
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    if (tid < nact(l)) {
+      prolong_add(l);
+      lsync(l);
+      smooth(l, a.nu2);
+    }
+    __syncthreads();
+  }
+  {  // level-0 phi to global
+    const int s = LOG0, n = 1 << s;
+    const double* p = PHI(0);
+    for (int e = tid; e < cells(0); e += kTailThreads) {
+      const int k = e & (n - 1), j = (e >> s) & (n - 1), i = e >> (2 * s);
+      a.phi[i * a.ps0 + j * a.ps1 + k] = p[e];
     }
   }
 }
@@ -249,6 +405,12 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
     if (bytes > 227 * 1024) throw Error(AMRB_EINVAL, "coarse tail does not fit in shared memory");
     const FabView& vr = fr.host[0];
     const FabView& vp = fp.host[0];
+    a.warp_from = nlev;
+    for (int l = 0; l < nlev; ++l)
+      if (a.lv[l].n[0] * a.lv[l].n[1] * a.lv[l].n[2] <= 512) {
+        a.warp_from = l;
+        break;
+      }
     a.nu1 = nu1;
     a.nu2 = nu2;
     a.nbottom = nbottom;
@@ -258,11 +420,35 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
     a.phi = phi_base + vp.off;
     a.ps0 = vp.s0;
     a.ps1 = vp.s1;
+    // power-of-two cubic chain (each level >= 4 per side except possibly the
+    // bottom, which must be >= 2): dense layout, masked periodic indexing
+    const int n0 = a.lv[0].n[0];
+    bool p2 = n0 >= 2 && n0 <= 16 && (n0 & (n0 - 1)) == 0 && (n0 >> (nlev - 1)) >= 2;
+    for (int l = 0; l < nlev && p2; ++l)
+      p2 = a.lv[l].n[0] == (n0 >> l) && a.lv[l].n[1] == (n0 >> l) && a.lv[l].n[2] == (n0 >> l);
+    if (p2) {
+      int o2 = 0;
+      for (int l = 0; l < nlev; ++l) {
+        const int c = (n0 >> l) * (n0 >> l) * (n0 >> l);
+        a.lv[l].phi_off = o2;
+        o2 += c;
+        a.lv[l].rhs_off = o2;
+        o2 += c;
+      }
+      const size_t b2 = (size_t)o2 * sizeof(double);
+      auto kern = n0 == 16 ? k_coarse_tail_p2<4> : n0 == 8 ? k_coarse_tail_p2<3> : n0 == 4 ? k_coarse_tail_p2<2>
+                                                                                            : k_coarse_tail_p2<1>;
+      AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2));
+      kern<<<1, kTailThreads, b2, (cudaStream_t)stream>>>(a);
+      check_launch("k_coarse_tail_p2");
+      return;
+    }
     static bool configured = false;
     if (!configured) {
       AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       configured = true;
     }
+    a.warp_from = nlev;  // block mode throughout (measured faster than one warp)
     k_coarse_tail<<<1, kTailThreads, bytes, (cudaStream_t)stream>>>(a);
     check_launch("k_coarse_tail");
   });

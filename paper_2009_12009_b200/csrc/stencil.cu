@@ -683,6 +683,38 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0 && threadIdx.y == 0) partial[blockIdx.x] = acc;
 }
 
+// Residual inf-norm without materialising r: per-tile max |rhs - L(phi)|,
+// then the ordered final pass of k_reduce_final (max is order-independent).
+__global__ void __launch_bounds__(256)
+    k_resid_norm(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fr,
+                 const double* __restrict__ rhs, const FabView* __restrict__ fp, const double* __restrict__ phi,
+                 Coef cf, double* __restrict__ partial) {
+  __shared__ double scratch[32];
+  const int4 t = tiles[blockIdx.x];
+  const BoxGeom g = geo[t.x];
+  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
+  double acc = 0.0;
+  if (j < g.n[1] && k < g.n[2]) {
+    const FabView P = fp[t.x], R = fr[t.x];
+    const double* p = phi + P.off + (int64_t)j * P.s1 + k;
+    const double* r = rhs + R.off + (int64_t)j * R.s1 + k;
+    const int iend = min(t.y + kTI, g.n[0]);
+    int i = t.y;
+    double xm = ldg(p + (int64_t)(i - 1) * P.s0);
+    double c = ldg(p + (int64_t)i * P.s0);
+    for (; i < iend; ++i) {
+      const double* pc = p + (int64_t)i * P.s0;
+      const double xp = ldg(pc + P.s0);
+      const double lap = lap7(c, xm, xp, ldg(pc - P.s1), ldg(pc + P.s1), ldg(pc - 1), ldg(pc + 1), cf);
+      acc = fmax(acc, fabs(ldg(r + (int64_t)i * R.s0) - lap));
+      xm = c;
+      c = xp;
+    }
+  }
+  acc = block_combine(2, acc, scratch);
+  if (threadIdx.x == 0 && threadIdx.y == 0) partial[blockIdx.x] = acc;
+}
+
 __global__ void __launch_bounds__(1024) k_reduce_final(const double* __restrict__ partial, int n, int kind,
                                                        double* __restrict__ out) {
   __shared__ double scratch[32];
@@ -1057,6 +1089,28 @@ extern "C" int amrb_prolong(const amrb_level* flv_, amrb_field* fine, double* fi
     launch_tiles(tt, k_prolong, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(fine).dev.p, fine_base,
                  F(crse).dev.p, crse_base, ncomp, add, sh);
     check_launch("k_prolong");
+  });
+}
+
+extern "C" int amrb_residual_norm(const amrb_level* lv_, const amrb_field* rhs, const double* rhs_base,
+                                  const amrb_field* phi, const double* phi_base, const double dh[3], double* dev_out,
+                                  void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(phi), 1, "residual_norm");
+    need_same_level(F(rhs), lv, "residual_norm");
+    need_same_level(F(phi), lv, "residual_norm");
+    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const int n = (int)tt.host.size();
+    if (lv.partials.n < (size_t)std::max(n, 1)) lv.partials.alloc(std::max(n, 1));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n) {
+      launch_tiles(tt, k_resid_norm, st, dim3(32, 8), lv.dgeo.p, F(rhs).dev.p, rhs_base, F(phi).dev.p, phi_base,
+                   make_coef(dh), lv.partials.p);
+      check_launch("k_resid_norm");
+    }
+    k_reduce_final<<<1, 1024, 0, st>>>(lv.partials.p, n, 3, dev_out);
+    check_launch("k_reduce_final");
   });
 }
 

@@ -103,9 +103,9 @@ constexpr int kTK = 64;
 // cp.async.bulk copy per plane, smem rows keep the storage pitch PP = 72 and
 // smem col CO + c holds cell k0-2+c.  Otherwise a 4-D tensor-map TMA box of
 // PP = TK+4 columns (CO = 0).
-template <int TJ, int D, bool BULK>
+template <int TJ, int TK, int D, bool BULK>
 struct Sweep4Layout {
-  static constexpr int PP = BULK ? kTK + 8 : kTK + 4;  // smem row pitch (doubles)
+  static constexpr int PP = BULK ? TK + 8 : TK + 4;  // smem row pitch (doubles)
   static constexpr int CO = BULK ? 2 : 0;
   static constexpr int PJ = TJ + 4;   // phi rows j0-2 .. j0+TJ+1
   static constexpr int RJ = TJ + 2;   // rhs rows j0-1 .. j0+TJ
@@ -119,10 +119,10 @@ struct Sweep4Layout {
   static constexpr int NW = TJ + 2;  // warps
 };
 
-template <int TJ, int D, int MINB, bool FIXED, bool BULK>
+template <int TJ, int TK, int D, int MINB, bool FIXED, bool BULK>
 __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     k_gsrb_sweep4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR, Sweep4Args args) {
-  using LY = Sweep4Layout<TJ, D, BULK>;
+  using LY = Sweep4Layout<TJ, TK, D, BULK>;
   constexpr int PK = LY::PP;
   constexpr int CO = LY::CO;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       const double* Rh = rhs_slot(ip - rbase);
       const int gi = g.lo[0] + ip;
       const int bp = (gi + jk0) & 1;  // smem cell (r, c) has parity (bp + r + c) & 1; red is even
-      {
+      if (lane < TK / 2) {
         const int r = warp + 1;
         const int c = 2 * lane + 2 + ((bp + r) & 1);
         if (!(FIXED && is_fixed(gi, r, c))) {
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       }
       if (warp >= TJ && lane < TJ + 2) {
         const int r = lane + 1;
-        const int c = warp == TJ ? 1 : kTK + 2;
+        const int c = warp == TJ ? 1 : TK + 2;
         if (((bp + r + c) & 1) == 0 && !(FIXED && is_fixed(gi, r, c))) {
           const int o = r * PK + CO + c;
           P[o] = relax_at(P, Pm, Pp, Rh, o);
@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       const double* R2 = rhs_slot(p + 2 - rbase);
       double* out = args.b + B.off + (int64_t)p * B.s0 + (int64_t)(j0 + warp - 1) * B.s1 + k0 - 2;
 #pragma unroll
-      for (int h = 0; h < kTK / 32; ++h) {
+      for (int h = 0; h < (TK + 31) / 32; ++h) {
+        if (TK < 32 && lane >= TK) break;
         const int c = 2 + lane + 32 * h;
         const bool black = ((bp + r + c) & 1) != 0;  // cell (r, c) is black in planes p, p+2
         const double* P = black ? S0 : S2;
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       }
       // ring columns k0-1 / k0+TK of plane p+2 (red only)
       if (do_red && lane < 2) {
-        const int c = lane ? kTK + 2 : 1;
+        const int c = lane ? TK + 2 : 1;
         if (((bp + r + c) & 1) == 0 && !(FIXED && is_fixed(gi + 2, r, c))) {
           const int o = r * PK + CO + c;
           S2[o] = relax_at(S2, S1, S3, R2, o);
@@ -398,13 +399,13 @@ bool make_map(CUtensorMap* map, const double* base, const TmaDesc& d, int nblock
   return r == CUDA_SUCCESS;
 }
 
-template <int TJ, int D, int MINB, bool BULK>
+template <int TJ, int TK, int D, int MINB, bool BULK>
 bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
              const double* r_base, const Coef& cf, const int fixed_lo[3], const int fixed_hi[3], bool fixed,
              cudaStream_t st) {
-  using LY = Sweep4Layout<TJ, D, BULK>;
+  using LY = Sweep4Layout<TJ, TK, D, BULK>;
   for (auto& gg : lv.geo)
-    if (gg.n[1] % TJ || gg.n[2] % kTK || (BULK && gg.n[2] != kTK)) return false;
+    if (gg.n[1] % TJ || gg.n[2] % TK || (BULK && gg.n[2] != TK)) return false;
   if (a.ngrow < 2 || r.ngrow < 1) return false;
   CUtensorMap ma, mr;
   std::memset(&ma, 0, sizeof ma);
@@ -436,7 +437,7 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
     args.r_jc = -1 + dr.g;
     args.r_ic = dr.g;
   }
-  const auto& cols = lv.columns(TJ, kTK);
+  const auto& cols = lv.columns(TJ, TK);
   if (cols.host.empty()) return true;
   args.cols = cols.dev.p;
   args.fa = a.dev.p;
@@ -454,7 +455,7 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
     args.fixed_lo[x] = fixed_lo[x];
     args.fixed_hi[x] = fixed_hi[x];
   }
-  auto kern = fixed ? k_gsrb_sweep4<TJ, D, MINB, true, BULK> : k_gsrb_sweep4<TJ, D, MINB, false, BULK>;
+  auto kern = fixed ? k_gsrb_sweep4<TJ, TK, D, MINB, true, BULK> : k_gsrb_sweep4<TJ, TK, D, MINB, false, BULK>;
   static int per_sm[2] = {0, 0};
   if (!per_sm[fixed]) {
     AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
@@ -464,9 +465,10 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
   const long long slots = (long long)per_sm[fixed] * num_sms();
   const long long ncol = (long long)cols.host.size();
   long long grid;
-  (void)ncol;
-  // balanced persistent split: every CTA marches ~total/G plane-steps
-  grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 16));
+  // balanced persistent split: every CTA marches ~total/G plane-steps.  Big
+  // levels: one CTA slot each.  Small levels: segments of >= 2 planes so the
+  // level still spreads over the chip (their data lives in L2 anyway).
+  grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
   kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES, st>>>(ma, mr, args);
   check_launch("k_gsrb_sweep4");
   return true;
@@ -477,10 +479,27 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
 bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                       const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
                       const int fixed_hi[3], bool fixed, cudaStream_t st) {
-  // TJ = 16 rows per tile, one plane of prefetch, 2 CTAs per SM.  (Measured on
-  // B200 at C3: 114.6 us; deeper prefetch, TJ = 8, 1-D bulk copies, cp.async
-  // and register-staged loads were all slower -- see DESIGN.md.)
-  return launch4<16, 1, 1, false>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st);
+  // Tile: TK = widest of 64/32/16 dividing every box's k-extent, TJ = 16 (8 for
+  // small boxes); one plane of prefetch.  (C3 fine level: 114.6 us.  Deeper
+  // prefetch, 1-D bulk copies, cp.async and register-staged loads were all
+  // slower on B200 -- see DESIGN.md.)
+  int mink = 1 << 30, minj = 1 << 30;
+  for (auto& g : lv.geo) {
+    mink = std::min(mink, g.n[2]);
+    minj = std::min(minj, g.n[1]);
+  }
+#define AMRB_TRY(TJ, TK) \
+  if (launch4<TJ, TK, 1, 1, false>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st)) return true;
+  if (minj >= 64) {
+    AMRB_TRY(16, 64)
+    AMRB_TRY(16, 32)
+  }
+  AMRB_TRY(8, 64)
+  AMRB_TRY(8, 32)
+  AMRB_TRY(8, 16)
+#undef AMRB_TRY
+  (void)mink;
+  return false;
 }
 
 }  // namespace amrb

@@ -80,6 +80,27 @@ def mg_hierarchy(domain, ba):
     return levels
 
 
+def rebox_per_rank(ba, dm):
+    """One box per rank when each rank's boxes tile a rectangle (the usual SFC
+    octants / slabs), else the layout unchanged.  The solver's internal levels
+    use it: fewer, larger boxes mean no inter-box ghost traffic and fills that
+    touch only rank boundaries, and a level's values do not depend on how it
+    is cut into boxes."""
+    boxes, owners = [], []
+    for r in range(dm.nranks):
+        mine = [ba[i] for i in range(len(ba)) if dm[i] == r]
+        if not mine:
+            continue
+        lo = [min(b.lo[d] for b in mine) for d in range(ba.dim)]
+        hi = [max(b.hi[d] for b in mine) for d in range(ba.dim)]
+        bb = Box(lo, hi)
+        if bb.num_cells() != sum(b.num_cells() for b in mine):
+            return ba, dm
+        boxes.append(bb)
+        owners.append(r)
+    return BoxArray(boxes), DistributionMapping(owners, dm.nranks)
+
+
 def _tail_bytes(levels):
     tot = 0
     for dom, _, _ in levels:
@@ -115,6 +136,8 @@ class MLMG:
         self.use_graph = use_graph and self.nu1 % 2 == 0 and self.nu2 % 2 == 0 and self.bottom_sweeps % 2 == 0
         self.periodic = geom.periodic
         self.levels = []
+        self.user_ba, self.user_dm = ba, dm
+        ba, dm = rebox_per_rank(ba, dm)
         for dom, lba, kind in mg_hierarchy(geom.domain, ba):
             lv = _Level()
             lv.domain, lv.ba, lv.kind = dom, lba, kind
@@ -157,7 +180,6 @@ class MLMG:
             self._tail_lohi = lohi
             self._tail_dh = dhs
         top = self.levels[0]
-        top.resid = MultiFab(top.ba, top.dm, 1, 0)
         self.norm = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
         self.graph = None
         self.graph_replays = 0
@@ -251,19 +273,17 @@ class MLMG:
         phi = top.phi[top.cur]
         self._fill(top, phi, 1)
         check(
-            lib().amrb_residual(
-                level_of(top.resid).handle,
-                field_of(top.resid).handle,
-                C.c_void_p(top.resid.storage.data_ptr()),
+            lib().amrb_residual_norm(
+                level_of(phi).handle,
                 field_of(top.rhs).handle,
                 C.c_void_p(top.rhs.storage.data_ptr()),
                 field_of(phi).handle,
                 C.c_void_p(phi.storage.data_ptr()),
                 top.dhc,
+                C.c_void_p(self.norm.data_ptr()),
                 stream_ptr(),
             )
         )
-        device_reduce(top.resid, "absmax", 0, out=self.norm)
         self._allmax(self.norm)
 
     def _allmax(self, t):
