@@ -176,7 +176,9 @@ def run_ours(args):
     ba = A.BoxArray([dom]).max_size(64)
     dm = A.sfc_distribute(ba, A.default_costs(ba), world)
     tr = A.Transport.distributed() if world > 1 else A.Transport(1)
-    geom = A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, True)
+    # weak scaling: the physical domain grows with the grid so cells stay cubic
+    # (dx = 1/256 in every direction at every GPU count)
+    geom = A.Geometry(dom, (0.0,) * 3, tuple(e / 256.0 for e in ext), True)
 
     # synthetic rhs: per-box seeded normals on device, centred globally
     rhs = A.MultiFab(ba, dm, 1, 0)
@@ -315,8 +317,7 @@ def run_ours(args):
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
-        tr.close()
-        dist.destroy_process_group()
+        dist.barrier(device_ids=[local])
 
 
 def main():

@@ -98,6 +98,9 @@ int amrb_plan_destroy(amrb_plan* p);
 /*     Remote records ride one NCCL send/recv per ordered peer pair.         */
 /* mode 2 (local): keep only records with src and dst owned by my_rank      */
 /*     (copies between a distributed FabArray and a per-rank replica).      */
+/* mode 3 (p2p): records with dst here; remote sources are read directly     */
+/*     from the owner's storage over NVLink (src_fabtab = every box's layout */
+/*     in its owner's allocation; see amrb_prog_run_p2p).                   */
 /* op: 0 = dst = src (fill / parallel_copy), 1 = dst += src (sum_boundary;   */
 /*     overlapping records are applied in plan order, in waves).             */
 /* Message payloads are C-order (ncomp, e0, e1, e2) record slices           */
@@ -119,6 +122,14 @@ int amrb_prog_pairs(const amrb_prog* g, int64_t* out);
 int amrb_prog_run(amrb_prog* g, const double* src_base, double* dst_base,
                   double* sendbuf, double* recvbuf, void* nccl_comm, void* stream);
 int amrb_prog_destroy(amrb_prog* g);
+/* Run a mode-3 program: peer_bases[r] = rank r's storage base, mapped into
+ * this process (symmetric memory).  Callers frame it with amrb_peer_barrier. */
+int amrb_prog_run_p2p(amrb_prog* g, const double* src_base, double* dst_base,
+                      const uint64_t* peer_bases, int npeers, void* stream);
+/* Device-side barrier across ranks over NVLink signal pads: pad_ptrs[r] =
+ * rank r's pad (>= nranks uint32 slots), epoch = this rank's device counter. */
+int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch,
+                      void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Level descriptors for the ParallelFor box loop (advect.py:143-178 is the  */

@@ -74,6 +74,7 @@ class Transport:
         self.rank = 0
         self.mode = "sim"
         self.nccl_comm = None
+        self.p2p = False
         self._queues = {}
 
     @classmethod
@@ -94,9 +95,46 @@ class Transport:
         comm = C.c_void_p()
         check(lib().amrb_nccl_comm_create(uid, t.nranks, t.rank, C.byref(comm)), src=t.rank, dst=-1)
         t.nccl_comm = comm
+        t._setup_p2p()
         return t
 
+    def _setup_p2p(self):
+        """Signal pads + device epoch for the NVLink barrier of p2p fills."""
+        self.p2p = False
+        if self.nranks > 8:
+            return
+        try:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            dev = torch.device("cuda", torch.cuda.current_device())
+            self._bar_buf = symm_mem.empty(64, dtype=torch.int32, device=dev)
+            self._bar = symm_mem.rendezvous(self._bar_buf, dist.group.WORLD.group_name)
+            self._pads = np.array(self._bar.signal_pad_ptrs, dtype=np.uint64)
+            self._epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+            # pads start at zero; make sure every rank sees that before the first barrier
+            self._bar.barrier()
+            torch.cuda.synchronize()
+            self.p2p = True
+        except Exception:  # no symmetric memory on this system: NCCL send/recv only
+            self.p2p = False
+
+    def peer_barrier(self):
+        check(
+            lib().amrb_peer_barrier(
+                self._pads.ctypes.data_as(C.POINTER(C.c_uint64)),
+                self.rank,
+                self.nranks,
+                C.c_void_p(self._epoch.data_ptr()),
+                stream_ptr(),
+            ),
+            src=self.rank,
+        )
+
     def close(self):
+        """Destroy the NCCL communicator.  Call only after every CUDA graph that
+        captured operations on it has been released (ncclCommDestroy otherwise
+        waits for them); at process exit it can simply be left to the OS."""
         if self.nccl_comm is not None and self.nccl_comm.value:
             check(lib().amrb_nccl_comm_destroy(self.nccl_comm))
             self.nccl_comm = None
@@ -128,12 +166,13 @@ class Transport:
 class _Program:
     """A plan bound to (src storage, dst storage, transport mode)."""
 
-    def __init__(self, plan, src_fa, dst_fa, transport, op):
+    def __init__(self, plan, src_fa, dst_fa, transport, op, p2p=False):
         self.plan = plan  # keep the native plan alive
+        self.p2p = p2p
         sim = transport.mode == "sim"
-        mode = {"nccl": 0, "sim": 1, "local": 2}[transport.mode]
+        mode = 3 if p2p else {"nccl": 0, "sim": 1, "local": 2}[transport.mode]
         ncomp = src_fa.ncomp
-        st, stp = i64p(src_fa.fabtab)
+        st, stp = i64p(src_fa.global_fabtab() if p2p else src_fa.fabtab)
         dt, dtp = i64p(dst_fa.fabtab)
         so, sop = i32p(src_fa.owners())
         do, dop = i32p(dst_fa.owners())
@@ -179,7 +218,24 @@ class _Program:
             except Exception:
                 pass
 
-    def run(self, src_fa, dst_fa, transport):
+    def run(self, src_fa, dst_fa, transport, post_barrier=True):
+        if self.p2p:
+            # pull model: peers' boxes are final once everyone reached this point
+            transport.peer_barrier()
+            check(
+                lib().amrb_prog_run_p2p(
+                    self.handle,
+                    C.c_void_p(src_fa.storage.data_ptr()),
+                    C.c_void_p(dst_fa.storage.data_ptr()),
+                    src_fa.peer_ptrs.ctypes.data_as(C.POINTER(C.c_uint64)),
+                    transport.nranks,
+                    stream_ptr(),
+                ),
+                src=transport.rank,
+            )
+            if post_barrier:  # nobody may overwrite what a peer is still reading
+                transport.peer_barrier()
+            return
         comm = transport.nccl_comm if transport.mode == "nccl" else None
         if transport.mode == "local":
             comm = None
@@ -199,21 +255,22 @@ class _Program:
             transport.account(s, d, 8 * cnt)
 
 
-def _execute(plan, src_fa, dst_fa, transport, op):
+def _execute(plan, src_fa, dst_fa, transport, op, post_barrier=True):
     nranks = transport.nranks
     if src_fa.dm.nranks != nranks or dst_fa.dm.nranks != nranks:
         raise ValueError("transport rank count differs from the distribution maps")
     src_fa.require_cuda("copy")
     dst_fa.require_cuda("copy")
-    key = (id(plan), src_fa.serial, op, transport.mode, nranks)
+    p2p = transport.mode == "nccl" and transport.p2p and getattr(src_fa, "symmetric", False)
+    key = (id(plan), src_fa.serial, op, transport.mode, nranks, p2p)
     prog = dst_fa._progs.get(key)
     if prog is None:
-        prog = _Program(plan, src_fa, dst_fa, transport, op)
+        prog = _Program(plan, src_fa, dst_fa, transport, op, p2p=p2p)
         dst_fa._progs[key] = prog
-    prog.run(src_fa, dst_fa, transport)
+    prog.run(src_fa, dst_fa, transport, post_barrier=post_barrier)
 
 
-def fill_boundary(fa, transport, domain, periodic=None, ngrow=None):
+def fill_boundary(fa, transport, domain, periodic=None, ngrow=None, _post_barrier=True):
     """Fill every in-domain (or periodic-image) ghost cell from the valid cell it
     shadows; out-of-domain non-periodic ghosts are untouched (fabarray.py:364).
 
@@ -226,7 +283,7 @@ def fill_boundary(fa, transport, domain, periodic=None, ngrow=None):
     if ng == 0:
         return
     plan = build_plan_fill_boundary(fa.ba, ng, domain, periodic)
-    _execute(plan, fa, fa, transport, 0)
+    _execute(plan, fa, fa, transport, 0, post_barrier=_post_barrier)
 
 
 def parallel_copy(dst_fa, src_fa, transport, domain=None, periodic=None):

@@ -44,6 +44,13 @@ struct DevRec {
   int64_t ds0, ds1, dcs;
   int32_t e0, e1, e2;
   int32_t from_buf;  // 1: source is the receive/staging buffer
+  int32_t src_peer = -1;  // >= 0: source lives in that peer's storage (p2p mode)
+  int32_t pad_ = 0;
+};
+
+constexpr int kMaxPeers = 8;
+struct PeerPtrs {
+  const double* p[kMaxPeers];
 };
 
 struct Wave {
@@ -65,7 +72,7 @@ template <bool kAdd>
 __global__ void __launch_bounds__(kCopyThreads)
     k_copy(const DevRec* __restrict__ recs, const int32_t* __restrict__ first, int64_t total,
            int ncomp, const double* __restrict__ src, const double* __restrict__ buf,
-           double* __restrict__ dst) {
+           double* __restrict__ dst, PeerPtrs peers) {
   const int64_t base = (int64_t)blockIdx.x * kChunk;
   const int rlo0 = first[blockIdx.x];
   const int rhi0 = first[blockIdx.x + 1];
@@ -90,7 +97,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     t /= r.e2;
     const int j = t % r.e1;
     const int i = t / r.e1;
-    const double* s = r.from_buf ? buf : src;
+    const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
     const double v = s[r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k];
     double* d = dst + r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
     if (kAdd)
@@ -152,15 +159,15 @@ void prepare_wave(Wave& w, int ncomp) {
 }
 
 void run_wave(const Wave& w, int ncomp, bool add, const double* src, const double* buf, double* dst,
-              cudaStream_t st) {
+              cudaStream_t st, const PeerPtrs& peers = PeerPtrs{}) {
   if (w.total == 0) return;
   int64_t nchunks = (w.total + kChunk - 1) / kChunk;
   if (add)
     k_copy<true><<<(unsigned)nchunks, kCopyThreads, 0, st>>>(w.recs.p, w.first.p, w.total, ncomp, src,
-                                                             buf, dst);
+                                                             buf, dst, peers);
   else
     k_copy<false><<<(unsigned)nchunks, kCopyThreads, 0, st>>>(w.recs.p, w.first.p, w.total, ncomp, src,
-                                                              buf, dst);
+                                                              buf, dst, peers);
   check_launch("k_copy");
 }
 
@@ -185,10 +192,11 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
   return amrb::guarded([&] {
     using namespace amrb;
     if (!plan_ || !out || ncomp < 1 || nranks < 1 || my_rank < 0 || my_rank >= nranks || (op != 0 && op != 1) ||
-        mode < 0 || mode > 2)
+        mode < 0 || mode > 3 || (mode == 3 && nranks > kMaxPeers))
       throw Error(AMRB_EINVAL, "amrb_prog_create: bad arguments");
     const int sim_ranks = mode == 1;
     const bool local_only = mode == 2;
+    const bool p2p = mode == 3;  // src_fabtab = each box's layout in its OWNER's storage
     const Plan& plan = *reinterpret_cast<const Plan*>(plan_);
     Tab st{src_fabtab}, dt{dst_fabtab};
     auto* g = new Prog;
@@ -216,7 +224,7 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
     {
       std::map<std::pair<int, int>, std::vector<int64_t>> pairs;
       for (int64_t r = 0; r < n; ++r)
-        if (sr[r] >= 0 && sr[r] != dr[r] && (sim_ranks || sr[r] == my_rank || dr[r] == my_rank))
+        if (!p2p && sr[r] >= 0 && sr[r] != dr[r] && (sim_ranks || sr[r] == my_rank || dr[r] == my_rank))
           pairs[{sr[r], dr[r]}].push_back(r);
       // sim: one staging buffer holding every pair; dist: separate send/recv
       int64_t soff = 0, roff = 0;
@@ -271,7 +279,7 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
       cs = q.cells();
     };
     // ---- pack ---------------------------------------------------------------
-    for (int64_t r = 0; r < n; ++r) {
+    for (int64_t r = 0; r < n && !p2p; ++r) {
       if (sr[r] == dr[r] || buf_off[r] < 0) continue;
       if (!sim_ranks && sr[r] != my_rank) continue;
       const Record& q = recs[r];
@@ -295,9 +303,15 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
       d.e2 = q.hi[2] - q.lo[2] + 1;
       int dlo[3] = {q.lo[0] + q.shift[0], q.lo[1] + q.shift[1], q.lo[2] + q.shift[2]};
       fab_side(dt, q.dst, dlo, d.dst, d.ds0, d.ds1, d.dcs);
+      d.src_peer = -1;
       if (sr[r] == dr[r]) {
         fab_side(st, q.src, q.lo, d.src, d.ss0, d.ss1, d.scs);
         d.from_buf = 0;
+      } else if (p2p) {
+        // the global table holds the owner's layout for every box
+        fab_side(st, q.src, q.lo, d.src, d.ss0, d.ss1, d.scs);
+        d.from_buf = 0;
+        d.src_peer = sr[r];
       } else {
         buf_side(r, d.src, d.ss0, d.ss1, d.scs);
         d.from_buf = 1;
@@ -390,6 +404,60 @@ extern "C" int amrb_prog_run(amrb_prog* g_, const double* src_base, double* dst_
 extern "C" int amrb_prog_destroy(amrb_prog* g) {
   delete reinterpret_cast<amrb::Prog*>(g);
   return AMRB_OK;
+}
+
+
+extern "C" int amrb_prog_run_p2p(amrb_prog* g_, const double* src_base, double* dst_base, const uint64_t* peer_bases,
+                                 int npeers, void* stream) {
+  return amrb::guarded([&] {
+    using namespace amrb;
+    if (!g_ || npeers < 1 || npeers > kMaxPeers || !peer_bases) throw Error(AMRB_EINVAL, "amrb_prog_run_p2p: bad arguments");
+    auto* g = reinterpret_cast<Prog*>(g_);
+    PeerPtrs peers{};
+    for (int r = 0; r < npeers; ++r) peers.p[r] = reinterpret_cast<const double*>(peer_bases[r]);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    for (auto* w : g->apply) run_wave(*w, g->ncomp, g->op == 1, src_base, nullptr, dst_base, st, peers);
+  });
+}
+
+namespace {
+struct PadPtrs {
+  uint32_t* p[amrb::kMaxPeers];
+};
+
+// Device-side barrier over NVLink: bump a device epoch counter, publish it in
+// every peer's signal pad (slot = my rank), wait until every peer published it
+// in mine.  The epoch lives in device memory, so a captured graph replays
+// correctly; the wrap-safe compare allows 2^31 outstanding epochs.
+__global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nranks, uint32_t* epoch) {
+  if (threadIdx.x != 0) return;
+  const uint32_t e = *epoch + 1;
+  *epoch = e;
+  __threadfence_system();
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
+  }
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(my_pad + p) : "memory");
+    } while ((int32_t)(v - e) < 0);
+  }
+}
+}  // namespace
+
+extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch, void* stream) {
+  return amrb::guarded([&] {
+    using namespace amrb;
+    if (!pad_ptrs || nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks || !epoch)
+      throw Error(AMRB_EINVAL, "amrb_peer_barrier: bad arguments");
+    PadPtrs pads{};
+    for (int r = 0; r < nranks; ++r) pads.p[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
+    k_peer_barrier<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pads.p[rank], pads, rank, nranks, epoch);
+    check_launch("k_peer_barrier");
+  });
 }
 
 // ----------------------------------------------------------------------------

@@ -49,21 +49,27 @@ def _coarsenable(e):
 _TAIL_MAX_EXTENT = 16  # agglomerate once the coarsened domain fits in one CTA
 
 
-def mg_hierarchy(domain, ba):
+def mg_hierarchy(domain, ba, nranks=1, agg_cells=64**3):
     """[(domain, BoxArray, kind)] fine -> coarse.
 
     Same level RESOLUTIONS as oracle.mlmg_ref.mg_levels (box-local coarsening,
     agglomeration, single-box coarsening while extents are even and >= 8), but
-    the device agglomerates as soon as the coarsened domain is <= 16 cells per
-    side, so the small levels are single boxes that the one-CTA coarse-tail
-    kernel can hold in shared memory.  A level's box decomposition does not
-    change its values (ghost fills are exact copies), so results stay
-    bit-identical to the oracle.
+    the device agglomerates earlier: as soon as the coarsened domain is <= 16
+    cells per side (so the one-CTA coarse-tail kernel can hold the rest), and,
+    with several ranks, as soon as it has <= agg_cells cells (below that a
+    replicated level is cheaper than a ghost exchange per sweep).  A level's box
+    decomposition does not change its values (ghost fills are exact copies),
+    so results stay bit-identical to the oracle.
     """
     levels = [(domain, ba, "base")]
-    while all(_coarsenable(e) for b in ba for e in b.extents()) and max(
-        domain.coarsen(2).extents()
-    ) > _TAIL_MAX_EXTENT:
+
+    def keep_boxlocal(dom):
+        nxt = dom.coarsen(2)
+        if max(nxt.extents()) <= _TAIL_MAX_EXTENT:
+            return False
+        return nranks == 1 or nxt.num_cells() > agg_cells
+
+    while all(_coarsenable(e) for b in ba for e in b.extents()) and keep_boxlocal(domain):
         ba = coarsened_layout(ba, 2)
         domain = domain.coarsen(2)
         levels.append((domain, ba, "boxlocal"))
@@ -75,8 +81,6 @@ def mg_hierarchy(domain, ba):
             domain = domain.coarsen(2)
             ba = BoxArray([domain])
             levels.append((domain, ba, "single"))
-    elif len(ba) > 1:
-        pass  # cannot coarsen further: the current level is the bottom
     return levels
 
 
@@ -138,7 +142,7 @@ class MLMG:
         self.levels = []
         self.user_ba, self.user_dm = ba, dm
         ba, dm = rebox_per_rank(ba, dm)
-        for dom, lba, kind in mg_hierarchy(geom.domain, ba):
+        for dom, lba, kind in mg_hierarchy(geom.domain, ba, nranks=dm.nranks if self.dist else 1):
             lv = _Level()
             lv.domain, lv.ba, lv.kind = dom, lba, kind
             lv.replicated = kind in ("agglom", "single")
@@ -146,7 +150,8 @@ class MLMG:
             cs = [(h - l) / e for l, h, e in zip(geom.prob_lo, geom.prob_hi, dom.extents())]
             lv.dh = tuple(1.0 / (c * c) for c in cs)
             lv.dhc = dh_array(lv.dh)
-            mk = lambda ng: MultiFab(lba, lv.dm, 1, ng, replicated=lv.replicated)  # noqa: E731
+            sym = self.dist and not lv.replicated and self.transport.p2p
+            mk = lambda ng: MultiFab(lba, lv.dm, 1, ng, replicated=lv.replicated, symmetric=sym)  # noqa: E731
             lv.phi = [mk(2), mk(2)]
             lv.cur = 0
             lv.rhs = mk(1)
@@ -193,7 +198,10 @@ class MLMG:
 
     # -- building blocks ---------------------------------------------------------
     def _fill(self, lv, fa, width):
-        fill_boundary(fa, self.transport, lv.domain, self.periodic, ngrow=width)
+        # Inside the V-cycle a rank only rewrites cells a peer pulled after the
+        # next fill's barrier (or an NCCL collective), so one barrier per fill
+        # suffices for the p2p path.
+        fill_boundary(fa, self.transport, lv.domain, self.periodic, ngrow=width, _post_barrier=False)
 
     def _sweep(self, lv):
         a = lv.phi[lv.cur]
@@ -347,7 +355,8 @@ class MLMG:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
+            # relaxed: NCCL's proxy thread keeps making CUDA calls during capture
+            with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
                 self._cap_l0 = int(lib().amrb_launch_count())
                 self._cycle_and_norm()
         torch.cuda.current_stream().wait_stream(s)

@@ -127,7 +127,8 @@ class ArrayView:
 class FabArray:
     """One Fab per box of ``ba``; boxes resident where ``dm`` puts them."""
 
-    def __init__(self, ba, dm, ncomp=1, ngrow=0, dtype=np.float64, *, device=None, replicated=False, rank=None):
+    def __init__(self, ba, dm, ncomp=1, ngrow=0, dtype=np.float64, *, device=None, replicated=False, rank=None,
+                 symmetric=False):
         if len(ba) != len(dm):
             raise ValueError("BoxArray and DistributionMapping lengths differ")
         if np.dtype(dtype) != np.float64:
@@ -147,7 +148,22 @@ class FabArray:
         else:
             self.resident = np.ones(len(ba), dtype=bool)
         self._layout()
-        self.storage = torch.zeros(self._nelems, dtype=torch.float64, device=self.device)
+        # symmetric: one process per GPU, storage in torch symmetric memory so
+        # every peer can read this rank's boxes over NVLink (p2p ghost fills)
+        self.symmetric = bool(symmetric) and self.distributed
+        self.peer_ptrs = None
+        if self.symmetric:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            n = torch.tensor([self._nelems], dtype=torch.int64, device=self.device)
+            dist.all_reduce(n, op=dist.ReduceOp.MAX)
+            self.storage = symm_mem.empty(int(n.item()), dtype=torch.float64, device=self.device)
+            self.storage.zero_()
+            self._symm = symm_mem.rendezvous(self.storage, dist.group.WORLD.group_name)
+            self.peer_ptrs = np.array(self._symm.buffer_ptrs, dtype=np.uint64)
+        else:
+            self.storage = torch.zeros(self._nelems, dtype=torch.float64, device=self.device)
         self.fabs = {}
         for i in range(len(ba)):
             if self.resident[i]:
@@ -157,6 +173,22 @@ class FabArray:
         self.serial = next(_serials)
 
     # -- layout ---------------------------------------------------------------
+    def global_fabtab(self):
+        """Every box's layout inside its OWNER's allocation (p2p copy sources)."""
+        if getattr(self, "_gtab", None) is None:
+            keep = self.resident
+            tab = np.zeros_like(self.fabtab)
+            for r in range(self.dm.nranks):
+                self.resident = np.array([o == r for o in self.dm.owner], dtype=bool)
+                saved = (self.fabtab, self._ext3, self._nelems)
+                self._layout()
+                rows = self.resident
+                tab[rows] = self.fabtab[rows]
+                self.fabtab, self._ext3, self._nelems = saved
+            self.resident = keep
+            self._gtab = tab
+        return self._gtab
+
     def _layout(self):
         dim = self.ba.dim
         pad = 3 - dim
