@@ -55,55 +55,49 @@ struct PeerPtrs {
 
 struct Wave {
   std::vector<DevRec> host;
-  std::vector<int32_t> chunk_first;
+  std::vector<int2> blocks;  // (record, first flat index inside the record)
   DevArray<DevRec> recs;
-  DevArray<int32_t> first;
+  DevArray<int2> dblocks;
   int64_t total = 0;
-  void finish(int ncomp) {
-    total = 0;
-    for (auto& r : host) {
-      r.begin = total;
-      total += (int64_t)r.e0 * r.e1 * r.e2 * ncomp;
-    }
-  }
 };
 
+// One CTA per (record, chunk of kChunk flat indices): no search, and each
+// thread issues all of its loads before its stores so remote (NVLink) and
+// local latencies overlap.
 template <bool kAdd>
 __global__ void __launch_bounds__(kCopyThreads)
-    k_copy(const DevRec* __restrict__ recs, const int32_t* __restrict__ first, int64_t total,
-           int ncomp, const double* __restrict__ src, const double* __restrict__ buf,
-           double* __restrict__ dst, PeerPtrs peers) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  const int rlo0 = first[blockIdx.x];
-  const int rhi0 = first[blockIdx.x + 1];
+    k_copy(const DevRec* __restrict__ recs, const int2* __restrict__ blocks, int ncomp,
+           const double* __restrict__ src, const double* __restrict__ buf, double* __restrict__ dst,
+           PeerPtrs peers) {
+  const int2 bl = blocks[blockIdx.x];
+  const DevRec r = recs[bl.x];
+  const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
+  const int64_t end = min(cells * ncomp, (int64_t)bl.y + kChunk);
+  const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
+  double v[kCopyItems];
+  int64_t dofs[kCopyItems];
 #pragma unroll
   for (int u = 0; u < kCopyItems; ++u) {
-    const int64_t f = base + u * kCopyThreads + threadIdx.x;
-    if (f >= total) return;
-    int lo = rlo0, hi = rhi0;
-    while (lo < hi) {  // last record with begin <= f
-      int mid = (lo + hi + 1) >> 1;
-      if (recs[mid].begin <= f)
-        lo = mid;
-      else
-        hi = mid - 1;
+    const int64_t loc = (int64_t)bl.y + u * kCopyThreads + threadIdx.x;
+    dofs[u] = -1;
+    if (loc < end) {
+      const int c = (int)(loc / cells);
+      int t = (int)(loc - (int64_t)c * cells);
+      const int k = t % r.e2;
+      t /= r.e2;
+      const int j = t % r.e1;
+      const int i = t / r.e1;
+      v[u] = s[r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k];
+      dofs[u] = r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
     }
-    const DevRec& r = recs[lo];
-    const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
-    int64_t loc = f - r.begin;  // in [0, ncomp * cells)
-    const int c = (int)(loc / cells);
-    int t = (int)(loc - (int64_t)c * cells);
-    const int k = t % r.e2;
-    t /= r.e2;
-    const int j = t % r.e1;
-    const int i = t / r.e1;
-    const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
-    const double v = s[r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k];
-    double* d = dst + r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
+  }
+#pragma unroll
+  for (int u = 0; u < kCopyItems; ++u) {
+    if (dofs[u] < 0) continue;
     if (kAdd)
-      *d = *d + v;
+      dst[dofs[u]] = dst[dofs[u]] + v[u];
     else
-      *d = v;
+      dst[dofs[u]] = v[u];
   }
 }
 
@@ -145,29 +139,27 @@ int64_t cell_offset(const Tab& tab, int b, const int lo[3]) {
 }
 
 void prepare_wave(Wave& w, int ncomp) {
-  w.finish(ncomp);
-  int64_t nchunks = (w.total + kChunk - 1) / kChunk;
-  w.chunk_first.assign((size_t)nchunks + 1, 0);
-  size_t r = 0;
-  for (int64_t c = 0; c <= nchunks; ++c) {
-    int64_t f = std::min<int64_t>(c * kChunk, std::max<int64_t>(w.total - 1, 0));
-    while (r + 1 < w.host.size() && w.host[r + 1].begin <= f) ++r;
-    w.chunk_first[(size_t)c] = (int32_t)r;
+  w.total = 0;
+  w.blocks.clear();
+  for (size_t i = 0; i < w.host.size(); ++i) {
+    DevRec& r = w.host[i];
+    const int64_t n = (int64_t)r.e0 * r.e1 * r.e2 * ncomp;
+    r.begin = w.total;
+    w.total += n;
+    for (int64_t o = 0; o < n; o += kChunk) w.blocks.push_back(make_int2((int)i, (int)o));
   }
   w.recs.upload(w.host);
-  w.first.upload(w.chunk_first);
+  w.dblocks.upload(w.blocks);
 }
 
 void run_wave(const Wave& w, int ncomp, bool add, const double* src, const double* buf, double* dst,
               cudaStream_t st, const PeerPtrs& peers = PeerPtrs{}) {
-  if (w.total == 0) return;
-  int64_t nchunks = (w.total + kChunk - 1) / kChunk;
+  if (w.blocks.empty()) return;
+  const unsigned nb = (unsigned)w.blocks.size();
   if (add)
-    k_copy<true><<<(unsigned)nchunks, kCopyThreads, 0, st>>>(w.recs.p, w.first.p, w.total, ncomp, src,
-                                                             buf, dst, peers);
+    k_copy<true><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers);
   else
-    k_copy<false><<<(unsigned)nchunks, kCopyThreads, 0, st>>>(w.recs.p, w.first.p, w.total, ncomp, src,
-                                                              buf, dst, peers);
+    k_copy<false><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers);
   check_launch("k_copy");
 }
 
