@@ -130,6 +130,10 @@ int amrb_prog_run_p2p(amrb_prog* g, const double* src_base, double* dst_base,
  * rank r's pad (>= nranks uint32 slots), epoch = this rank's device counter. */
 int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch,
                       void* stream);
+/* In-place max over ranks of one device double over NVLink (one launch):
+ * slot_ptrs[r] = rank r's symmetric buffer of >= nranks doubles. */
+int amrb_peer_allmax(const uint64_t* pad_ptrs, const uint64_t* slot_ptrs, int rank,
+                     int nranks, uint32_t* epoch, double* val, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Level descriptors for the ParallelFor box loop (advect.py:143-178 is the  */

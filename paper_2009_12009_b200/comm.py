@@ -111,6 +111,9 @@ class Transport:
             self._bar_buf = symm_mem.empty(64, dtype=torch.int32, device=dev)
             self._bar = symm_mem.rendezvous(self._bar_buf, dist.group.WORLD.group_name)
             self._pads = np.array(self._bar.signal_pad_ptrs, dtype=np.uint64)
+            self._slots_buf = symm_mem.empty(16, dtype=torch.float64, device=dev)
+            self._slots = symm_mem.rendezvous(self._slots_buf, dist.group.WORLD.group_name)
+            self._slot_ptrs = np.array(self._slots.buffer_ptrs, dtype=np.uint64)
             self._epoch = torch.zeros(1, dtype=torch.int32, device=dev)
             # pads start at zero; make sure every rank sees that before the first barrier
             self._bar.barrier()
@@ -118,6 +121,21 @@ class Transport:
             self.p2p = True
         except Exception:  # no symmetric memory on this system: NCCL send/recv only
             self.p2p = False
+
+    def peer_allmax(self, t):
+        """t (1-element float64 CUDA tensor) <- max over ranks, over NVLink."""
+        check(
+            lib().amrb_peer_allmax(
+                self._pads.ctypes.data_as(C.POINTER(C.c_uint64)),
+                self._slot_ptrs.ctypes.data_as(C.POINTER(C.c_uint64)),
+                self.rank,
+                self.nranks,
+                C.c_void_p(self._epoch.data_ptr()),
+                C.c_void_p(t.data_ptr()),
+                stream_ptr(),
+            ),
+            src=self.rank,
+        )
 
     def peer_barrier(self):
         check(

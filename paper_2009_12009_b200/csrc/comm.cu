@@ -452,6 +452,63 @@ extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks,
   });
 }
 
+
+using amrb::PeerPtrs;
+namespace {
+// Max-all-reduce of one double over NVLink: publish the local value into slot
+// [rank] of every peer's symmetric buffer, run the signal barrier, then take
+// the max over the local slots.  One launch, graph-replay safe (device epoch).
+__global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, const uint64_t* __restrict__ bufs_unused, int rank,
+                              int nranks, uint32_t* epoch, double* val, double* my_slots, PeerPtrs peer_slots) {
+  if (threadIdx.x != 0) return;
+  const double v = *val;
+  for (int p = 0; p < nranks; ++p) {
+    double* dst = const_cast<double*>(peer_slots.p[p]) + rank;
+    *dst = v;
+  }
+  const uint32_t e = *epoch + 1;
+  *epoch = e;
+  __threadfence_system();
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
+  }
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    uint32_t w;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(w) : "l"(my_pad + p) : "memory");
+    } while ((int32_t)(w - e) < 0);
+  }
+  double m = my_slots[0];
+  for (int p = 1; p < nranks; ++p) {
+    double x;
+    asm volatile("ld.acquire.sys.global.f64 %0, [%1];\n" : "=d"(x) : "l"(my_slots + p) : "memory");
+    m = fmax(m, x);
+  }
+  *val = m;
+  (void)bufs_unused;
+}
+}  // namespace
+
+extern "C" int amrb_peer_allmax(const uint64_t* pad_ptrs, const uint64_t* slot_ptrs, int rank, int nranks,
+                                uint32_t* epoch, double* val, void* stream) {
+  return amrb::guarded([&] {
+    using namespace amrb;
+    if (!pad_ptrs || !slot_ptrs || nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks || !epoch || !val)
+      throw Error(AMRB_EINVAL, "amrb_peer_allmax: bad arguments");
+    PadPtrs pads{};
+    PeerPtrs slots{};
+    for (int r = 0; r < nranks; ++r) {
+      pads.p[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
+      slots.p[r] = reinterpret_cast<const double*>(slot_ptrs[r]);
+    }
+    k_peer_allmax<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        pads.p[rank], pads, nullptr, rank, nranks, epoch, val, const_cast<double*>(slots.p[rank]), slots);
+    check_launch("k_peer_allmax");
+  });
+}
+
 // ----------------------------------------------------------------------------
 // NCCL plumbing
 // ----------------------------------------------------------------------------

@@ -163,7 +163,8 @@ class MLMG:
             lv.boxlocal_next = nx.kind == "boxlocal"
             if not lv.boxlocal_next:
                 cba = coarsened_layout(lv.ba, 2)
-                lv.tmp = MultiFab(cba, lv.dm, 1, 0, replicated=lv.replicated)
+                sym = self.dist and not lv.replicated and self.transport.p2p
+                lv.tmp = MultiFab(cba, lv.dm, 1, 0, replicated=lv.replicated, symmetric=sym)
                 lv.stage = MultiFab(cba, lv.dm, 1, 0, replicated=lv.replicated)
         # coarse tail: the longest suffix of single-box levels that fits one CTA
         n = len(self.levels)
@@ -252,7 +253,11 @@ class MLMG:
 
     def _gather_replica(self, lv, nx):
         """tmp (coarsened layout of lv, maybe distributed) -> nx.rhs (one box)."""
-        if self.dist and not lv.replicated:
+        if self.dist and not lv.replicated and self.transport.p2p:
+            # every rank pulls every rank's restricted boxes into its replica
+            # over NVLink (peer-pull copy program framed by the signal barrier)
+            copy_into(nx.rhs, lv.tmp, self.transport)
+        elif self.dist and not lv.replicated:
             nx.rhs.storage.zero_()
             # every rank copies its own boxes into its replica, then all-reduce(sum)
             copy_into(nx.rhs, lv.tmp, _LocalView(self.transport))
@@ -295,7 +300,9 @@ class MLMG:
         self._allmax(self.norm)
 
     def _allmax(self, t):
-        if self.dist:
+        if self.dist and self.transport.p2p:
+            self.transport.peer_allmax(t)
+        elif self.dist:
             check(lib().amrb_nccl_allreduce(C.c_void_p(t.data_ptr()), 1, 2, self.transport.nccl_comm, stream_ptr()))
 
     def _coarse_tail(self):
