@@ -54,6 +54,8 @@ int amrb_version(void);
 /* Kernel launches issued so far by this process (host-side count; launches
  * replayed from a captured CUDA graph are not included). */
 int64_t amrb_launch_count(void);
+/* Zero n doubles (cudaMemsetAsync on `stream`; a memset node in a graph). */
+int amrb_zero(double* ptr, int64_t n, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Communication plans (host).  Records are CopyRecord(src, dst, src_box,    */

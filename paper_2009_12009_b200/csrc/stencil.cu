@@ -107,7 +107,7 @@ enum class Op { kLap, kResid };
 
 template <Op op>
 __global__ void __launch_bounds__(256)
-    k_stencil(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fo,
+    k_stencil(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fo,
               double* __restrict__ out, const FabView* __restrict__ fr, const double* __restrict__ rhs,
               const FabView* __restrict__ fp, const double* __restrict__ phi, Coef cf) {
   const int4 t = tiles[blockIdx.x];
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256)
     r = rhs + R.off + (int64_t)j * R.s1 + k;
     rs0 = R.s0;
   }
-  const int iend = min(t.y + kTI, g.n[0]);
+  const int iend = min(t.y + ti, g.n[0]);
   int i = t.y;
   double xm = ldg(p + (int64_t)(i - 1) * P.s0);
   double c = ldg(p + (int64_t)i * P.s0);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256)
 // cell of the pair has the colour), so no lane idles on parity.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
-    k_gsrb_color(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fp,
+    k_gsrb_color(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fp,
                  double* __restrict__ phi, const FabView* __restrict__ fr, const double* __restrict__ rhs,
                  Coef cf, int color) {
   const int4 t = tiles[blockIdx.x];
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256)
   const int kp = t.w + 2 * threadIdx.x;
   if (j >= g.n[1] || kp >= g.n[2]) return;
   const FabView P = fp[t.x], R = fr[t.x];
-  const int iend = min(t.y + kTI, g.n[0]);
+  const int iend = min(t.y + ti, g.n[0]);
   for (int i = t.y; i < iend; ++i) {
     // global parity of (i, j, kp): pick the member of the pair with the colour
     const int par = (g.lo[0] + i + g.lo[1] + j + g.lo[2] + kp + color) & 1;
@@ -546,7 +546,7 @@ __device__ __forceinline__ double avg8(double c000, double c001, double c010, do
 // bit-for-bit against numpy 2.3 in 1-D, 2-D and 3-D).  mode 1 = injection
 // (child at offset 0, coarse_fine.py:150-154).
 __global__ void __launch_bounds__(256)
-    k_restrict(const int4* __restrict__ tiles, const BoxGeom* __restrict__ cgeo, const FabView* __restrict__ fc,
+    k_restrict(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ cgeo, const FabView* __restrict__ fc,
                double* __restrict__ crse, const FabView* __restrict__ ff, const double* __restrict__ fine,
                int ncomp, int3 rr, int mode, double inv) {
   const int4 t = tiles[blockIdx.x];
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256)
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
   if (j >= g.n[1] || k >= g.n[2]) return;
   const FabView C = fc[t.x], F = ff[t.x];
-  const int iend = min(t.y + kTI, g.n[0]);
+  const int iend = min(t.y + ti, g.n[0]);
   for (int n = 0; n < ncomp; ++n)
     for (int i = t.y; i < iend; ++i) {
       const double* f0 = fine + F.off + n * F.cs + (int64_t)(rr.x * i) * F.s0 + (int64_t)(rr.y * j) * F.s1 + rr.z * k;
@@ -583,7 +583,7 @@ __device__ __forceinline__ double resid_at(const double* p, int64_t s0, int64_t 
 }
 
 __global__ void __launch_bounds__(256)
-    k_resid_restrict(const int4* __restrict__ tiles, const BoxGeom* __restrict__ cgeo,
+    k_resid_restrict(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ cgeo,
                      const FabView* __restrict__ fc, double* __restrict__ crse, const FabView* __restrict__ fr,
                      const double* __restrict__ rhs, const FabView* __restrict__ fp,
                      const double* __restrict__ phi, Coef cf) {
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(256)
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
   if (j >= g.n[1] || k >= g.n[2]) return;
   const FabView C = fc[t.x], R = fr[t.x], P = fp[t.x];
-  const int iend = min(t.y + kTI, g.n[0]);
+  const int iend = min(t.y + ti, g.n[0]);
   for (int i = t.y; i < iend; ++i) {
     double v[8];
 #pragma unroll
@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(256)
 
 // Prolongation (pc), optionally added: fine(c) (+)= crse(c / 2).
 __global__ void __launch_bounds__(256)
-    k_prolong(const int4* __restrict__ tiles, const BoxGeom* __restrict__ fgeo, const FabView* __restrict__ ff,
+    k_prolong(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ fgeo, const FabView* __restrict__ ff,
               double* __restrict__ fine, const FabView* __restrict__ fc, const double* __restrict__ crse,
               int ncomp, int add, int3 sh) {
   const int4 t = tiles[blockIdx.x];
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(256)
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
   if (j >= g.n[1] || k >= g.n[2]) return;
   const FabView F = ff[t.x], C = fc[t.x];
-  const int iend = min(t.y + kTI, g.n[0]);
+  const int iend = min(t.y + ti, g.n[0]);
   // coarse local index: floor((lo + x)/2) - floor(lo/2); lo is even on coarsenable layouts
   for (int n = 0; n < ncomp; ++n)
     for (int i = t.y; i < iend; ++i) {
@@ -662,7 +662,7 @@ __device__ double block_combine(int kind, double v, double* scratch) {
 }
 
 __global__ void __launch_bounds__(256)
-    k_reduce_tiles(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fx,
+    k_reduce_tiles(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fx,
                    const double* __restrict__ x, int comp, int kind, double* __restrict__ partial) {
   __shared__ double scratch[32];
   const int4 t = tiles[blockIdx.x];
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(256)
   double acc = identity(rkind);
   if (j < g.n[1] && k < g.n[2]) {
     const FabView X = fx[t.x];
-    const int iend = min(t.y + kTI, g.n[0]);
+    const int iend = min(t.y + ti, g.n[0]);
     for (int i = t.y; i < iend; ++i) {
       double v = x[X.off + comp * X.cs + (int64_t)i * X.s0 + (int64_t)j * X.s1 + k];
       if (kind == 3) v = fabs(v);
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(256)
 // Residual inf-norm without materialising r: per-tile max |rhs - L(phi)|,
 // then the ordered final pass of k_reduce_final (max is order-independent).
 __global__ void __launch_bounds__(256)
-    k_resid_norm(const int4* __restrict__ tiles, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fr,
+    k_resid_norm(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fr,
                  const double* __restrict__ rhs, const FabView* __restrict__ fp, const double* __restrict__ phi,
                  Coef cf, double* __restrict__ partial) {
   __shared__ double scratch[32];
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(256)
     const FabView P = fp[t.x], R = fr[t.x];
     const double* p = phi + P.off + (int64_t)j * P.s1 + k;
     const double* r = rhs + R.off + (int64_t)j * R.s1 + k;
-    const int iend = min(t.y + kTI, g.n[0]);
+    const int iend = min(t.y + ti, g.n[0]);
     int i = t.y;
     double xm = ldg(p + (int64_t)(i - 1) * P.s0);
     double c = ldg(p + (int64_t)i * P.s0);
@@ -809,6 +809,13 @@ extern "C" const char* amrb_last_error(void) { return amrb::g_last_error.c_str()
 extern "C" int amrb_version(void) { return 1; }
 extern "C" int64_t amrb_launch_count(void) { return (int64_t)amrb::g_launches.load(); }
 
+extern "C" int amrb_zero(double* ptr, int64_t n, void* stream) {
+  return amrb::guarded([&] {
+    if (n < 0 || (n && !ptr)) throw amrb::Error(AMRB_EINVAL, "amrb_zero: bad arguments");
+    if (n) AMRB_CUDA(cudaMemsetAsync(ptr, 0, (size_t)n * sizeof(double), (cudaStream_t)stream));
+  });
+}
+
 extern "C" int amrb_level_create(int nboxes, const int32_t* boxes, const uint8_t* resident, amrb_level** out) {
   return guarded([&] {
     if (nboxes < 0 || (nboxes && !boxes) || !out) throw Error(AMRB_EINVAL, "amrb_level_create: bad arguments");
@@ -872,7 +879,20 @@ namespace {
 template <class K, class... Args>
 void launch_tiles(const TileTable& tt, K kernel, cudaStream_t st, dim3 block, Args... args) {
   if (tt.host.empty()) return;
-  kernel<<<(unsigned)tt.host.size(), block, 0, st>>>(tt.dev.p, args...);
+  kernel<<<(unsigned)tt.host.size(), block, 0, st>>>(tt.dev.p, tt.ti, args...);
+}
+
+// Tile depth along i: 8 planes per CTA (register reuse along i) on levels big
+// enough to fill the chip several times over, 1 plane on small levels so the
+// latency-bound work spreads over more CTAs.
+int pick_ti(const Level& lv, int tj, int tk) {
+  long long tiles8 = 0;
+  for (int b = 0; b < lv.nboxes; ++b) {
+    if (!lv.resident[b]) continue;
+    const BoxGeom& g = lv.geo[b];
+    tiles8 += (long long)((g.n[0] + 7) / 8) * ((g.n[1] + tj - 1) / tj) * ((g.n[2] + tk - 1) / tk);
+  }
+  return tiles8 >= 4LL * num_sms() ? 8 : 1;
 }
 }  // namespace
 
@@ -883,7 +903,7 @@ extern "C" int amrb_lap_apply(const amrb_level* lv_, amrb_field* out, double* ou
     need_ghost(F(phi), 1, "lap_apply");
     need_same_level(F(out), lv, "lap_apply");
     need_same_level(F(phi), lv, "lap_apply");
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     launch_tiles(tt, k_stencil<Op::kLap>, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(out).dev.p, out_base,
                  (const FabView*)nullptr, (const double*)nullptr, F(phi).dev.p, phi_base, make_coef(dh));
     check_launch("k_stencil<lap>");
@@ -897,7 +917,7 @@ extern "C" int amrb_residual(const amrb_level* lv_, amrb_field* r, double* r_bas
     Level& lv = Lm(lv_);
     need_ghost(F(phi), 1, "residual");
     for (auto* f : {r, (amrb_field*)rhs, (amrb_field*)phi}) need_same_level(F(f), lv, "residual");
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     launch_tiles(tt, k_stencil<Op::kResid>, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(r).dev.p, r_base,
                  F(rhs).dev.p, rhs_base, F(phi).dev.p, phi_base, make_coef(dh));
     check_launch("k_stencil<resid>");
@@ -912,7 +932,7 @@ extern "C" int amrb_gsrb_color(const amrb_level* lv_, amrb_field* phi, double* p
     need_same_level(F(phi), lv, "gsrb_color");
     need_same_level(F(rhs), lv, "gsrb_color");
     if (color != 0 && color != 1) throw Error(AMRB_EINVAL, "color must be 0 or 1");
-    const auto& tt = lv.tiles(kTI, kTJ, 2 * kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, 2 * kTK), kTJ, 2 * kTK);
     launch_tiles(tt, k_gsrb_color, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(phi).dev.p, phi_base,
                  F(rhs).dev.p, rhs_base, make_coef(dh), color);
     check_launch("k_gsrb_color");
@@ -1057,7 +1077,7 @@ extern "C" int amrb_restrict(const amrb_level* clv_, amrb_field* crse, double* c
     need_same_level(F(crse), lv, "restrict");
     const int3 r = ratio3(ratio);
     if (mode != 0 && mode != 1) throw Error(AMRB_EINVAL, "restrict mode must be 0 (average) or 1 (injection)");
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     launch_tiles(tt, k_restrict, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(crse).dev.p, crse_base,
                  F(fine).dev.p, fine_base, ncomp, r, mode, 1.0 / (r.x * r.y * r.z));
     check_launch("k_restrict");
@@ -1071,7 +1091,7 @@ extern "C" int amrb_residual_restrict(const amrb_level* clv_, amrb_field* crse, 
     Level& lv = Lm(clv_);
     need_same_level(F(crse), lv, "residual_restrict");
     need_ghost(F(phi), 1, "residual_restrict");
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     launch_tiles(tt, k_resid_restrict, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(crse).dev.p, crse_base,
                  F(rhs).dev.p, rhs_base, F(phi).dev.p, phi_base, make_coef(dh));
     check_launch("k_resid_restrict");
@@ -1085,7 +1105,7 @@ extern "C" int amrb_prolong(const amrb_level* flv_, amrb_field* fine, double* fi
     need_same_level(F(fine), lv, "prolong");
     const int3 r = ratio3(ratio);
     const int3 sh = make_int3(r.x == 2, r.y == 2, r.z == 2);
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     launch_tiles(tt, k_prolong, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(fine).dev.p, fine_base,
                  F(crse).dev.p, crse_base, ncomp, add, sh);
     check_launch("k_prolong");
@@ -1100,7 +1120,7 @@ extern "C" int amrb_residual_norm(const amrb_level* lv_, const amrb_field* rhs, 
     need_ghost(F(phi), 1, "residual_norm");
     need_same_level(F(rhs), lv, "residual_norm");
     need_same_level(F(phi), lv, "residual_norm");
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     const int n = (int)tt.host.size();
     if (lv.partials.n < (size_t)std::max(n, 1)) lv.partials.alloc(std::max(n, 1));
     cudaStream_t st = (cudaStream_t)stream;
@@ -1120,7 +1140,7 @@ extern "C" int amrb_reduce(const amrb_level* lv_, const amrb_field* x, const dou
     Level& lv = Lm(lv_);
     if (kind < 0 || kind > 3) throw Error(AMRB_EINVAL, "unknown reduction kind");
     need_same_level(F(x), lv, "reduce");
-    const auto& tt = lv.tiles(kTI, kTJ, kTK);
+    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     const int n = (int)tt.host.size();
     if (lv.partials.n < (size_t)std::max(n, 1)) lv.partials.alloc(std::max(n, 1));
     cudaStream_t st = (cudaStream_t)stream;

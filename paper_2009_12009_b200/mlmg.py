@@ -117,6 +117,11 @@ class _Level:
     pass
 
 
+def _zero(fa):
+    st = fa.storage
+    check(lib().amrb_zero(C.c_void_p(st.data_ptr()), st.numel(), stream_ptr()))
+
+
 class MLMG:
     """V(nu1, nu2) multigrid for L(phi) = rhs on a periodic 3-D domain.
 
@@ -334,7 +339,7 @@ class MLMG:
         for l in range(T):
             lv = L[l]
             if l > 0:
-                lv.phi[lv.cur].storage.zero_()
+                _zero(lv.phi[lv.cur])
             if l == n - 1:
                 self._smooth(lv, self.bottom_sweeps)
                 break
