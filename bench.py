@@ -22,7 +22,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 
@@ -33,6 +32,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 cell-updates/s (GSRB, %HBM roofline); MLMG 256^3 solve time @1/2/4/8 GPU"
 UNIT = "cell-updates/s"
+
+
+def _traffic(alg_bytes):
+    """dram read+write bytes per launch of the roofline kernel from the committed
+    ncu capture (profiles/fine_sweep_traffic.json, see profiles/prof_fine_sweep.py);
+    None when absent or captured on another layout."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "fine_sweep_traffic.json")) as f:
+            t = json.load(f)
+        if "k_gsrb_sweep5" in t.get("kernel", "") and t.get("alg_bytes_per_launch", alg_bytes) == alg_bytes:
+            return t["traffic_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
 
 
 def _peaks():
@@ -52,49 +65,64 @@ def _domain_for(n_gpus):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled every ~2 ms through NVML on a
+    background thread while the timed region runs (nvidia-smi's 100 ms minimum
+    period would catch one or two samples of a ~50 ms region)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
+        self.rows = []
+        self.err = None
+        self._stop = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml as N
+
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[self.index].isdigit() else self.index
+            h = N.nvmlDeviceGetHandleByIndex(idx)
+            self._max = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = [(n, getattr(N, attr)) for n, attr in self.NAMES]
+        except Exception as e:  # no NVML: report unsampled
+            self.err = repr(e)
+            return self
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    clk = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((clk, [n for n, bit in bits if rs & bit]))
+                except Exception as e:
+                    self.err = repr(e)
+                    return
+                self._stop.wait(0.002)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=5)
 
     def summary(self):
-        rows = []
-        for line in (self.out or "").splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                try:
-                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
-                except ValueError:
-                    pass
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for _, _, flags in rows for n, f in zip(names, flags) if f.lower() == "active"})
-        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        reasons = sorted({n for _, rs in self.rows for n in rs})
+        return {"sm_mhz": float(np.median([c for c, _ in self.rows])), "sm_max_mhz": self._max,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 2 ms period"}
 
 
 def run_reference(args):
@@ -212,14 +240,14 @@ def run_ours(args):
         phi.setval(0.0)
         return mg.solve(phi, rhs, rtol=1e-10, max_iter=100)
 
-    clk = ClockSampler(local)
-    clk.__enter__()  # nvidia-smi needs ~0.1 s to start: sample from the warm-up on
     for _ in range(args.warmup):
         one_solve()
     iters = []
     launches0 = lib().amrb_launch_count()
     replays0 = mg.graph_replays
     barrier()
+    clk = ClockSampler(local)
+    clk.__enter__()
     st = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -284,6 +312,7 @@ def run_ours(args):
     alg_bytes = 24 * nloc + 8 * floc
     achieved = alg_bytes / t_sweep / 1e9
     peak, peak_kind = _peaks()
+    traffic = _traffic(alg_bytes)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,9 +334,9 @@ def run_ours(args):
             },
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": 1e3 * t_e2e / args.steps},
-            "roofline": {"bound": "hbm", "kernel": "k_gsrb_sweep4 (fine level, fused red+black, TMA-fed)",
+            "roofline": {"bound": "hbm", "kernel": "k_gsrb_sweep5 (fine level, fused red+black, TMA-fed)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "peak_kind": peak_kind, "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                         "peak_kind": peak_kind, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "us_per_launch": t_sweep * 1e6,
                          "kernel_cell_updates_per_s": nloc / t_sweep},
             "gpu_launches": int(launches),

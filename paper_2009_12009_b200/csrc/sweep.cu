@@ -320,6 +320,303 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
 }
 
 // ---------------------------------------------------------------------------
+// k_gsrb_sweep5: same schedule and result as k_gsrb_sweep4, re-balanced for
+// the B200 (ncu of sweep4: issue-bound at ~227 warp-instructions per warp-step,
+// every relaxation a serial LDS -> 9-deep DADD chain, one plane of phi in
+// flight, barrier waits on the one warp that also issued TMA and relaxed ring
+// columns).
+//
+//  * only phi goes through shared memory (TMA ring of D+5 plane tiles); rhs,
+//    read once per cell per sweep, is loaded by each lane straight into
+//    registers two steps ahead (ld.global.nc);
+//  * the step body is branch-free: all shared loads first, both of a lane's
+//    relaxations computed unconditionally and selected, so their DADD chains
+//    interleave;
+//  * warp roles balance the per-step latency at <= 2 chains per warp:
+//      warp 0          red cells of the two ring rows (j0-1, j0+TJ), one per lane,
+//      warps 1..TJ     tile row j0+w-1: black(p) or red(p+2) per lane, streams plane p out,
+//      warp TJ+1       red cells of the two ring columns (k0-1, k0+TK), and issues the TMA;
+//  * ring-slot indices, mbarrier phases and pointers advance incrementally.
+// ---------------------------------------------------------------------------
+template <int TJ, int TK, int D>
+struct Sweep5Layout {
+  // smem row = TMA box width: cols k0-2 .. k0+TK+3 (two spare columns keep the
+  // ring-column warp's every-other-row accesses off a single bank pair)
+  static constexpr int PK = TK + 6;
+  static constexpr int PJ = TJ + 4;
+  static constexpr int NPHI = D + 5;
+  static constexpr int PBYTES = PJ * PK * 8;
+  static constexpr int PSTRIDE = (PBYTES + 127) / 128 * 128;
+  static constexpr int BAR_OFF = NPHI * PSTRIDE;
+  static constexpr int BYTES = BAR_OFF + 8 * NPHI;
+  static constexpr int NW = TJ + 2;
+  static constexpr int NH = (TK + 31) / 32;
+};
+
+template <int TJ, int TK, int D, int MINB, bool FIXED>
+__global__ void __launch_bounds__(32 * (TJ + 2), MINB)
+    k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, Sweep4Args args) {
+  using LY = Sweep5Layout<TJ, TK, D>;
+  constexpr int PK = LY::PK, NPHI = LY::NPHI, NH = LY::NH, NW = LY::NW;
+  static_assert(TJ % 2 == 0 && TJ + 2 <= 32, "ring-column warp holds one cell per lane");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + LY::BAR_OFF);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int ROLE_RROW = 0, ROLE_ROW = 1, ROLE_RCOL = 2;
+  const int role = warp == 0 ? ROLE_RROW : (warp == NW - 1 ? ROLE_RCOL : ROLE_ROW);
+  const int producer = 32 * (NW - 1);  // lane 0 of the ring-column warp
+  const Coef cf = args.cf;
+  auto slot = [&](int idx) { return reinterpret_cast<double*>(smem_raw + idx * LY::PSTRIDE); };
+  auto wrap = [](int x) { return x >= NPHI ? x - NPHI : x; };
+
+  const long long G = gridDim.x;
+  long long s = args.total * blockIdx.x / G;
+  const long long e = args.total * (blockIdx.x + 1) / G;
+  if (s >= e) return;
+  int col = 0;
+  {
+    int lo = 0, hi = args.ncols - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (args.cols[mid].w <= s)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    col = lo;
+  }
+  bool first_segment = true;
+  while (s < e) {
+    const int4 cd = args.cols[col];
+    const BoxGeom g = args.geo[cd.x];
+    const FabView B = args.fb[cd.x];
+    const FabView RV = args.fr[cd.x];
+    const int bslot = args.slot[cd.x];
+    const int j0 = cd.y, k0 = cd.z;
+    const int i0 = (int)(s - cd.w);
+    const int i1 = (int)min((long long)g.n[0], e - cd.w);
+    s += i1 - i0;
+    ++col;
+    const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
+    // smem cell (row, c) of plane ip is red iff ((g.lo[0] + ip + jk0 + row + c) & 1) == 0
+    const int par0 = (g.lo[0] + i0 + jk0) & 1;  // parity base of plane i0
+
+    __syncthreads();
+    if (tid == producer) {
+      for (int x = 0; x < NPHI; ++x) {
+        if (!first_segment) mbar_inval(&bars[x]);
+        mbar_init(&bars[x], 1);
+      }
+      fence_barrier_init();
+    }
+    first_segment = false;
+    __syncthreads();
+
+    // plane ip lives in slot (ip - i0 + 2) % NPHI
+    auto issue = [&](int ip, int idx) {
+      mbar_expect_tx(&bars[idx], LY::PBYTES);
+      tma_load4(slot(idx), &tmA, &bars[idx], k0 + args.a_kc, j0 + args.a_jc, ip + args.a_ic, bslot);
+    };
+    if (tid == producer)
+      for (int ip = i0 - 2; ip <= min(i0 + 2 + D, i1 + 1); ++ip) issue(ip, ip - i0 + 2);
+
+    auto is_fixed = [&](int gi, int rw, int c) {
+      const int gj = g.lo[1] + j0 - 2 + rw, gk = g.lo[2] + k0 - 2 + c;
+      return gi < args.fixed_lo[0] || gi > args.fixed_hi[0] || gj < args.fixed_lo[1] || gj > args.fixed_hi[1] ||
+             gk < args.fixed_lo[2] || gk > args.fixed_hi[2];
+    };
+    auto relax_at = [&](const double* P, const double* Pm, const double* Pp, double rh, int o) {
+      const double v = P[o];
+      const double lap = lap7(v, Pm[o], Pp[o], P[o - PK], P[o + PK], P[o - 1], P[o + 1], cf);
+      return relax(v, rh, lap, cf.rgamma);
+    };
+    const double* rbase = args.rhs + RV.off + (int64_t)(j0 - 2) * RV.s1 + (k0 - 2);  // smem (0, 0) of plane 0
+    const int64_t rs0 = RV.s0, rs1 = RV.s1;
+
+    for (int ip = i0 - 2; ip <= i0 + 2; ++ip) mbar_wait(&bars[ip - i0 + 2], 0);
+    // prologue: red of planes i0-1, i0, i0+1 over rows 1..TJ+2, cols 1..TK+2
+    // (independent: red reads only black cells).  Red cells only, loads first.
+    {
+      constexpr int RW = TJ + 2, HC = (TK + 2) / 2;  // red cells per ring-row
+      constexpr int NCELL = 3 * RW * HC;
+      constexpr int NIT = (NCELL + 32 * NW - 1) / (32 * NW);
+      double rh[NIT];
+      int oo[NIT], pl[NIT];
+      bool ok[NIT];
+#pragma unroll
+      for (int it = 0; it < NIT; ++it) {
+        const int x = tid + it * 32 * NW;
+        ok[it] = x < NCELL;
+        const int xx = ok[it] ? x : 0;
+        pl[it] = xx / (RW * HC);
+        const int rem = xx - pl[it] * RW * HC;
+        const int rw = 1 + rem / HC;
+        const int ip = i0 - 1 + pl[it];
+        const int c = 1 + ((par0 + pl[it] + 1 + rw + 1) & 1) + 2 * (rem % HC);  // red column
+        oo[it] = rw * PK + c;
+        if (FIXED && is_fixed(g.lo[0] + ip, rw, c)) ok[it] = false;
+        rh[it] = ok[it] ? __ldg(rbase + (int64_t)ip * rs0 + (int64_t)rw * rs1 + c) : 0.0;
+      }
+#pragma unroll
+      for (int it = 0; it < NIT; ++it) {
+        double* P = slot(pl[it] + 1);
+        const double v = relax_at(P, slot(pl[it]), slot(pl[it] + 2), rh[it], oo[it]);
+        if (ok[it]) P[oo[it]] = v;
+      }
+    }
+    fence_proxy_async();
+
+    // ---- per-role geometry -------------------------------------------------
+    // ROLE_ROW: row r = warp+1, column c = 2 + lane + 32h; cell black in plane p
+    //           iff ((par0 + (p - i0) + r + lane) & 1) == 1 (same colour in p+2).
+    // ROLE_RROW: red cell m = lane + 32h of the ring rows (m < TK/2: row 1, else
+    //           row TJ+2), column 2 + 2 idx + parity; plane p+2.
+    // ROLE_RCOL: red cell m = lane of the ring columns (m < (TJ+2)/2: col 1, else
+    //           col TK+2), row 1 + 2 idx + parity; plane p+2.
+    const int r = warp + 1;
+    const int lk = TK >= 32 ? lane : (lane & (TK - 1));  // idle lanes alias a valid column
+    int rrow[NH], ridx[NH];
+    bool rok[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      const int m = lane + 32 * h;
+      rok[h] = m < TK;
+      const int mm = rok[h] ? m : 0;
+      rrow[h] = mm < TK / 2 ? 1 : TJ + 2;
+      ridx[h] = mm < TK / 2 ? mm : mm - TK / 2;
+    }
+    const bool cok = lane < TJ + 2;
+    const int cm = cok ? lane : 0;
+    const int ccol = cm < (TJ + 2) / 2 ? 1 : TK + 2;
+    const int cidx = cm < (TJ + 2) / 2 ? cm : cm - (TJ + 2) / 2;
+    // smem offset of the role's cell h in plane q (q relative to i0: colour flips with q)
+    auto cell_off = [&](int q, int h) {
+      if (role == ROLE_ROW) return r * PK + 2 + lk + 32 * h;
+      if (role == ROLE_RROW) return rrow[h] * PK + 2 + ((par0 + q + rrow[h]) & 1) + 2 * ridx[h];
+      return (1 + ((par0 + q + ccol + 1) & 1) + 2 * cidx) * PK + ccol;
+    };
+
+    // rhs of the cells step p relaxes, straight to registers
+    auto load_rhs = [&](int p, double (&rv)[NH]) {
+      const int q = p - i0;
+      if (role == ROLE_ROW) {
+        const bool blk = ((par0 + q + r + lane) & 1) != 0;
+        const int t = blk ? p : p + 2;
+        const bool need = (TK >= 32 || lane < TK) && p < i1 && (blk || p + 2 <= i1);
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          rv[h] = need ? __ldg(rbase + (int64_t)t * rs0 + (int64_t)r * rs1 + 2 + lk + 32 * h) : 0.0;
+      } else {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const bool need = p + 2 <= i1 && (role == ROLE_RROW ? rok[h] : (h == 0 && cok));
+          const int o = cell_off(q + 2, h);
+          const int rw = o / PK, c = o - rw * PK;
+          rv[h] = need ? __ldg(rbase + (int64_t)(p + 2) * rs0 + (int64_t)rw * rs1 + c) : 0.0;
+        }
+      }
+    };
+
+    // rhs one step ahead; a lane's colour is the same in steps p and p+2, so a
+    // red lane streams out at step p the red(p) it computed at step p-2 (vpA /
+    // vpB by step parity; the first two come from the prologue, in shared)
+    double rv[NH], vpA[NH], vpB[NH];
+    load_rhs(i0, rv);
+    int m1 = 1;                         // slot of plane p-1
+    int widx = 5 % NPHI;                // slot of plane p+3 (awaited)
+    unsigned wph = (5 / NPHI) & 1;
+    int iidx = 0;                       // slot of plane p+3+D (issued)
+    double* out = args.b + B.off + (int64_t)i0 * B.s0 + (int64_t)(j0 - 2 + r) * B.s1 + (k0 + lk);
+    const int64_t bs0 = B.s0;
+
+    auto step = [&](int p, double (&vp)[NH]) {
+      const int q = p - i0;
+      const bool do_red = p + 2 <= i1;
+      if (do_red) mbar_wait(&bars[widx], wph);
+      widx = wrap(widx + 1);
+      wph ^= widx == 0 ? 1u : 0u;
+      __syncthreads();
+      if (tid == producer && p + 3 + D <= i1 + 1) issue(p + 3 + D, iidx);
+      iidx = wrap(iidx + 1);
+      const double* Sm = slot(m1);
+      const double* S0 = slot(wrap(m1 + 1));
+      const double* S1 = slot(wrap(m1 + 2));
+      double* S2 = slot(wrap(m1 + 3));
+      const double* S3 = slot(wrap(m1 + 4));
+      m1 = wrap(m1 + 1);
+      if (role == ROLE_ROW) {
+        const bool blk = ((par0 + q + r + lane) & 1) != 0;
+        const double* P = blk ? S0 : S2;
+        const double* Pm = blk ? Sm : S1;
+        const double* Pp = blk ? S1 : S3;
+        const bool lane_ok = TK >= 32 || lane < TK;
+        const bool act = lane_ok && (blk || do_red);
+        // all shared loads first (red(p+2) writes only red cells of S2, which no
+        // lane reads in this step except as its own centre value)
+        double c[NH], xm[NH], xp[NH], ym[NH], yp[NH], zm[NH], zp[NH];
+        if (q < 2) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) vp[h] = S0[r * PK + 2 + lk + 32 * h];
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int o = r * PK + 2 + lk + 32 * h;
+          c[h] = P[o];
+          xm[h] = Pm[o];
+          xp[h] = Pp[o];
+          ym[h] = P[o - PK];
+          yp[h] = P[o + PK];
+          zm[h] = P[o - 1];
+          zp[h] = P[o + 1];
+        }
+        const int gi = g.lo[0] + (blk ? p : p + 2);
+        double v[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const double nv = relax(c[h], rv[h], lap7(c[h], xm[h], xp[h], ym[h], yp[h], zm[h], zp[h], cf), cf.rgamma);
+          const bool a = act && !(FIXED && is_fixed(gi, r, 2 + lk + 32 * h));
+          v[h] = a ? nv : c[h];
+          if (a && !blk) S2[r * PK + 2 + lk + 32 * h] = v[h];
+        }
+        if (lane_ok) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) out[32 * h] = blk ? v[h] : vp[h];
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h) vp[h] = v[h];
+      } else if (do_red) {
+        // ring rows / ring columns: red(p+2) only
+        double nv[NH];
+        int o[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          o[h] = cell_off(q + 2, h);
+          nv[h] = relax_at(S2, S1, S3, rv[h], o[h]);
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          bool a = role == ROLE_RROW ? rok[h] : (h == 0 && cok);
+          if (FIXED && a) {
+            const int rw = o[h] / PK, cc = o[h] - rw * PK;
+            a = !is_fixed(g.lo[0] + p + 2, rw, cc);
+          }
+          if (a) S2[o[h]] = nv[h];
+        }
+      }
+      out += bs0;
+      load_rhs(p + 1, rv);
+      if (q & 1) fence_proxy_async();
+    };
+    for (int p = i0; p < i1; p += 2) {
+      step(p, vpA);
+      if (p + 1 < i1) step(p + 1, vpB);
+    }
+    fence_proxy_async();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -474,30 +771,98 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
   return true;
 }
 
+template <int TJ, int TK, int D, int MINB>
+bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
+             const double* r_base, const Coef& cf, const int fixed_lo[3], const int fixed_hi[3], bool fixed,
+             cudaStream_t st) {
+  using LY = Sweep5Layout<TJ, TK, D>;
+  for (auto& gg : lv.geo)
+    if (gg.n[1] % TJ || gg.n[2] % TK) return false;
+  if (a.ngrow < 2 || r.ngrow < 1) return false;
+  CUtensorMap ma;
+  std::memset(&ma, 0, sizeof ma);
+  Sweep4Args args;
+  std::memset(&args, 0, sizeof args);
+  TmaDesc da = describe(lv, a);
+  if (!da.ok || da.slot != lv.slot) return false;
+  int nres = 0;
+  for (auto x : lv.resident) nres += x ? 1 : 0;
+  if (!make_map(&ma, a_base, da, nres, LY::PJ, LY::PK)) return false;
+  args.a_kc = -2 + da.g + da.f;
+  args.a_jc = -2 + da.g;
+  args.a_ic = da.g;
+  const auto& cols = lv.columns(TJ, TK);
+  if (cols.host.empty()) return true;
+  args.cols = cols.dev.p;
+  args.fa = a.dev.p;
+  args.fr = r.dev.p;
+  args.a = a_base;
+  args.rhs = r_base;
+  args.slot = lv.dslot.p;
+  args.ncols = (int)cols.host.size();
+  args.total = cols.total;
+  args.geo = lv.dgeo.p;
+  args.fb = b.dev.p;
+  args.b = b_base;
+  args.cf = cf;
+  for (int x = 0; x < 3; ++x) {
+    args.fixed_lo[x] = fixed_lo[x];
+    args.fixed_hi[x] = fixed_hi[x];
+  }
+  auto kern = fixed ? k_gsrb_sweep5<TJ, TK, D, MINB, true> : k_gsrb_sweep5<TJ, TK, D, MINB, false>;
+  static int per_sm[2] = {0, 0};
+  if (!per_sm[fixed]) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[fixed], kern, 32 * LY::NW, LY::BYTES));
+    per_sm[fixed] = std::max(per_sm[fixed], 1);
+  }
+  const long long slots = (long long)per_sm[fixed] * num_sms();
+  const long long ncol = (long long)cols.host.size();
+  // balanced contiguous (column, plane) ranges; aligning ranges across columns
+  // (grid = ncol * (slots / ncol)) cut L2 misses but measured no faster
+  const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
+  kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES, st>>>(ma, args);
+  check_launch("k_gsrb_sweep5");
+  return true;
+}
+
 }  // namespace
 
 bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                       const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
                       const int fixed_hi[3], bool fixed, cudaStream_t st) {
-  // Tile: TK = widest of 64/32/16 dividing every box's k-extent, TJ = 16 (8 for
-  // small boxes); one plane of prefetch.  (C3 fine level: 114.6 us.  Deeper
-  // prefetch, 1-D bulk copies, cp.async and register-staged loads were all
-  // slower on B200 -- see DESIGN.md.)
+  // Tile: TK = widest of 64/32/16 dividing every box's k-extent.  C3 fine level
+  // (64 boxes of 64^3): k_gsrb_sweep5 104.5 us, k_gsrb_sweep4 114.6 us; see
+  // DESIGN.md for the variants measured.
   int mink = 1 << 30, minj = 1 << 30;
   for (auto& g : lv.geo) {
     mink = std::min(mink, g.n[2]);
     minj = std::min(minj, g.n[1]);
   }
-#define AMRB_TRY(TJ, TK) \
+  // 16-row tiles (boxes >= 32 in j): k_gsrb_sweep5, D = 2, two CTAs/SM.  8-row
+  // tiles (small, L2-resident levels): k_gsrb_sweep4, which measured faster there.
+  // AMRB_SWEEP_IMPL=4 forces k_gsrb_sweep4 everywhere (A/B runs).
+  static const int impl = getenv("AMRB_SWEEP_IMPL") ? atoi(getenv("AMRB_SWEEP_IMPL")) : 5;
+#define AMRB_TRY4(TJ, TK) \
   if (launch4<TJ, TK, 1, 1, false>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st)) return true;
-  if (minj >= 64) {
-    AMRB_TRY(16, 64)
-    AMRB_TRY(16, 32)
+#define AMRB_TRY5(TJ, TK) \
+  if (launch5<TJ, TK, 2, 2>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st)) return true;
+  if (minj >= 32) {
+    if (impl == 4) {
+      if (minj >= 64) {
+        AMRB_TRY4(16, 64)
+        AMRB_TRY4(16, 32)
+      }
+    } else {
+      AMRB_TRY5(16, 64)
+      AMRB_TRY5(16, 32)
+    }
   }
-  AMRB_TRY(8, 64)
-  AMRB_TRY(8, 32)
-  AMRB_TRY(8, 16)
-#undef AMRB_TRY
+  AMRB_TRY4(8, 64)
+  AMRB_TRY4(8, 32)
+  AMRB_TRY4(8, 16)
+#undef AMRB_TRY4
+#undef AMRB_TRY5
   (void)mink;
   return false;
 }
