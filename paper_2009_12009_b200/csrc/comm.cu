@@ -16,9 +16,8 @@
 //               contributions in plan order, which keeps sums bit-identical to
 //               the reference for any rank count.
 //
-// The kernel walks a flat index space over all records of a wave: each CTA
-// covers CHUNK consecutive cells, knows the first record of its chunk, and
-// binary-searches the record prefix for each cell.
+// The kernel walks a flat index space over all records of a wave (see k_copy
+// for how records map to CTAs).
 #include <nccl.h>
 
 #include <algorithm>
@@ -61,34 +60,82 @@ struct Wave {
   int64_t total = 0;
 };
 
-// One CTA per (record, chunk of kChunk flat indices): no search, and each
-// thread issues all of its loads before its stores so remote (NVLink) and
-// local latencies overlap.
+// Blocks: a record of >= kSmall flat indices gets one CTA per chunk of kChunk
+// (no search); runs of consecutive small records (edges and corners: 1-64
+// cells each) are packed into shared CTAs of up to kChunk indices / kPackMax
+// records, and each thread binary-searches the packed records' offsets (staged
+// in shared memory).  Every thread issues all of its loads before its stores
+// so remote (NVLink) and local latencies overlap.
+constexpr int kSmall = kChunk / 4;
+constexpr int kPackMax = 256;
+
+__device__ __forceinline__ void rec_cell(const DevRec& r, int64_t loc, int64_t cells, int64_t& so, int64_t& dofs) {
+  const int c = (int)(loc / cells);
+  int t = (int)(loc - (int64_t)c * cells);
+  const int k = t % r.e2;
+  t /= r.e2;
+  const int j = t % r.e1;
+  const int i = t / r.e1;
+  so = r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k;
+  dofs = r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
+}
+
 template <bool kAdd>
 __global__ void __launch_bounds__(kCopyThreads)
     k_copy(const DevRec* __restrict__ recs, const int2* __restrict__ blocks, int ncomp,
            const double* __restrict__ src, const double* __restrict__ buf, double* __restrict__ dst,
-           PeerPtrs peers) {
+           const __grid_constant__ PeerPtrs peers) {
   const int2 bl = blocks[blockIdx.x];
-  const DevRec r = recs[bl.x];
-  const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
-  const int64_t end = min(cells * ncomp, (int64_t)bl.y + kChunk);
-  const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
   double v[kCopyItems];
   int64_t dofs[kCopyItems];
+  if (bl.x >= 0) {  // one large record, chunk starting at flat index bl.y
+    const DevRec r = recs[bl.x];
+    const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
+    const int64_t end = min(cells * ncomp, (int64_t)bl.y + kChunk);
+    const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
 #pragma unroll
-  for (int u = 0; u < kCopyItems; ++u) {
-    const int64_t loc = (int64_t)bl.y + u * kCopyThreads + threadIdx.x;
-    dofs[u] = -1;
-    if (loc < end) {
-      const int c = (int)(loc / cells);
-      int t = (int)(loc - (int64_t)c * cells);
-      const int k = t % r.e2;
-      t /= r.e2;
-      const int j = t % r.e1;
-      const int i = t / r.e1;
-      v[u] = s[r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k];
-      dofs[u] = r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
+    for (int u = 0; u < kCopyItems; ++u) {
+      const int64_t loc = (int64_t)bl.y + u * kCopyThreads + threadIdx.x;
+      dofs[u] = -1;
+      if (loc < end) {
+        int64_t so, dof;
+        rec_cell(r, loc, cells, so, dof);
+        dofs[u] = dof;
+        v[u] = s[so];
+      }
+    }
+  } else {  // records -bl.x-1 .. -bl.x-1+bl.y-1, packed
+    __shared__ int64_t beg[kPackMax + 1];
+    const int r0 = -bl.x - 1, cnt = bl.y;
+    const int64_t base = recs[r0].begin;
+    for (int q = threadIdx.x; q < cnt; q += kCopyThreads) beg[q] = recs[r0 + q].begin - base;
+    if (threadIdx.x == 0) {
+      const DevRec& last = recs[r0 + cnt - 1];
+      beg[cnt] = last.begin - base + (int64_t)last.e0 * last.e1 * last.e2 * ncomp;
+    }
+    __syncthreads();
+    const int64_t total = beg[cnt];
+#pragma unroll
+    for (int u = 0; u < kCopyItems; ++u) {
+      const int64_t loc = (int64_t)u * kCopyThreads + threadIdx.x;
+      dofs[u] = -1;
+      if (loc < total) {
+        int lo = 0, hi = cnt - 1;  // last q with beg[q] <= loc
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (beg[mid] <= loc)
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        const DevRec& r = recs[r0 + lo];
+        const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
+        const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
+        int64_t so, dof;
+        rec_cell(r, loc - beg[lo], cells, so, dof);
+        dofs[u] = dof;
+        v[u] = s[so];
+      }
     }
   }
 #pragma unroll
@@ -141,13 +188,30 @@ int64_t cell_offset(const Tab& tab, int b, const int lo[3]) {
 void prepare_wave(Wave& w, int ncomp) {
   w.total = 0;
   w.blocks.clear();
+  int pack0 = -1, packn = 0;  // open run of small records
+  int64_t packc = 0;
+  auto close_pack = [&] {
+    if (packn) w.blocks.push_back(make_int2(-pack0 - 1, packn));
+    pack0 = -1;
+    packn = 0;
+    packc = 0;
+  };
   for (size_t i = 0; i < w.host.size(); ++i) {
     DevRec& r = w.host[i];
     const int64_t n = (int64_t)r.e0 * r.e1 * r.e2 * ncomp;
     r.begin = w.total;
     w.total += n;
-    for (int64_t o = 0; o < n; o += kChunk) w.blocks.push_back(make_int2((int)i, (int)o));
+    if (n >= kSmall) {
+      close_pack();  // packs hold consecutive records only
+      for (int64_t o = 0; o < n; o += kChunk) w.blocks.push_back(make_int2((int)i, (int)o));
+      continue;
+    }
+    if (packn && (packc + n > kChunk || packn == kPackMax)) close_pack();
+    if (!packn) pack0 = (int)i;
+    ++packn;
+    packc += n;
   }
+  close_pack();
   w.recs.upload(w.host);
   w.dblocks.upload(w.blocks);
 }

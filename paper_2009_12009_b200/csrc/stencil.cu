@@ -610,7 +610,9 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Prolongation (pc), optionally added: fine(c) (+)= crse(c / 2).
+// Prolongation (pc), optionally added: fine(c) (+)= crse(c / 2).  Planes go
+// four at a time with every load issued before the first store (four fine
+// reads in flight per thread instead of one).
 __global__ void __launch_bounds__(256)
     k_prolong(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ fgeo, const FabView* __restrict__ ff,
               double* __restrict__ fine, const FabView* __restrict__ fc, const double* __restrict__ crse,
@@ -622,12 +624,26 @@ __global__ void __launch_bounds__(256)
   const FabView F = ff[t.x], C = fc[t.x];
   const int iend = min(t.y + ti, g.n[0]);
   // coarse local index: floor((lo + x)/2) - floor(lo/2); lo is even on coarsenable layouts
-  for (int n = 0; n < ncomp; ++n)
-    for (int i = t.y; i < iend; ++i) {
-      const double c = crse[C.off + n * C.cs + (int64_t)(i >> sh.x) * C.s0 + (int64_t)(j >> sh.y) * C.s1 + (k >> sh.z)];
-      double* f = fine + F.off + n * F.cs + (int64_t)i * F.s0 + (int64_t)j * F.s1 + k;
+  for (int n = 0; n < ncomp; ++n) {
+    const double* cb = crse + C.off + n * C.cs + (int64_t)(j >> sh.y) * C.s1 + (k >> sh.z);
+    double* fb = fine + F.off + n * F.cs + (int64_t)j * F.s1 + k;
+    int i = t.y;
+    for (; i + 4 <= iend; i += 4) {
+      double c[4], f[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = ldg(cb + (int64_t)((i + u) >> sh.x) * C.s0);
+        f[u] = add ? fb[(int64_t)(i + u) * F.s0] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) fb[(int64_t)(i + u) * F.s0] = add ? f[u] + c[u] : c[u];
+    }
+    for (; i < iend; ++i) {
+      const double c = ldg(cb + (int64_t)(i >> sh.x) * C.s0);
+      double* f = fb + (int64_t)i * F.s0;
       *f = add ? *f + c : c;
     }
+  }
 }
 
 // ---------------------------------------------------------------------------
