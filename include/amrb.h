@@ -45,6 +45,7 @@ extern "C" {
 #define AMRB_ECUDA (-2)
 #define AMRB_ENCCL (-3)
 #define AMRB_ENOMEM (-4)
+#define AMRB_ENOTSUP (-5) /* valid request this fast path does not cover (caller falls back) */
 
 #define AMRB_FABTAB_W 8
 #define AMRB_REC_W 11 /* src, dst, src_lo[3], src_hi[3], shift[3] (3-D padded) */
@@ -186,6 +187,32 @@ int amrb_gsrb_sweep(const amrb_level* lv, const amrb_field* a, const double* a_b
                     const double* rhs_base, const double dh[3],
                     const int32_t* fixed_lohi, void* stream);
 
+/* Ghost push: FillBoundary (fabarray.py:364-374) fused into the kernel that
+ * produces a field.  A push table holds the fill plan's records whose source
+ * box this rank owns (rec11 = amrb_plan_records rows; fabtab = the GLOBAL fab
+ * table of the destination field: every box's layout inside its owner's
+ * allocation; owner = rank per box).  A producer given the table and the
+ * per-rank base pointers of the field (peer_bases[r] = rank r's allocation,
+ * NVLink-mapped symmetric memory for r != my_rank) stores every valid cell it
+ * writes also into each ghost cell the plan copies it to, so the ghosts are
+ * filled to `width` when the kernel ends (multi-GPU: after a device barrier).
+ * AMRB_ENOTSUP when a box is thinner than 2*width or the records are not the
+ * face/edge/corner slabs of a box (callers then fill with a copy program). */
+typedef struct amrb_push amrb_push;
+int amrb_push_create(const amrb_level* lv, int nrec, const int32_t* rec11,
+                     const int64_t* fabtab, int nboxes, const int32_t* owner,
+                     int my_rank, int nranks, int width, amrb_push** out);
+int amrb_push_destroy(amrb_push* p);
+
+/* amrb_gsrb_sweep that also fills b's ghosts (push table built for b's
+ * layout, width <= b's ngrow).  AMRB_ENOTSUP when the level does not take the
+ * k_gsrb_sweep5 path (nothing launched). */
+int amrb_gsrb_sweep_push(const amrb_level* lv, const amrb_field* a, const double* a_base,
+                         amrb_field* b, double* b_base, const amrb_field* rhs,
+                         const double* rhs_base, const double dh[3],
+                         const int32_t* fixed_lohi, const amrb_push* push,
+                         const uint64_t* peer_bases, int npeers, void* stream);
+
 /* average_down (coarse_fine.py:136-163) on the box-local coarsened layout
  * (crse box b = fine box b coarsened).  ratio = int32[3] per 3-D axis, each 1
  * or 2 (NULL = 2,2,2).  mode 0 "average": crse = mean of the children summed
@@ -209,6 +236,13 @@ int amrb_residual_restrict(const amrb_level* crse_lv, amrb_field* crse,
 int amrb_prolong(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
                  const amrb_field* crse, const double* crse_base, int ncomp,
                  const int32_t* ratio, int add, void* stream);
+
+/* amrb_prolong (ncomp = 1) that also fills fine's ghosts through a push
+ * table (see amrb_push_create). */
+int amrb_prolong_push(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
+                      const amrb_field* crse, const double* crse_base,
+                      const int32_t* ratio, int add, const amrb_push* push,
+                      const uint64_t* peer_bases, int npeers, void* stream);
 
 /* ||rhs - L(phi)||_inf over this device's valid cells, without writing the
  * residual (phi ghosts width 1 filled).  Result (one double) to dev_out. */

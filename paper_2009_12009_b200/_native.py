@@ -17,7 +17,7 @@ __all__ = ["lib", "check", "LIB_PATH", "AmrbError", "ptr", "i32p", "i64p", "u8p"
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libamrb.so")
 
-AMRB_OK, AMRB_EINVAL, AMRB_ECUDA, AMRB_ENCCL, AMRB_ENOMEM = 0, -1, -2, -3, -4
+AMRB_OK, AMRB_EINVAL, AMRB_ECUDA, AMRB_ENCCL, AMRB_ENOMEM, AMRB_ENOTSUP = 0, -1, -2, -3, -4, -5
 FABTAB_W = 8
 REC_W = 11
 
@@ -68,6 +68,10 @@ _SIGS = {
     "amrb_restrict": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
     "amrb_residual_restrict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
     "amrb_prolong": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
+    "amrb_push_create": (C.c_int, [vp, C.c_int, P(i32), P(i64), C.c_int, P(i32), C.c_int, C.c_int, C.c_int, P(vp)]),
+    "amrb_push_destroy": (C.c_int, [vp]),
+    "amrb_gsrb_sweep_push": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, P(C.c_uint64), C.c_int, vp]),
+    "amrb_prolong_push": (C.c_int, [vp, vp, vp, vp, vp, P(i32), C.c_int, vp, P(C.c_uint64), C.c_int, vp]),
     "amrb_reduce": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
     "amrb_residual_norm": (C.c_int, [vp, vp, vp, vp, vp, P(f64), vp, vp]),
     "amrb_coarse_tail": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),

@@ -47,7 +47,6 @@ struct DevRec {
   int32_t pad_ = 0;
 };
 
-constexpr int kMaxPeers = 8;
 struct PeerPtrs {
   const double* p[kMaxPeers];
 };

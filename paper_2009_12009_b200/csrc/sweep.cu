@@ -54,6 +54,7 @@ struct Sweep4Args {
   int a_kc, a_jc, a_ic;  // tensor-map coordinate offsets: phi plane ip, rows from j0-2, cols from k0-2
   int r_kc, r_jc, r_ic;  // rhs: rows from j0-1, cols from k0-2
   int fixed_lo[3], fixed_hi[3];
+  PushDev push;  // k_gsrb_sweep5<..., PUSH>: fill b's ghosts as planes are written
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -351,11 +352,15 @@ struct Sweep5Layout {
   static constexpr int BYTES = BAR_OFF + 8 * NPHI;
   static constexpr int NW = TJ + 2;
   static constexpr int NH = (TK + 31) / 32;
+  // PUSH: per (warp, destination slot 0..3NH-1, lane) element delta of the lane's
+  // interior-plane ghost destinations
+  static constexpr int PDEL_OFF = BYTES;
+  static constexpr int BYTES_PUSH = PDEL_OFF + NW * 3 * NH * 32 * 8;  // + NW flag words
 };
 
-template <int TJ, int TK, int D, int MINB, bool FIXED>
+template <int TJ, int TK, int D, int MINB, bool FIXED, bool PUSH>
 __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
-    k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, Sweep4Args args) {
+    k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ Sweep4Args args) {
   using LY = Sweep5Layout<TJ, TK, D>;
   constexpr int PK = LY::PK, NPHI = LY::NPHI, NH = LY::NH, NW = LY::NW;
   static_assert(TJ % 2 == 0 && TJ + 2 <= 32, "ring-column warp holds one cell per lane");
@@ -386,6 +391,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     }
     col = lo;
   }
+  bool remote = false;  // this thread stored ghosts on another rank
   bool first_segment = true;
   while (s < e) {
     const int4 cd = args.cols[col];
@@ -529,6 +535,28 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     int iidx = 0;                       // slot of plane p+3+D (issued)
     double* out = args.b + B.off + (int64_t)i0 * B.s0 + (int64_t)(j0 - 2 + r) * B.s1 + (k0 + lk);
     const int64_t bs0 = B.s0;
+    // ghost push (PUSH): in interior planes each lane cell has at most two
+    // destinations, fixed element deltas from its output address (computed
+    // here, kept in shared memory); the first/last g planes take push_cell.
+    // shared: [warp][slot 0..3NH-1][lane] deltas, then one flag word per warp
+    auto pdel = [&]() {
+      return reinterpret_cast<int64_t*>(smem_raw + LY::PDEL_OFF) + warp * 3 * NH * 32 + lane;
+    };
+    if (PUSH && role == ROLE_ROW) {
+      bool any = false;
+      int64_t* pd = pdel();
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        int64_t d[kPushMid] = {0, 0, 0};
+        if (TK >= 32 || lane < TK) push_deltas_mid(args.push, cd.x, j0 - 2 + r, k0 + lk + 32 * h, B, args.b, d, remote);
+#pragma unroll
+        for (int x = 0; x < kPushMid; ++x) pd[(3 * h + x) * 32] = d[x];
+        any |= d[0] != 0;
+      }
+      any = __any_sync(0xffffffffu, any);
+      if (lane == 0) reinterpret_cast<int*>(smem_raw + LY::BYTES_PUSH)[warp] = any ? 1 : 0;
+      __syncwarp();
+    }
 
     auto step = [&](int p, double (&vp)[NH]) {
       const int q = p - i0;
@@ -555,7 +583,9 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
         // all shared loads first (red(p+2) writes only red cells of S2, which no
         // lane reads in this step except as its own centre value)
         double c[NH], xm[NH], xp[NH], ym[NH], yp[NH], zm[NH], zp[NH];
-        if (q < 2) {
+        // red lanes stream out red(p): computed two steps ago, in vp -- or, in
+        // the push variant (register-bound), read back from shared
+        if (PUSH || q < 2) {
 #pragma unroll
           for (int h = 0; h < NH; ++h) vp[h] = S0[r * PK + 2 + lk + 32 * h];
         }
@@ -579,12 +609,36 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
           v[h] = a ? nv : c[h];
           if (a && !blk) S2[r * PK + 2 + lk + 32 * h] = v[h];
         }
+        double ov[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) ov[h] = blk ? v[h] : vp[h];
         if (lane_ok) {
 #pragma unroll
-          for (int h = 0; h < NH; ++h) out[32 * h] = blk ? v[h] : vp[h];
+          for (int h = 0; h < NH; ++h) out[32 * h] = ov[h];
         }
+        if (PUSH) {
+          if (push_cls(p, g.n[0], args.push.g) == 1) {
+            if (reinterpret_cast<const int*>(smem_raw + LY::BYTES_PUSH)[warp]) {
+              const int64_t* pd = pdel();
 #pragma unroll
-        for (int h = 0; h < NH; ++h) vp[h] = v[h];
+              for (int h = 0; h < NH; ++h)
+#pragma unroll
+                for (int x = 0; x < kPushMid; ++x) {
+                  const int64_t dx = pd[(3 * h + x) * 32];
+                  if (dx != 0) out[32 * h + dx] = ov[h];
+                }
+            }
+          } else if (lane_ok) {
+            const int4 cc = args.cols[col - 1];  // this segment's column
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              remote |= push_cell_t(&args.push, cc.x, p, cc.y - 2 + r, cc.z + lk + 32 * h, ov[h]);
+          }
+        }
+        if (!PUSH) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) vp[h] = v[h];
+        }
       } else if (do_red) {
         // ring rows / ring columns: red(p+2) only
         double nv[NH];
@@ -614,6 +668,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     }
     fence_proxy_async();
   }
+  if (PUSH && remote) __threadfence_system();  // remote ghost stores before the consumer's barrier
 }
 
 // ---------------------------------------------------------------------------
@@ -774,7 +829,7 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
 template <int TJ, int TK, int D, int MINB>
 bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
              const double* r_base, const Coef& cf, const int fixed_lo[3], const int fixed_hi[3], bool fixed,
-             cudaStream_t st) {
+             cudaStream_t st, const PushDev* push) {
   using LY = Sweep5Layout<TJ, TK, D>;
   for (auto& gg : lv.geo)
     if (gg.n[1] % TJ || gg.n[2] % TK) return false;
@@ -809,19 +864,25 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
     args.fixed_lo[x] = fixed_lo[x];
     args.fixed_hi[x] = fixed_hi[x];
   }
-  auto kern = fixed ? k_gsrb_sweep5<TJ, TK, D, MINB, true> : k_gsrb_sweep5<TJ, TK, D, MINB, false>;
-  static int per_sm[2] = {0, 0};
-  if (!per_sm[fixed]) {
-    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
-    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[fixed], kern, 32 * LY::NW, LY::BYTES));
-    per_sm[fixed] = std::max(per_sm[fixed], 1);
+  if (push) args.push = *push;
+  const int kv = (fixed ? 1 : 0) + (push ? 2 : 0);
+  auto kern = kv == 0   ? k_gsrb_sweep5<TJ, TK, D, MINB, false, false>
+              : kv == 1 ? k_gsrb_sweep5<TJ, TK, D, MINB, true, false>
+              : kv == 2 ? k_gsrb_sweep5<TJ, TK, D, MINB, false, true>
+                        : k_gsrb_sweep5<TJ, TK, D, MINB, true, true>;
+  const int bytes = push ? LY::BYTES_PUSH + 4 * LY::NW : LY::BYTES;
+  static int per_sm[4] = {0, 0, 0, 0};
+  if (!per_sm[kv]) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[kv], kern, 32 * LY::NW, bytes));
+    per_sm[kv] = std::max(per_sm[kv], 1);
   }
-  const long long slots = (long long)per_sm[fixed] * num_sms();
+  const long long slots = (long long)per_sm[kv] * num_sms();
   const long long ncol = (long long)cols.host.size();
   // balanced contiguous (column, plane) ranges; aligning ranges across columns
   // (grid = ncol * (slots / ncol)) cut L2 misses but measured no faster
   const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
-  kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES, st>>>(ma, args);
+  kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st>>>(ma, args);
   check_launch("k_gsrb_sweep5");
   return true;
 }
@@ -830,7 +891,7 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
 
 bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                       const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
-                      const int fixed_hi[3], bool fixed, cudaStream_t st) {
+                      const int fixed_hi[3], bool fixed, cudaStream_t st, const PushDev* push) {
   // Tile: TK = widest of 64/32/16 dividing every box's k-extent.  C3 fine level
   // (64 boxes of 64^3): k_gsrb_sweep5 104.5 us, k_gsrb_sweep4 114.6 us; see
   // DESIGN.md for the variants measured.
@@ -846,7 +907,13 @@ bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Fie
 #define AMRB_TRY4(TJ, TK) \
   if (launch4<TJ, TK, 1, 1, false>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st)) return true;
 #define AMRB_TRY5(TJ, TK) \
-  if (launch5<TJ, TK, 2, 2>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st)) return true;
+  if (launch5<TJ, TK, 2, 2>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st, push)) return true;
+  if (push) {  // only k_gsrb_sweep5 pushes ghosts
+    if (minj < 32) return false;
+    AMRB_TRY5(16, 64)
+    AMRB_TRY5(16, 32)
+    return false;
+  }
   if (minj >= 32) {
     if (impl == 4) {
       if (minj >= 64) {

@@ -37,6 +37,7 @@ from .device import dh_array, field_of, level_of, stream_ptr
 from .geometry import Geometry
 from .interlevel import coarsened_layout, prolong_from
 from .layout import BoxArray, DistributionMapping
+from .push import PushTable, prolong_push
 from .multifab import FabArray, MultiFab, world_size
 
 __all__ = ["MLMG", "mg_hierarchy"]
@@ -130,7 +131,8 @@ class MLMG:
     and history are left in ``self.iterations`` / ``self.history``.
     """
 
-    def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True):
+    def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
+                 ghost_push=False):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
         if not all(geom.periodic):
@@ -190,6 +192,20 @@ class MLMG:
                 dhs[x] = lv.dh
             self._tail_lohi = lohi
             self._tail_dh = dhs
+        # ghost push: sweeps and prolongation fill their output's ghosts in the
+        # kernel (csrc/push.cu); the tracker below decides where a copy-program
+        # fill or (multi-GPU) a device barrier is still needed
+        # Measured on the C3 fine level (scratch/mb_push.py): prolongation with
+        # ghost push 80 us vs 66 us for prolongation + copy-program fill, so it
+        # is off by default; ghost_push=True exercises the path (tests).
+        self.p2p = self.dist and self.transport.p2p
+        for lv in self.levels:
+            lv.push, lv.push_local = False, lv.replicated or not self.dist
+            if ghost_push:
+                self._make_push(lv)
+        self._ghost = {}  # id(field) -> ghost width known to be current
+        self._pending = False  # pushes to peers since the last device barrier
+        self._reads = set()  # fields whose ghosts were read since the last barrier
         top = self.levels[0]
         self.norm = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
         self.graph = None
@@ -202,6 +218,47 @@ class MLMG:
             for i, lv in enumerate(self.levels)
         )
 
+    # -- ghost push / ghost state ------------------------------------------------
+    def _make_push(self, lv):
+        """Push table for the level's phi layout (width 2); lv.push stays False
+        when the layout is not supported."""
+        if self.dist and not lv.push_local and not self.p2p:
+            return  # NCCL copy programs only: peers' storage is not mapped
+        t = PushTable(lv.phi[0], lv.domain, self.periodic, 2, rank=self.transport.rank, local=lv.push_local)
+        if t.ok:
+            lv.push, lv.push_table = True, t
+
+    def _barrier(self):
+        self.transport.peer_barrier()
+        self._pending = False
+        self._reads.clear()
+
+    def _need_ghosts(self, lv, fa, width):
+        """Before a kernel reads fa's ghosts (width cells)."""
+        if self._ghost.get(id(fa), 0) >= width:
+            if self._pending:
+                self._barrier()
+        else:
+            self._fill(lv, fa, width)
+            self._ghost[id(fa)] = width
+            if self.p2p:  # the p2p fill starts with a device barrier
+                self._pending = False
+                self._reads.clear()
+        if self.dist:
+            self._reads.add(id(fa))
+
+    def _produced(self, fa, width, pushed_to_peers=False):
+        """After a kernel rewrote fa's valid cells; width = ghosts it filled."""
+        self._ghost[id(fa)] = width
+        if pushed_to_peers:
+            self._pending = True
+
+    def _before_push(self, lv, fa):
+        """Before a kernel stores into peers' ghosts of fa: no peer may still be
+        reading them."""
+        if not lv.push_local and id(fa) in self._reads:
+            self._barrier()
+
     # -- building blocks ---------------------------------------------------------
     def _fill(self, lv, fa, width):
         # Inside the V-cycle a rank only rewrites cells a peer pulled after the
@@ -212,22 +269,26 @@ class MLMG:
     def _sweep(self, lv):
         a = lv.phi[lv.cur]
         b = lv.phi[1 - lv.cur]
-        self._fill(lv, a, 2)
+        self._need_ghosts(lv, a, 2)
+        self._need_ghosts(lv, lv.rhs, 1)
         lvh = level_of(a)
-        check(
-            lib().amrb_gsrb_sweep(
-                lvh.handle,
-                field_of(a).handle,
-                C.c_void_p(a.storage.data_ptr()),
-                field_of(b).handle,
-                C.c_void_p(b.storage.data_ptr()),
-                field_of(lv.rhs).handle,
-                C.c_void_p(lv.rhs.storage.data_ptr()),
-                lv.dhc,
-                None,
-                stream_ptr(),
-            )
+        args = (
+            lvh.handle,
+            field_of(a).handle,
+            C.c_void_p(a.storage.data_ptr()),
+            field_of(b).handle,
+            C.c_void_p(b.storage.data_ptr()),
+            field_of(lv.rhs).handle,
+            C.c_void_p(lv.rhs.storage.data_ptr()),
+            lv.dhc,
+            None,
         )
+        # The sweep does not push its ghosts: measured, the per-plane delta loads
+        # compete with the kernel's own shared-memory pipe (k_gsrb_sweep5<PUSH>
+        # 163-175 us vs 112 us for fill + sweep on the C3 fine level), so the
+        # next consumer fills.  amrb_gsrb_sweep_push stays available (tests).
+        check(lib().amrb_gsrb_sweep(*args, stream_ptr()))
+        self._produced(b, 0)
         lv.cur = 1 - lv.cur
 
     def _smooth(self, lv, n):
@@ -237,7 +298,7 @@ class MLMG:
     def _resid_restrict(self, l):
         lv, nx = self.levels[l], self.levels[l + 1]
         phi = lv.phi[lv.cur]
-        self._fill(lv, phi, 1)
+        self._need_ghosts(lv, phi, 1)
         dst = nx.rhs if lv.boxlocal_next else lv.tmp
         check(
             lib().amrb_residual_restrict(
@@ -254,7 +315,8 @@ class MLMG:
         )
         if not lv.boxlocal_next:
             self._gather_replica(lv, nx)
-        self._fill(nx, nx.rhs, 1)
+        self._produced(nx.rhs, 0)
+        self._need_ghosts(nx, nx.rhs, 1)
 
     def _gather_replica(self, lv, nx):
         """tmp (coarsened layout of lv, maybe distributed) -> nx.rhs (one box)."""
@@ -279,17 +341,22 @@ class MLMG:
         lv, nx = self.levels[l], self.levels[l + 1]
         fine = lv.phi[lv.cur]
         crse = nx.phi[nx.cur]
-        if lv.boxlocal_next:
-            prolong_from(fine, crse, (2, 2, 2), add=True)
-        else:
+        if not lv.boxlocal_next:
             tr = _LocalView(self.transport) if (self.dist and not lv.replicated) else self.transport
             copy_into(lv.stage, crse, tr)
-            prolong_from(fine, lv.stage, (2, 2, 2), add=True)
+            crse = lv.stage
+        if lv.push:
+            self._before_push(lv, fine)
+            prolong_push(fine, crse, lv.push_table, add=True)
+            self._produced(fine, 2, not lv.push_local)
+        else:
+            prolong_from(fine, crse, (2, 2, 2), add=True)
+            self._produced(fine, 0)
 
     def _residual_norm(self):
         top = self.levels[0]
         phi = top.phi[top.cur]
-        self._fill(top, phi, 1)
+        self._need_ghosts(top, phi, 1)
         check(
             lib().amrb_residual_norm(
                 level_of(phi).handle,
@@ -314,6 +381,7 @@ class MLMG:
         """All tail levels in one kernel: reads rhs, writes phi of levels[tail]."""
         lv = self.levels[self.tail]
         phi = lv.phi[lv.cur]
+        self._produced(phi, 0)
         lohi, lp = i32p(self._tail_lohi)
         dh = np.ascontiguousarray(self._tail_dh)
         check(
@@ -340,6 +408,7 @@ class MLMG:
             lv = L[l]
             if l > 0:
                 _zero(lv.phi[lv.cur])
+                self._produced(lv.phi[lv.cur], 2)  # zero ghosts are the periodic fill of zero
             if l == n - 1:
                 self._smooth(lv, self.bottom_sweeps)
                 break
@@ -382,11 +451,15 @@ class MLMG:
     def set_rhs(self, rhs):
         top = self.levels[0]
         parallel_copy(top.rhs, rhs, self.transport)
-        self._fill(top, top.rhs, 1)
+        self._produced(top.rhs, 0)
+        self._need_ghosts(top, top.rhs, 1)
 
     def set_phi(self, phi):
         top = self.levels[0]
         parallel_copy(top.phi[top.cur], phi, self.transport)
+        # the captured cycle starts from current ghosts (its last sweep pushed them)
+        self._produced(top.phi[top.cur], 0)
+        self._need_ghosts(top, top.phi[top.cur], 2)
 
     def get_phi(self, phi):
         top = self.levels[0]
@@ -400,6 +473,7 @@ class MLMG:
             for lv in self.levels:
                 for f in lv.phi + [lv.rhs]:
                     f.storage.zero_()
+                    self._produced(f, f.ngrow)
             self.graph = self._capture()
         self.set_rhs(rhs)
         self.set_phi(phi)
