@@ -129,6 +129,13 @@ int amrb_prog_destroy(amrb_prog* g);
  * this process (symmetric memory).  Callers frame it with amrb_peer_barrier. */
 int amrb_prog_run_p2p(amrb_prog* g, const double* src_base, double* dst_base,
                       const uint64_t* peer_bases, int npeers, void* stream);
+/* amrb_peer_barrier + amrb_prog_run_p2p in one launch: the copy kernel's CTA
+ * 0 publishes this rank's epoch, CTAs reading peer storage (and CTA 0) wait
+ * for every peer's; local-source CTAs start at once.  epoch = uint32[2]
+ * (epoch, completion ticket), shared with amrb_peer_barrier. */
+int amrb_prog_run_p2p_sync(amrb_prog* g, const double* src_base, double* dst_base,
+                           const uint64_t* peer_bases, int npeers, const uint64_t* pad_ptrs,
+                           int rank, uint32_t* epoch, void* stream);
 /* Device-side barrier across ranks over NVLink signal pads: pad_ptrs[r] =
  * rank r's pad (>= nranks uint32 slots), epoch = this rank's device counter. */
 int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch,

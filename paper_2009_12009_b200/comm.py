@@ -114,7 +114,7 @@ class Transport:
             self._slots_buf = symm_mem.empty(16, dtype=torch.float64, device=dev)
             self._slots = symm_mem.rendezvous(self._slots_buf, dist.group.WORLD.group_name)
             self._slot_ptrs = np.array(self._slots.buffer_ptrs, dtype=np.uint64)
-            self._epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._epoch = torch.zeros(2, dtype=torch.int32, device=dev)  # epoch, CTA ticket
             # pads start at zero; make sure every rank sees that before the first barrier
             self._bar.barrier()
             torch.cuda.synchronize()
@@ -238,15 +238,18 @@ class _Program:
 
     def run(self, src_fa, dst_fa, transport, post_barrier=True):
         if self.p2p:
-            # pull model: peers' boxes are final once everyone reached this point
-            transport.peer_barrier()
+            # pull model: peers' boxes are final once everyone reached this point;
+            # the barrier is fused into the copy launch (k_copy, SyncArgs)
             check(
-                lib().amrb_prog_run_p2p(
+                lib().amrb_prog_run_p2p_sync(
                     self.handle,
                     C.c_void_p(src_fa.storage.data_ptr()),
                     C.c_void_p(dst_fa.storage.data_ptr()),
                     src_fa.peer_ptrs.ctypes.data_as(C.POINTER(C.c_uint64)),
                     transport.nranks,
+                    transport._pads.ctypes.data_as(C.POINTER(C.c_uint64)),
+                    transport.rank,
+                    C.c_void_p(transport._epoch.data_ptr()),
                     stream_ptr(),
                 ),
                 src=transport.rank,

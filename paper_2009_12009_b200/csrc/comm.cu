@@ -51,6 +51,14 @@ struct PeerPtrs {
   const double* p[kMaxPeers];
 };
 
+// Device barrier fused into a p2p copy launch (see k_copy): pads[r] = rank r's
+// signal pad, epoch = {this rank's barrier epoch, CTA completion ticket}.
+struct SyncArgs {
+  uint32_t* pads[kMaxPeers];
+  uint32_t* epoch;
+  int rank, nranks, on;
+};
+
 struct Wave {
   std::vector<DevRec> host;
   std::vector<int2> blocks;  // (record, first flat index inside the record)
@@ -79,12 +87,46 @@ __device__ __forceinline__ void rec_cell(const DevRec& r, int64_t loc, int64_t c
   dofs = r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
 }
 
+// With sy.on (p2p fills) the launch also is the cross-rank barrier that used to
+// precede it: CTA 0 publishes this rank's next epoch in every peer's pad; CTA 0
+// and every CTA that reads a peer's storage wait until all peers published
+// it (their previous kernels -- the producers of the data pulled here -- are
+// complete); CTAs with local sources start at once.  The last CTA to finish
+// advances the epoch.  CTA 0 always waits, so this launch also orders every
+// peer's earlier pulls from this rank before whatever follows it here.
 template <bool kAdd>
 __global__ void __launch_bounds__(kCopyThreads)
     k_copy(const DevRec* __restrict__ recs, const int2* __restrict__ blocks, int ncomp,
            const double* __restrict__ src, const double* __restrict__ buf, double* __restrict__ dst,
-           const __grid_constant__ PeerPtrs peers) {
+           const __grid_constant__ PeerPtrs peers, const __grid_constant__ SyncArgs sy) {
   const int2 bl = blocks[blockIdx.x];
+  uint32_t ep = 0;
+  if (sy.on) {
+    if (threadIdx.x == 0) {
+      ep = *reinterpret_cast<volatile uint32_t*>(sy.epoch) + 1;
+      bool wait = blockIdx.x == 0;
+      if (bl.x >= 0) {
+        wait |= recs[bl.x].src_peer >= 0 && recs[bl.x].src_peer != sy.rank;
+      } else {
+        for (int q = 0; q < bl.y && !wait; ++q) wait |= recs[-bl.x - 1 + q].src_peer != sy.rank;
+      }
+      if (blockIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < sy.nranks; ++p)
+          if (p != sy.rank)
+            asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(sy.pads[p] + sy.rank), "r"(ep) : "memory");
+      }
+      if (wait)
+        for (int p = 0; p < sy.nranks; ++p) {
+          if (p == sy.rank) continue;
+          uint32_t x;
+          do {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(sy.pads[sy.rank] + p) : "memory");
+          } while ((int32_t)(x - ep) < 0);
+        }
+    }
+    __syncthreads();
+  }
   double v[kCopyItems];
   int64_t dofs[kCopyItems];
   if (bl.x >= 0) {  // one large record, chunk starting at flat index bl.y
@@ -144,6 +186,10 @@ __global__ void __launch_bounds__(kCopyThreads)
       dst[dofs[u]] = dst[dofs[u]] + v[u];
     else
       dst[dofs[u]] = v[u];
+  }
+  if (sy.on && threadIdx.x == 0 && atomicAdd(sy.epoch + 1, 1u) == gridDim.x - 1) {
+    sy.epoch[0] = ep;  // every CTA has read the old epoch by now
+    sy.epoch[1] = 0;
   }
 }
 
@@ -215,15 +261,16 @@ void prepare_wave(Wave& w, int ncomp) {
   w.dblocks.upload(w.blocks);
 }
 
-void run_wave(const Wave& w, int ncomp, bool add, const double* src, const double* buf, double* dst,
-              cudaStream_t st, const PeerPtrs& peers = PeerPtrs{}) {
-  if (w.blocks.empty()) return;
+bool run_wave(const Wave& w, int ncomp, bool add, const double* src, const double* buf, double* dst,
+              cudaStream_t st, const PeerPtrs& peers = PeerPtrs{}, const SyncArgs& sy = SyncArgs{}) {
+  if (w.blocks.empty()) return false;
   const unsigned nb = (unsigned)w.blocks.size();
   if (add)
-    k_copy<true><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers);
+    k_copy<true><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
   else
-    k_copy<false><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers);
+    k_copy<false><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
   check_launch("k_copy");
+  return true;
 }
 
 bool overlaps(const Record& a, const Record& b) {
@@ -461,6 +508,39 @@ extern "C" int amrb_prog_destroy(amrb_prog* g) {
   return AMRB_OK;
 }
 
+
+extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch, void* stream);
+
+extern "C" int amrb_prog_run_p2p_sync(amrb_prog* g_, const double* src_base, double* dst_base,
+                                      const uint64_t* peer_bases, int npeers, const uint64_t* pad_ptrs, int rank,
+                                      uint32_t* epoch, void* stream) {
+  int status = amrb::guarded([&] {
+    using namespace amrb;
+    if (!g_ || npeers < 1 || npeers > kMaxPeers || !peer_bases || !pad_ptrs || rank < 0 || rank >= npeers || !epoch)
+      throw Error(AMRB_EINVAL, "amrb_prog_run_p2p_sync: bad arguments");
+    auto* g = reinterpret_cast<Prog*>(g_);
+    PeerPtrs peers{};
+    SyncArgs sy{};
+    for (int r = 0; r < npeers; ++r) {
+      peers.p[r] = reinterpret_cast<const double*>(peer_bases[r]);
+      sy.pads[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
+    }
+    sy.epoch = epoch;
+    sy.rank = rank;
+    sy.nranks = npeers;
+    sy.on = 1;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    bool synced = false;
+    for (auto* w : g->apply) {
+      if (run_wave(*w, g->ncomp, g->op == 1, src_base, nullptr, dst_base, st, peers, synced ? SyncArgs{} : sy))
+        synced = true;
+    }
+    // nothing to copy here: the peers still wait for this rank's epoch
+    if (!synced && amrb_peer_barrier(pad_ptrs, rank, npeers, epoch, stream) != AMRB_OK)
+      throw Error(AMRB_ECUDA, "amrb_prog_run_p2p_sync: barrier launch failed");
+  });
+  return status;
+}
 
 extern "C" int amrb_prog_run_p2p(amrb_prog* g_, const double* src_base, double* dst_base, const uint64_t* peer_bases,
                                  int npeers, void* stream) {
