@@ -36,6 +36,15 @@ from .layout import (
 )
 from .mlmg import MLMG, mg_hierarchy
 from .multifab import ArrayView, Fab, FabArray, MultiFab
+from .plotfile import (
+    OutputMode,
+    PlotfileHeader,
+    WriteHandle,
+    read_checkpoint,
+    read_plotfile,
+    write_checkpoint,
+    write_plotfile,
+)
 from .plans import (
     CommPlan,
     CopyRecord,
@@ -47,6 +56,13 @@ from .plans import (
 )
 
 __all__ = [
+    "OutputMode",
+    "PlotfileHeader",
+    "WriteHandle",
+    "read_checkpoint",
+    "read_plotfile",
+    "write_checkpoint",
+    "write_plotfile",
     "ArrayView",
     "BoundaryRecord",
     "Box",

@@ -184,7 +184,38 @@ def main():
         out0=fa.fab(0).data.copy(),
         out1=fa.fab(1).data.copy(),
     )
+    _plotfile_golden()
     print("amrkit", amrkit.__version__, "->", HERE)
+
+
+def _plotfile_golden():
+    """Directory digests + Header text of amrkit.write_plotfile for the cases
+    in plotfile_cases.py (the device writer must reproduce them byte for byte)."""
+    import json
+    import tempfile
+    import types
+
+    import amrkit
+    from amrkit import distribution, plotfile
+
+    sys.path.insert(0, HERE)
+    import plotfile_cases as PC
+
+    ns = types.SimpleNamespace(
+        Box=amrkit.Box, IntVect=amrkit.IntVect, BoxArray=amrkit.BoxArray, Geometry=amrkit.Geometry,
+        FabArray=amrkit.FabArray, sfc_distribute=distribution.sfc_distribute,
+        default_costs=distribution.default_costs, PlotfileHeader=plotfile.PlotfileHeader)
+    out = {}
+    for case in PC.CASES:
+        header, meshes = PC.build(ns, case)
+        with tempfile.TemporaryDirectory() as tmp:
+            path = os.path.join(tmp, "plt")
+            plotfile.write_plotfile(path, meshes, header).wait()
+            with open(os.path.join(path, "Header")) as fh:
+                text = fh.read()
+            out[case[0]] = {"digest": PC.dir_digest(path), "header": text}
+    with open(os.path.join(HERE, "plotfile.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
 
 
 if __name__ == "__main__":

@@ -131,3 +131,31 @@ def test_matches_reference_layout_layer(amrkit, rng):
         assert A.sfc_distribute(ob, A.default_costs(ob), R).owner == rsfc(rb, rdc(rb), R).owner
         cost = rng.integers(1, 100, size=len(ob)).astype(float)
         assert A.knapsack_distribute(cost, R).owner == rks(cost, R).owner
+
+
+def test_plotfile_header_text_matches_reference_golden():
+    """The device writer's Header (pure host code) equals amrkit's, for the
+    golden cases (tests/golden/plotfile.json, made from the reference)."""
+    import json
+    import os
+    import sys
+    import types
+
+    import paper_2009_12009_b200 as A
+    from paper_2009_12009_b200.plotfile import _header_text
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    import plotfile_cases as PC
+
+    gold = json.load(open(os.path.join(here, "plotfile.json")))
+    for name, dim, n, m, ncomp, nranks, two, time, names in PC.CASES:
+        domain = A.Box(A.IntVect([0] * dim), A.IntVect([n - 1] * dim))
+        g0 = A.Geometry(domain, (0.0,) * dim, (1.0,) * dim, (True,) * dim)
+        levels = [(A.BoxArray([domain]).max_size(m), g0)]
+        if two:
+            fine = A.Box(A.IntVect([n // 2] * dim), A.IntVect([n + n // 2 - 1] * dim))
+            levels.append((A.BoxArray([fine]).max_size(m), g0.refine(A.IntVect([2] * dim))))
+        meshes = [types.SimpleNamespace(ba=ba, ncomp=ncomp) for ba, _ in levels]
+        header = A.PlotfileHeader(time, names, [g for _, g in levels])
+        assert _header_text(header, meshes) == gold[name]["header"]
