@@ -251,6 +251,52 @@ int amrb_prolong_push(const amrb_level* fine_lv, amrb_field* fine, double* fine_
                       const int32_t* ratio, int add, const amrb_push* push,
                       const uint64_t* peer_bases, int npeers, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Inter-level AMR operators + two-level advection.  Work     */
+/* lists: prefix = int64[nb+1] prefix of per-box work items over the        */
+/* resident boxes `boxes` (int32[nb]); total = prefix[nb].  All results are  */
+/* bit-identical to the reference's numpy (see csrc/amr.cu).                */
+/* ------------------------------------------------------------------------ */
+/* Upwind face fluxes (advect.py:24-36) along 3-D axis axis3: face array of
+ * box b at flux + face_off[b], layout (ncomp, n + e_axis) C order; phi needs
+ * one filled ghost layer. */
+int amrb_adv_flux(const amrb_level* lv, const amrb_field* phi_f, const double* phi,
+                  const int64_t* prefix, const int32_t* boxes, int nb, int64_t total,
+                  const int64_t* face_off, double* flux, int ncomp, int axis3, double u,
+                  void* stream);
+/* phi -= dtdx[d] * (F_d[hi] - F_d[lo]) for d = 0..dim-1 (advect.py:39-47);
+ * flux[d] / face_off[d] = device pointers of dimension d's face arrays. */
+int amrb_adv_update(const amrb_level* lv, const amrb_field* phi_f, double* phi,
+                    const int64_t* prefix, const int32_t* boxes, int nb, int64_t total,
+                    const double* const* flux, const int64_t* const* face_off, int ncomp,
+                    int dim, const double dtdx[3], void* stream);
+/* out = a*x + b*y on valid cells (fill_patch time blend, coarse_fine.py:267-273). */
+int amrb_axpby(const amrb_level* lv, const int64_t* prefix, const int32_t* boxes, int nb,
+               int64_t total, const amrb_field* out_f, double* out, double a,
+               const amrb_field* x_f, const double* x, double b, const amrb_field* y_f,
+               const double* y, void* stream);
+/* fine (every cell of each box's grown box) <- interpolation of crse (box b =
+ * coarsen(fine box b) with enough ghosts), pc (linear = 0) or minmod-limited
+ * linear (interp_block, coarse_fine.py:60-99). */
+int amrb_interp(const amrb_level* fine_lv, const amrb_field* fine_f, double* fine,
+                const amrb_level* crse_lv, const amrb_field* crse_f, const double* crse,
+                const int64_t* prefix, const int32_t* boxes, int nb, int64_t total, int ncomp,
+                int dim, const int32_t ratio[3], int linear, void* stream);
+/* *dev_count += NaNs in region (int32[nb][6] box-local lo, hi) of each box. */
+int amrb_nan_count(const amrb_field* f, const double* x, const int64_t* prefix,
+                   const int32_t* boxes, int nb, int64_t total, const int32_t* region,
+                   int ncomp, unsigned long long* dev_count, void* stream);
+/* FluxRegister (coarse_fine.py:317-472).  crse_add: reg[p0] -= scale*F[p1]
+ * per (p0, p1) pair; fine_add: reg[e0] += scale * avg(F[e1..e_nsrc]) in
+ * numpy's reshape-mean order (seq = 1: sequential 4-term sum); reflux:
+ * crse[tgt[t]] += coef[e] * reg[src[e]], e in start[t] .. start[t+1]-1. */
+int amrb_fr_crse(const int64_t* pairs, int64_t n, double* reg, const double* flux,
+                 double scale, void* stream);
+int amrb_fr_fine(const int64_t* idx, int64_t n, int nsrc, int seq, double* reg,
+                 const double* flux, double scale, void* stream);
+int amrb_fr_reflux(const int64_t* tgt, const int64_t* start, int64_t n, const int64_t* src,
+                   const double* coef, double* crse, const double* reg, void* stream);
+
 /* ||rhs - L(phi)||_inf over this device's valid cells, without writing the
  * residual (phi ghosts width 1 filled).  Result (one double) to dev_out. */
 int amrb_residual_norm(const amrb_level* lv, const amrb_field* rhs,

@@ -10,6 +10,7 @@ fallback.
 """
 
 from . import counters
+from .amr import AdvectionSolver, FaceFluxes, FluxRegister, fill_patch, snapshot_valid
 from .boxes import Box, IndexType, IntVect, box_diff
 from .comm import (
     Transport,
@@ -56,6 +57,11 @@ from .plans import (
 )
 
 __all__ = [
+    "AdvectionSolver",
+    "FaceFluxes",
+    "FluxRegister",
+    "fill_patch",
+    "snapshot_valid",
     "OutputMode",
     "PlotfileHeader",
     "WriteHandle",

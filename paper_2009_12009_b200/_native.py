@@ -69,6 +69,14 @@ _SIGS = {
     "amrb_restrict": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
     "amrb_residual_restrict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
     "amrb_prolong": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
+    "amrb_adv_flux": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, i64, vp, vp, C.c_int, C.c_int, f64, vp]),
+    "amrb_adv_update": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, i64, vp, vp, C.c_int, C.c_int, P(f64), vp]),
+    "amrb_axpby": (C.c_int, [vp, vp, vp, C.c_int, i64, vp, vp, f64, vp, vp, f64, vp, vp, vp]),
+    "amrb_interp": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, P(i32), C.c_int, vp]),
+    "amrb_nan_count": (C.c_int, [vp, vp, vp, vp, C.c_int, i64, vp, C.c_int, vp, vp]),
+    "amrb_fr_crse": (C.c_int, [vp, i64, vp, vp, f64, vp]),
+    "amrb_fr_fine": (C.c_int, [vp, i64, C.c_int, C.c_int, vp, vp, f64, vp]),
+    "amrb_fr_reflux": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp]),
     "amrb_push_create": (C.c_int, [vp, C.c_int, P(i32), P(i64), C.c_int, P(i32), C.c_int, C.c_int, C.c_int, P(vp)]),
     "amrb_push_destroy": (C.c_int, [vp]),
     "amrb_gsrb_sweep_push": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, P(C.c_uint64), C.c_int, vp]),

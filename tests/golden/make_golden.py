@@ -185,7 +185,58 @@ def main():
         out1=fa.fab(1).data.copy(),
     )
     _plotfile_golden()
+    _advection_golden()
     print("amrkit", amrkit.__version__, "->", HERE)
+
+
+ADV_CASES = [
+    # name, dim, n, max_grid, blocking, velocity, nranks, cfl, steps
+    ("adv2d", 2, 16, 8, 4, (1.0, 0.5), 2, 0.4, (1, 5, 100)),
+    ("adv3d", 3, 16, 8, 4, (1.0, 0.5, 0.25), 2, 0.4, (1, 4)),
+]
+
+
+def _advection_golden():
+    """Two-level subcycled advection (advect.py:130-188) run by the reference:
+    the hierarchy its regrid built, the initial state and the state after a few
+    coarse steps, with and without refluxing."""
+    from amrkit.advect import AdvectionSolver
+    from amrkit.amr_core import Geometry, GridGenParams
+
+    import amrkit
+
+    for name, dim, n, mg, bf, vel, nranks, cfl, steps in ADV_CASES:
+        out = {}
+        for reflux in (True, False):
+            domain = amrkit.Box(amrkit.IntVect.zero(dim), amrkit.IntVect([n - 1] * dim))
+            geom = Geometry(domain, (0.0,) * dim, (1.0,) * dim, (True,) * dim)
+            params = GridGenParams(dim=dim, max_level=1, max_grid_size=mg, blocking_factor=bf)
+            s = AdvectionSolver(geom, params, velocity=vel, nranks=nranks, cfl=cfl, use_reflux=reflux,
+                                regrid_interval=0)
+            assert s.hier.finest_level == 1
+            tag = "r" if reflux else "n"
+            if reflux:
+                for lev in (0, 1):
+                    out[f"ba{lev}"] = _boxes(s.hier.ba(lev))
+                    out[f"dm{lev}"] = np.array(list(s.hier.dm(lev)), dtype=np.int32)
+                out["ratio"] = np.array(s.params.ref_ratio[0].coords, dtype=np.int32)
+                out["mass0"] = np.array(s.total_mass())
+            done = 0
+            for st in (0,) + tuple(steps):
+                while done < st:
+                    s.step()
+                    done += 1
+                for lev in (0, 1):
+                    fa = s.hier.field("phi", lev)
+                    for i in range(len(fa.ba)):
+                        out[f"{tag}_s{st}_L{lev}_b{i}"] = fa.fab(i).valid().copy()
+                out[f"{tag}_s{st}_mass"] = np.array(s.total_mass())
+                out[f"{tag}_s{st}_time"] = np.array(s.time)
+        out["steps"] = np.array((0,) + tuple(steps))
+        out["meta"] = np.array([dim, n, nranks], dtype=np.int32)
+        out["velocity"] = np.array(vel)
+        out["cfl"] = np.array(cfl)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 
 
 def _plotfile_golden():
