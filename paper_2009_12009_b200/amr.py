@@ -27,7 +27,7 @@ from .boxes import Box, IntVect, box_diff
 from .comm import Transport, copy_into, fill_boundary, parallel_copy
 from .device import field_of, level_of, stream_ptr
 from .geometry import apply_domain_boundary
-from .interlevel import as_ratio, average_down, coarsened_layout
+from .interlevel import _scratch, as_ratio, average_down, coarsened_layout
 from .multifab import FabArray
 from .plans import normalize_periodic
 
@@ -68,10 +68,15 @@ def _work(fa, kind):
     return w
 
 
-def snapshot_valid(fa, transport=None):
+def snapshot_valid(fa, transport=None, reuse=False):
     """Ghost-free copy of fa's valid data on the same layout (coarse_fine.py:223-228):
-    one box-to-same-box copy program (no messages)."""
-    out = FabArray(fa.ba, fa.dm, fa.ncomp, 0, device=fa.device, replicated=fa.replicated)
+    one box-to-same-box copy program (no messages).  reuse=True returns a
+    scratch FabArray cached on fa (overwritten by the next reuse call), so its
+    copy program is built once."""
+    if reuse:
+        out = _scratch(fa, fa.ba, 0, "snapshot")
+    else:
+        out = FabArray(fa.ba, fa.dm, fa.ncomp, 0, device=fa.device, replicated=fa.replicated)
     parallel_copy(out, fa, transport if transport is not None else Transport(fa.dm.nranks))
     return out
 
@@ -144,32 +149,35 @@ def _axpby(out, a, x, b, y):
 
 
 def fill_patch(dst, fine_src, crse_old, crse_new, time_weight, ratio, transport, domain=None, periodic=None,
-               kind="linear", boundary=None, geom=None):
+               kind="linear", boundary=None, geom=None, check_coverage=True):
     """Fill dst (valid + ghost cells) from fine data where available, else from
     time-blended coarse data interpolated to the fine level
     (coarse_fine.py:231-309): blend (1-w)*old + w*new, copy the blend onto the
     coarsened layout with ghosts (NaN elsewhere), interpolate every grown cell
     on the device, then let fine copies win, apply physical BCs, and reject
-    in-domain cells neither level covers."""
+    in-domain cells neither level covers (check_coverage=False skips that
+    host-synchronising test, e.g. on a fixed hierarchy after its first fill)."""
     if not 0.0 <= time_weight <= 1.0:
         raise ValueError("time_weight must lie in [0, 1]")
     if kind not in ("linear", "pc"):
         raise ValueError(f"unknown interpolation kind {kind!r}")
     dim = dst.dim
     ratio = as_ratio(ratio, dim)
+    # scratch FabArrays are cached on dst / crse_new (their copy programs are
+    # built once); each is fully rewritten before use
     if fine_src is dst:
-        fine_src = snapshot_valid(dst, transport)
+        fine_src = snapshot_valid(dst, transport, reuse=True)
     if time_weight == 0.0:
         blended = crse_old
     elif time_weight == 1.0 or crse_old is None:
         blended = crse_new
     else:
-        blended = FabArray(crse_new.ba, crse_new.dm, crse_new.ncomp, 0, device=crse_new.device)
+        blended = _scratch(crse_new, crse_new.ba, 0, "blend")
         _axpby(blended, 1.0 - time_weight, crse_old, time_weight, crse_new)
     margin = 1 if kind == "linear" else 0
     gc = -(-dst.ngrow // max(min(tuple(ratio)), 1)) + max(margin, 1)
     cdomain = domain.coarsen(ratio) if domain is not None else None
-    stage = FabArray(coarsened_layout(dst.ba, ratio), dst.dm, dst.ncomp, gc, device=dst.device)
+    stage = _scratch(dst, coarsened_layout(dst.ba, ratio), gc, "fp_stage")
     stage.storage.fill_(float("nan"))
     copy_into(stage, blended, transport, include_dst_ghosts=True, domain=cdomain, periodic=periodic)
     prefix, boxes, nb, total = _work(dst, "grown")
@@ -184,7 +192,7 @@ def fill_patch(dst, fine_src, crse_old, crse_new, time_weight, ratio, transport,
         copy_into(dst, fine_src, transport, include_dst_ghosts=True, domain=domain, periodic=periodic)
     if boundary is not None:
         apply_domain_boundary(dst, geom, boundary)
-    if domain is not None:
+    if domain is not None and check_coverage:
         _check_covered(dst, domain, periodic)
 
 
@@ -393,11 +401,14 @@ class FluxRegister:
         tgt, start, src, sign, dims = plan
         if not len(tgt):
             return
-        coef = np.array([sign[e] * float(dt_over_dx[dims[e]]) for e in range(len(sign))], dtype=np.float64)
-        coef_t = torch.as_tensor(coef, device=self.device)
+        ckey = key + ("coef",) + tuple(float(x) for x in dt_over_dx)
+        coef_t = self._cache.get(ckey)
+        if coef_t is None:  # (sign * dt/dx[d]) per contribution, like the reference's scalar
+            coef = np.array([sign[e] * float(dt_over_dx[dims[e]]) for e in range(len(sign))], dtype=np.float64)
+            coef_t = torch.as_tensor(coef, device=self.device)
+            self._cache[ckey] = coef_t
         check(lib().amrb_fr_reflux(_vp(tgt), _vp(start), len(tgt), _vp(src), _vp(coef_t), _vp(crse.storage),
                                    _vp(self.data), stream_ptr()))
-        self._keep = coef_t
 
     def _reflux_plan(self, crse, domain, per):
         ext = domain.extents()
@@ -476,7 +487,8 @@ class AdvectionSolver:
     use_reflux=True)``; fields ``phi[0]``, ``phi[1]`` (ncomp 1, ngrow 1);
     ``step()`` returns dt like the reference."""
 
-    def __init__(self, geom0, ba0, dm0, ba1, dm1, ratio, velocity, cfl=0.45, use_reflux=True, transport=None):
+    def __init__(self, geom0, ba0, dm0, ba1, dm1, ratio, velocity, cfl=0.45, use_reflux=True, transport=None,
+                 use_graph=True):
         self.geoms = [geom0, geom0.refine(as_ratio(ratio, geom0.dim))]
         self.ratio = as_ratio(ratio, geom0.dim)
         self.velocity = tuple(float(v) for v in velocity)
@@ -489,6 +501,9 @@ class AdvectionSolver:
         self._ff = FaceFluxes(self.phi[1])
         self.time = 0.0
         self.step_count = 0
+        self.use_graph = use_graph
+        self._graph = None
+        self._dt = None
 
     @property
     def dim(self):
@@ -500,11 +515,34 @@ class AdvectionSolver:
         return self.cfl / speed if speed > 0 else 1.0
 
     def step(self):
-        dim = self.dim
+        """One coarse step.  The first two run eagerly (the first also checks
+        that both levels cover every fine ghost cell); later steps replay a
+        CUDA graph of the identical launch sequence (dt, the hierarchy and
+        every buffer are fixed)."""
         dt = self.dt_coarse()
+        if self._graph is not None:
+            self._graph.replay()
+        elif self.use_graph and self.step_count >= 2:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._advance(dt, check=False)
+            torch.cuda.current_stream().wait_stream(s)
+            self._graph = g
+            g.replay()  # capture records the launches without running them
+        else:
+            self._advance(dt, check=self.step_count == 0)
+        self.time += dt
+        self.step_count += 1
+        return dt
+
+    def _advance(self, dt, check):
+        dim = self.dim
         gc, gf = self.geoms
         phi_c, phi_f = self.phi
-        crse_old = snapshot_valid(phi_c, self.transport)
+        crse_old = snapshot_valid(phi_c, self.transport, reuse=True)
         dto_dx_c = [dt / gc.cell_size[d] for d in range(dim)]
         fill_boundary(phi_c, self.transport, gc.domain, gc.periodic)
         upwind_fluxes(phi_c, self.velocity, self._cf)
@@ -516,16 +554,14 @@ class AdvectionSolver:
         dto_dx_f = [dt_f / gf.cell_size[d] for d in range(dim)]
         for m in range(nsub):
             fill_patch(phi_f, phi_f, crse_old, phi_c, time_weight=m / nsub, ratio=self.ratio,
-                       transport=self.transport, domain=gf.domain, periodic=gf.periodic, kind="linear")
+                       transport=self.transport, domain=gf.domain, periodic=gf.periodic, kind="linear",
+                       check_coverage=check)
             upwind_fluxes(phi_f, self.velocity, self._ff)
             apply_fluxes(phi_f, self._ff, dto_dx_f)
             self.fluxreg.fine_add_all(self._ff, scale=1.0 / nsub)
         average_down(phi_f, phi_c, self.ratio, self.transport)
         if self.use_reflux:
             self.fluxreg.reflux(phi_c, dto_dx_c, gc.domain, gc.periodic)
-        self.time += dt
-        self.step_count += 1
-        return dt
 
     def total_mass(self):
         """Volume-weighted composite sum (advect.py:202-225), evaluated like the
