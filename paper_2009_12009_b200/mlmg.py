@@ -50,7 +50,7 @@ def _coarsenable(e):
 _TAIL_MAX_EXTENT = 16  # agglomerate once the coarsened domain fits in one CTA
 
 
-def mg_hierarchy(domain, ba, nranks=1, agg_cells=64**3):
+def mg_hierarchy(domain, ba, nranks=1, agg_cells=128**3):
     """[(domain, BoxArray, kind)] fine -> coarse.
 
     Same level RESOLUTIONS as oracle.mlmg_ref.mg_levels (box-local coarsening,
@@ -132,7 +132,7 @@ class MLMG:
     """
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
-                 ghost_push=False):
+                 ghost_push=False, agg_cells=128**3):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
         if not all(geom.periodic):
@@ -149,7 +149,8 @@ class MLMG:
         self.levels = []
         self.user_ba, self.user_dm = ba, dm
         ba, dm = rebox_per_rank(ba, dm)
-        for dom, lba, kind in mg_hierarchy(geom.domain, ba, nranks=dm.nranks if self.dist else 1):
+        for dom, lba, kind in mg_hierarchy(geom.domain, ba, nranks=dm.nranks if self.dist else 1,
+                                           agg_cells=agg_cells):
             lv = _Level()
             lv.domain, lv.ba, lv.kind = dom, lba, kind
             lv.replicated = kind in ("agglom", "single")
