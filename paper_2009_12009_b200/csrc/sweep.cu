@@ -914,6 +914,10 @@ bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Fie
     AMRB_TRY5(16, 32)
     return false;
   }
+  static const int tk_force = getenv("AMRB_SWEEP_TK") ? atoi(getenv("AMRB_SWEEP_TK")) : 0;
+  if (tk_force == 32 && minj >= 32 && impl != 4) {
+    AMRB_TRY5(16, 32)
+  }
   if (minj >= 32) {
     if (impl == 4) {
       if (minj >= 64) {

@@ -3,7 +3,9 @@ sys.path.insert(0, '/root/repo')
 import paper_2009_12009_b200 as A
 from paper_2009_12009_b200 import stencil as S
 res = {}
-for n, m in ((256, 64), (256, 256), (128, 32), (512, 32)):
+import os
+cfgs = [tuple(int(x) for x in c.split('/')) for c in os.environ.get('MB_CFGS', '256/64,256/256,128/32,512/32').split(',')]
+for n, m in cfgs:
     dom = A.Box((0,0,0),(n-1,)*3); ba = A.BoxArray([dom]).max_size(m)
     dm = A.DistributionMapping.single_rank(len(ba)); tr = A.Transport(1)
     a = A.MultiFab(ba, dm, 1, 2); b = A.MultiFab(ba, dm, 1, 2); r = A.MultiFab(ba, dm, 1, 1)
