@@ -57,6 +57,10 @@ int amrb_version(void);
 int64_t amrb_launch_count(void);
 /* Zero n doubles (cudaMemsetAsync on `stream`; a memset node in a graph). */
 int amrb_zero(double* ptr, int64_t n, void* stream);
+/* host_dst[0..n) <- src (device) by a kernel storing through UVA into pinned
+ * host memory: small results reach the host without a copy-engine transfer
+ * (which would queue behind bulk copies).  Synchronize the stream to read. */
+int amrb_store_host(const double* src, double* host_dst, int64_t n, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Communication plans (host).  Records are CopyRecord(src, dst, src_box,    */

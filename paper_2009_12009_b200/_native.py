@@ -37,6 +37,7 @@ _SIGS = {
     "amrb_version": (C.c_int, []),
     "amrb_launch_count": (i64, []),
     "amrb_zero": (C.c_int, [vp, i64, vp]),
+    "amrb_store_host": (C.c_int, [vp, vp, i64, vp]),
     "amrb_plan_fill_create": (C.c_int, [C.c_int, C.c_int, P(i32), C.c_int, P(i32), P(C.c_uint8), P(vp)]),
     "amrb_plan_copy_create": (
         C.c_int,

@@ -881,6 +881,27 @@ extern "C" const char* amrb_last_error(void) { return amrb::g_last_error.c_str()
 extern "C" int amrb_version(void) { return 1; }
 extern "C" int64_t amrb_launch_count(void) { return (int64_t)amrb::g_launches.load(); }
 
+namespace amrb {
+namespace {
+__global__ void k_store_host(const double* __restrict__ src, double* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  __threadfence_system();
+}
+}  // namespace
+}  // namespace amrb
+
+// Small device -> pinned-host transfers by a kernel (UVA stores), so they do
+// not queue behind bulk copies on the copy engines.
+extern "C" int amrb_store_host(const double* src, double* host_dst, int64_t n, void* stream) {
+  return amrb::guarded([&] {
+    if (n < 0 || (n && (!src || !host_dst))) throw amrb::Error(AMRB_EINVAL, "amrb_store_host: bad arguments");
+    if (!n) return;
+    amrb::k_store_host<<<1, 32, 0, (cudaStream_t)stream>>>(src, host_dst, n);
+    amrb::check_launch("k_store_host");
+  });
+}
+
 extern "C" int amrb_zero(double* ptr, int64_t n, void* stream) {
   return amrb::guarded([&] {
     if (n < 0 || (n && !ptr)) throw amrb::Error(AMRB_EINVAL, "amrb_zero: bad arguments");

@@ -209,6 +209,10 @@ class MLMG:
         self._reads = set()  # fields whose ghosts were read since the last barrier
         top = self.levels[0]
         self.norm = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
+        # the per-cycle norm reaches the host through a kernel store into pinned
+        # memory (amrb_store_host): no copy-engine transfer to queue behind the
+        # caller's bulk copies on other streams
+        self.norm_host = torch.zeros(1, dtype=torch.float64).pin_memory()
         self.graph = None
         self.graph_replays = 0
         self.launches_per_cycle = 0
@@ -424,6 +428,15 @@ class MLMG:
     def _cycle_and_norm(self):
         self.vcycle()
         self._residual_norm()
+        check(lib().amrb_store_host(C.c_void_p(self.norm.data_ptr()), C.c_void_p(self.norm_host.data_ptr()), 1,
+                                    stream_ptr()))
+
+    def _host_scalar(self, t):
+        """t (1-element device tensor) -> float via the pinned mailbox."""
+        check(lib().amrb_store_host(C.c_void_p(t.data_ptr()), C.c_void_p(self.norm_host.data_ptr()), 1,
+                                    stream_ptr()))
+        torch.cuda.current_stream().synchronize()
+        return float(self.norm_host[0])
 
     # -- graph capture -------------------------------------------------------------
     def _capture(self):
@@ -480,7 +493,7 @@ class MLMG:
         self.set_phi(phi)
         r0t = device_reduce(top.rhs, "absmax", 0)
         self._allmax(r0t)
-        r0 = float(r0t.item())
+        r0 = self._host_scalar(r0t)
         self.history = []
         self.iterations = 0
         rn = r0
@@ -493,7 +506,8 @@ class MLMG:
             else:
                 self._cycle_and_norm()
             self.iterations += 1
-            rn = float(self.norm.item())
+            torch.cuda.current_stream().synchronize()
+            rn = float(self.norm_host[0])
             self.history.append(rn)
             if rn <= rtol * r0:
                 break

@@ -273,6 +273,47 @@ class FabArray:
         return np.asarray(self.dm.owner, dtype=np.int32)
 
     # -- host <-> device helpers ----------------------------------------------
+    # -- bulk host <-> device (one contiguous copy + one launch each way) -------
+    def image_size(self):
+        """Elements of the host image: every RESIDENT box's valid region,
+        comp-major C order, boxes back to back in index order (the plotfile
+        data.bin record layout restricted to this rank's boxes)."""
+        return self.ncomp * sum(self.ba[i].num_cells() for i in range(len(self.ba)) if self.resident[i])
+
+    def from_host_image(self, image, stream=None):
+        """Valid cells of resident boxes <- a host image (pinned float64 tensor of
+        image_size() elements, see image_size): one async host->device copy
+        into a cached device staging buffer and one scatter launch, both on
+        `stream` (default: current).  The caller keeps `image` alive until the
+        copy has run."""
+        from .plotfile import _packer
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        stage = self._native.get("img_in")
+        if stage is None:
+            stage = torch.empty(max(self.image_size(), 1), dtype=torch.float64, device=self.device)
+            self._native["img_in"] = stage
+        with torch.cuda.stream(st):
+            stage[: image.numel()].copy_(image, non_blocking=True)
+            _packer(self, False, compact=True).run(stage.data_ptr(), self.storage.data_ptr())
+        return self
+
+    def to_host_image(self, image, stream=None):
+        """host image (pinned float64, image_size() elements) <- valid cells of
+        resident boxes: one gather launch + one async device->host copy on
+        `stream`; synchronize before reading `image`."""
+        from .plotfile import _packer
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        stage = self._native.get("img_out")
+        if stage is None:
+            stage = torch.empty(max(self.image_size(), 1), dtype=torch.float64, device=self.device)
+            self._native["img_out"] = stage
+        with torch.cuda.stream(st):
+            _packer(self, True, compact=True).run(self.storage.data_ptr(), stage.data_ptr())
+            image.copy_(stage[: image.numel()], non_blocking=True)
+        return image
+
     def load_valid_from(self, domain, global_arr):
         """Load every resident fab's valid region from one dense array over domain."""
         g = np.asarray(global_arr)

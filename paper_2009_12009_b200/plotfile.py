@@ -220,10 +220,18 @@ def _staging_fabtab(ba, offsets, resident):
 
 class _Packer:
     """Copy program between a FabArray and its data.bin staging image (either
-    direction), cached on the FabArray."""
+    direction), cached on the FabArray.  compact=True: records of this rank's
+    resident boxes only, back to back (FabArray host images)."""
 
-    def __init__(self, fa, to_staging):
+    def __init__(self, fa, to_staging, compact=False):
         self.offsets, self.sizes, self.total = _record_layout(fa.ba, fa.ncomp)
+        if compact:
+            at = 0
+            for i in range(len(fa.ba)):
+                n = self.sizes[i] if fa.resident[i] else 0
+                self.offsets[i], self.sizes[i] = at, n
+                at += n
+            self.total = at
         owners = fa.owners()
         nranks = fa.dm.nranks if world_size() > 1 else 1
         rank = fa.rank if world_size() > 1 else 0
@@ -256,11 +264,11 @@ class _Packer:
                 pass
 
 
-def _packer(fa, to_staging):
-    key = "plot_pack" if to_staging else "plot_unpack"
+def _packer(fa, to_staging, compact=False):
+    key = ("plot_pack" if to_staging else "plot_unpack", compact)
     p = fa._native.get(key)
     if p is None:
-        p = _Packer(fa, to_staging)
+        p = _Packer(fa, to_staging, compact)
         fa._native[key] = p
     return p
 

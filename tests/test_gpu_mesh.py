@@ -283,3 +283,26 @@ def test_average_down_and_interp_match_oracle_3d(rng):
     got = oracle_fabs_from_device(fine)
     for i in ff:
         assert np.array_equal(got[i], ff[i])
+
+
+def test_host_image_round_trip():
+    """FabArray.to_host_image / from_host_image: comp-major per-box records of
+    the resident boxes, one copy + one launch each way."""
+    dom = A.Box((0, 0, 0), (47, 31, 15))
+    ba = A.BoxArray([dom]).max_size(16)
+    dm = A.DistributionMapping.single_rank(len(ba))
+    src = A.MultiFab(ba, dm, 2, 1)
+    src.storage.normal_()
+    img = torch.empty(src.image_size(), dtype=torch.float64).pin_memory()
+    src.to_host_image(img)
+    torch.cuda.synchronize()
+    off = 0
+    for i in range(len(ba)):
+        want = src.fab(i).valid().cpu().numpy().ravel()
+        assert np.array_equal(img[off : off + want.size].numpy(), want)
+        off += want.size
+    dst = A.MultiFab(ba, dm, 2, 2)
+    dst.from_host_image(img)
+    torch.cuda.synchronize()
+    for i in range(len(ba)):
+        assert torch.equal(dst.fab(i).valid(), src.fab(i).valid())
