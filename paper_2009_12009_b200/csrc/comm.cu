@@ -102,28 +102,29 @@ __global__ void __launch_bounds__(kCopyThreads)
   const int2 bl = blocks[blockIdx.x];
   uint32_t ep = 0;
   if (sy.on) {
-    if (threadIdx.x == 0) {
-      ep = *reinterpret_cast<volatile uint32_t*>(sy.epoch) + 1;
+    // warp 0: lane p publishes to / polls peer p concurrently (one NVLink
+    // round trip whatever the peer count)
+    ep = *reinterpret_cast<volatile uint32_t*>(sy.epoch) + 1;
+    if (threadIdx.x < 32) {
+      const int p = threadIdx.x;
       bool wait = blockIdx.x == 0;
       if (bl.x >= 0) {
         wait |= recs[bl.x].src_peer >= 0 && recs[bl.x].src_peer != sy.rank;
       } else {
         for (int q = 0; q < bl.y && !wait; ++q) wait |= recs[-bl.x - 1 + q].src_peer != sy.rank;
       }
-      if (blockIdx.x == 0) {
-        __threadfence_system();
-        for (int p = 0; p < sy.nranks; ++p)
-          if (p != sy.rank)
-            asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(sy.pads[p] + sy.rank), "r"(ep) : "memory");
-      }
-      if (wait)
-        for (int p = 0; p < sy.nranks; ++p) {
-          if (p == sy.rank) continue;
+      if (p < sy.nranks && p != sy.rank) {
+        if (blockIdx.x == 0) {
+          __threadfence_system();
+          asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(sy.pads[p] + sy.rank), "r"(ep) : "memory");
+        }
+        if (wait) {
           uint32_t x;
           do {
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(sy.pads[sy.rank] + p) : "memory");
           } while ((int32_t)(x - ep) < 0);
         }
+      }
     }
     __syncthreads();
   }
@@ -565,21 +566,20 @@ struct PadPtrs {
 // in mine.  The epoch lives in device memory, so a captured graph replays
 // correctly; the wrap-safe compare allows 2^31 outstanding epochs.
 __global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nranks, uint32_t* epoch) {
-  if (threadIdx.x != 0) return;
-  const uint32_t e = *epoch + 1;
-  *epoch = e;
-  __threadfence_system();
-  for (int p = 0; p < nranks; ++p) {
-    if (p == rank) continue;
+  // one warp; lane p publishes to and polls peer p concurrently
+  const int p = threadIdx.x;
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch) + 1;
+  __syncwarp();
+  if (p < nranks && p != rank) {
+    __threadfence_system();
     asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
-  }
-  for (int p = 0; p < nranks; ++p) {
-    if (p == rank) continue;
     uint32_t v;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(my_pad + p) : "memory");
     } while ((int32_t)(v - e) < 0);
   }
+  __syncwarp();
+  if (p == 0) *epoch = e;
 }
 }  // namespace
 
@@ -603,26 +603,26 @@ namespace {
 // the max over the local slots.  One launch, graph-replay safe (device epoch).
 __global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, const uint64_t* __restrict__ bufs_unused, int rank,
                               int nranks, uint32_t* epoch, double* val, double* my_slots, PeerPtrs peer_slots) {
-  if (threadIdx.x != 0) return;
+  // one warp; lane p serves peer p (value store, publish, poll) concurrently
+  const int p = threadIdx.x;
   const double v = *val;
-  for (int p = 0; p < nranks; ++p) {
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch) + 1;
+  __syncwarp();
+  if (p < nranks) {
     double* dst = const_cast<double*>(peer_slots.p[p]) + rank;
     *dst = v;
+    if (p != rank) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
+      uint32_t w;
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(w) : "l"(my_pad + p) : "memory");
+      } while ((int32_t)(w - e) < 0);
+    }
   }
-  const uint32_t e = *epoch + 1;
+  __syncwarp();
+  if (p != 0) return;
   *epoch = e;
-  __threadfence_system();
-  for (int p = 0; p < nranks; ++p) {
-    if (p == rank) continue;
-    asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
-  }
-  for (int p = 0; p < nranks; ++p) {
-    if (p == rank) continue;
-    uint32_t w;
-    do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(w) : "l"(my_pad + p) : "memory");
-    } while ((int32_t)(w - e) < 0);
-  }
   double m = my_slots[0];
   for (int p = 1; p < nranks; ++p) {
     double x;
