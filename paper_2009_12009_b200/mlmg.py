@@ -196,7 +196,7 @@ class MLMG:
         # ghost push: sweeps and prolongation fill their output's ghosts in the
         # kernel (csrc/push.cu); the tracker below decides where a copy-program
         # fill or (multi-GPU) a device barrier is still needed
-        # Measured on the C3 fine level (scratch/mb_push.py): prolongation with
+        # Measured on the C3 fine level (tools/mb_push.py): prolongation with
         # ghost push 80 us vs 66 us for prolongation + copy-program fill, so it
         # is off by default; ghost_push=True exercises the path (tests).
         self.p2p = self.dist and self.transport.p2p

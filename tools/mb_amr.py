@@ -1,5 +1,5 @@
 """Device two-level advection step on the reference's own hierarchy
-(scratch/ref_amr_<n>.json): ms per coarse step, cell updates/s."""
+(tools/ref_amr_<n>.json): ms per coarse step, cell updates/s."""
 import json, sys, time, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_2009_12009_b200 as A

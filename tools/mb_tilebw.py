@@ -1,5 +1,6 @@
+# build first: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -lcuda tools/tilebw.cu -o tools/libtilebw.so
 import ctypes as C
-L = C.CDLL('/root/repo/scratch/libtilebw.so')
+L = C.CDLL('/root/repo/tools/libtilebw.so')
 us = C.c_float()
 for rows in (20, 36):
     for mode, name in ((0, "ldg->sts"), (1, "cp.async16"), (2, "tma2d")):

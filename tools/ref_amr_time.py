@@ -1,5 +1,5 @@
 """Reference AdvectionSolver timing (CPU, this container) + hierarchy dump for
-the device benchmark (scratch/mb_amr.py)."""
+the device benchmark (tools/mb_amr.py)."""
 import json, sys, time
 sys.path.insert(0, "/root/reference/pkg/src")
 import numpy as np
