@@ -918,6 +918,7 @@ bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Fie
   if (tk_force == 32 && minj >= 32 && impl != 4) {
     AMRB_TRY5(16, 32)
   }
+
   // Large levels (every box a multiple of 128 in k, >= ~200 plane-steps per
   // CTA slot): 8 x 128 tiles, four cells per lane, amortize the per-step
   // overhead (512^3 in 128^3 boxes: 773.6 -> 708.5 us).  On the C3 fine level
