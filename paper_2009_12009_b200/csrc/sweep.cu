@@ -503,25 +503,44 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       return (1 + ((par0 + q + ccol + 1) & 1) + 2 * cidx) * PK + ccol;
     };
 
-    // rhs of the cells step p relaxes, straight to registers
-    auto load_rhs = [&](int p, double (&rv)[NH]) {
-      const int q = p - i0;
-      if (role == ROLE_ROW) {
-        const bool blk = ((par0 + q + r + lane) & 1) != 0;
-        const int t = blk ? p : p + 2;
-        const bool need = (TK >= 32 || lane < TK) && p < i1 && (blk || p + 2 <= i1);
+    // rhs of the cells step p relaxes, straight to registers.  load_rhs runs for
+    // p = i0, i0+1, ... in order: a running plane pointer plus, per cell, two
+    // element offsets selected by a parity bit that flips every call (row
+    // lanes: black(p) / red(p+2); ring lanes: the red cell of plane p+2)
+    const double* rptr;
+    int co0[NH], co1[NH];  // ring lanes: smem offset of the red cell in plane p+2, by parity of p - i0
+    int rsel;
+    if (role == ROLE_ROW) {
+      rptr = rbase + (int64_t)i0 * rs0 + (int64_t)r * rs1 + 2 + lk;
+      rsel = ((par0 + r + lane) & 1) != 0 ? 0 : 1;  // 0: black(p)
 #pragma unroll
-        for (int h = 0; h < NH; ++h)
-          rv[h] = need ? __ldg(rbase + (int64_t)t * rs0 + (int64_t)r * rs1 + 2 + lk + 32 * h) : 0.0;
+      for (int h = 0; h < NH; ++h) co0[h] = co1[h] = 0;
+    } else {
+      rptr = rbase + (int64_t)(i0 + 2) * rs0;
+      rsel = 0;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        co0[h] = cell_off(2, h);
+        co1[h] = cell_off(3, h);
+      }
+    }
+    auto load_rhs = [&](int p, double (&rv)[NH]) {
+      if (role == ROLE_ROW) {
+        const bool need = (TK >= 32 || lane < TK) && (rsel == 0 ? p < i1 : p + 2 <= i1);
+        const double* rp = rptr + (rsel ? 2 * rs0 : 0);
+#pragma unroll
+        for (int h = 0; h < NH; ++h) rv[h] = need ? __ldg(rp + 32 * h) : 0.0;
       } else {
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           const bool need = p + 2 <= i1 && (role == ROLE_RROW ? rok[h] : (h == 0 && cok));
-          const int o = cell_off(q + 2, h);
-          const int rw = o / PK, c = o - rw * PK;
-          rv[h] = need ? __ldg(rbase + (int64_t)(p + 2) * rs0 + (int64_t)rw * rs1 + c) : 0.0;
+          const int o = rsel ? co1[h] : co0[h];
+          const int rw = o / PK;
+          rv[h] = need ? __ldg(rptr + ((int64_t)rw * rs1 + (o - rw * PK))) : 0.0;
         }
       }
+      rptr += rs0;
+      rsel ^= 1;
     };
 
     // rhs one step ahead; a lane's colour is the same in steps p and p+2, so a
@@ -529,7 +548,9 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     // vpB by step parity; the first two come from the prologue, in shared)
     double rv[NH], vpA[NH], vpB[NH];
     load_rhs(i0, rv);
-    int m1 = 1;                         // slot of plane p-1
+    // slots of planes p-1 .. p+3 (rotated each step); nidx = slot of plane p+4
+    double *sm_ = slot(1), *s0_ = slot(2), *s1_ = slot(3), *s2_ = slot(4), *s3_ = slot(5);
+    int nidx = 6 % NPHI;
     int widx = 5 % NPHI;                // slot of plane p+3 (awaited)
     unsigned wph = (5 / NPHI) & 1;
     int iidx = 0;                       // slot of plane p+3+D (issued)
@@ -567,12 +588,17 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       __syncthreads();
       if (tid == producer && p + 3 + D <= i1 + 1) issue(p + 3 + D, iidx);
       iidx = wrap(iidx + 1);
-      const double* Sm = slot(m1);
-      const double* S0 = slot(wrap(m1 + 1));
-      const double* S1 = slot(wrap(m1 + 2));
-      double* S2 = slot(wrap(m1 + 3));
-      const double* S3 = slot(wrap(m1 + 4));
-      m1 = wrap(m1 + 1);
+      const double* Sm = sm_;
+      const double* S0 = s0_;
+      const double* S1 = s1_;
+      double* S2 = s2_;
+      const double* S3 = s3_;
+      sm_ = s0_;
+      s0_ = s1_;
+      s1_ = s2_;
+      s2_ = s3_;
+      s3_ = slot(nidx);
+      nidx = wrap(nidx + 1);
       if (role == ROLE_ROW) {
         const bool blk = ((par0 + q + r + lane) & 1) != 0;
         const double* P = blk ? S0 : S2;
@@ -645,7 +671,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
         int o[NH];
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          o[h] = cell_off(q + 2, h);
+          o[h] = (q & 1) ? co1[h] : co0[h];
           nv[h] = relax_at(S2, S1, S3, rv[h], o[h]);
         }
 #pragma unroll
