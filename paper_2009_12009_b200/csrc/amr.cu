@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(kThreads)
     k_adv_flux(const int64_t* __restrict__ prefix, const int* __restrict__ boxes, int nb, const BoxGeom* __restrict__ geo,
                const FabView* __restrict__ pv, const double* __restrict__ phi, const int64_t* __restrict__ foff,
                double* __restrict__ flux, int ncomp, int ax, double u) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= prefix[nb]) return;
   const int q = find_box(prefix, nb, g);
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(kThreads)
     k_adv_update(const int64_t* __restrict__ prefix, const int* __restrict__ boxes, int nb,
                  const BoxGeom* __restrict__ geo, const FabView* __restrict__ pv, double* __restrict__ phi,
                  const __grid_constant__ Faces F, int ncomp, int dim, double dt0, double dt1, double dt2) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= prefix[nb]) return;
   const int q = find_box(prefix, nb, g);
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(kThreads)
     k_axpby(const int64_t* __restrict__ prefix, const int* __restrict__ boxes, int nb, const BoxGeom* __restrict__ geo,
             const FabView* __restrict__ ov, double* __restrict__ out, double a, const FabView* __restrict__ xv,
             const double* __restrict__ x, double bcoef, const FabView* __restrict__ yv, const double* __restrict__ y) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= prefix[nb]) return;
   const int q = find_box(prefix, nb, g);
@@ -150,6 +153,7 @@ __global__ void __launch_bounds__(kThreads)
              int3 fng, const FabView* __restrict__ fv, double* __restrict__ fine, const BoxGeom* __restrict__ cgeo,
              const FabView* __restrict__ cv, const double* __restrict__ crse, int ncomp, int dim, int r0, int r1,
              int r2, int linear) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= prefix[nb]) return;
   const int q = find_box(prefix, nb, g);
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(kThreads)
     k_nan_count(const int64_t* __restrict__ prefix, const int* __restrict__ boxes, int nb,
                 const int* __restrict__ region, const FabView* __restrict__ fv, const double* __restrict__ x, int ncomp,
                 unsigned long long* __restrict__ count) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= prefix[nb]) return;
   const int q = find_box(prefix, nb, g);
@@ -220,6 +225,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     k_fr_crse(const int64_t* __restrict__ pairs, int64_t n, double* __restrict__ reg, const double* __restrict__ F,
               double scale) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= n) return;
   const int64_t d = pairs[2 * g], s = pairs[2 * g + 1];
@@ -233,6 +239,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     k_fr_fine(const int64_t* __restrict__ idx, int64_t n, int nsrc, int seq, double* __restrict__ reg,
               const double* __restrict__ F, double scale) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= n) return;
   const int64_t* e = idx + g * (1 + nsrc);
@@ -254,6 +261,7 @@ __global__ void __launch_bounds__(kThreads)
     k_fr_reflux(const int64_t* __restrict__ tgt, const int64_t* __restrict__ start, int64_t n,
                 const int64_t* __restrict__ src, const double* __restrict__ coef, double* __restrict__ crse,
                 const double* __restrict__ reg) {
+  pdl_entry();
   const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (g >= n) return;
   double v = crse[tgt[g]];
@@ -289,7 +297,7 @@ extern "C" int amrb_adv_flux(const amrb_level* lv, const amrb_field* phi_f, cons
                              int ncomp, int axis3, double u, void* stream) {
   return amrb::guarded([&] {
     if (nb < 1 || total < 1) return;
-    amrb::k_adv_flux<<<amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream>>>(
+    amrb::launch_k(amrb::k_adv_flux, amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream,
         prefix, boxes, nb, LV(lv).dgeo.p, FD(phi_f).dev.p, phi, face_off, flux, ncomp, axis3, u);
     amrb::check_launch("k_adv_flux");
   });
@@ -306,7 +314,7 @@ extern "C" int amrb_adv_update(const amrb_level* lv, const amrb_field* phi_f, do
       F.f[d] = flux[d];
       F.off[d] = face_off[d];
     }
-    amrb::k_adv_update<<<amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream>>>(
+    amrb::launch_k(amrb::k_adv_update, amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream,
         prefix, boxes, nb, LV(lv).dgeo.p, FD(phi_f).dev.p, phi, F, ncomp, dim, dtdx[0], dtdx[1], dtdx[2]);
     amrb::check_launch("k_adv_update");
   });
@@ -317,7 +325,7 @@ extern "C" int amrb_axpby(const amrb_level* lv, const int64_t* prefix, const int
                           double b, const amrb_field* y_f, const double* y, void* stream) {
   return amrb::guarded([&] {
     if (nb < 1 || total < 1) return;
-    amrb::k_axpby<<<amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream>>>(
+    amrb::launch_k(amrb::k_axpby, amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream,
         prefix, boxes, nb, LV(lv).dgeo.p, FD(out_f).dev.p, out, a, FD(x_f).dev.p, x, b, FD(y_f).dev.p, y);
     amrb::check_launch("k_axpby");
   });
@@ -330,7 +338,7 @@ extern "C" int amrb_interp(const amrb_level* fine_lv, const amrb_field* fine_f, 
   return amrb::guarded([&] {
     if (nb < 1 || total < 1) return;
     const Field& ff = FD(fine_f);
-    amrb::k_interp<<<amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream>>>(
+    amrb::launch_k(amrb::k_interp, amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream,
         prefix, boxes, nb, LV(fine_lv).dgeo.p, make_int3(ff.ng3[0], ff.ng3[1], ff.ng3[2]), ff.dev.p, fine,
         LV(crse_lv).dgeo.p, FD(crse_f).dev.p, crse, ncomp, dim, ratio[0], ratio[1], ratio[2], linear);
     amrb::check_launch("k_interp");
@@ -342,7 +350,7 @@ extern "C" int amrb_nan_count(const amrb_field* f, const double* x, const int64_
                               void* stream) {
   return amrb::guarded([&] {
     if (nb < 1 || total < 1) return;
-    amrb::k_nan_count<<<amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream>>>(
+    amrb::launch_k(amrb::k_nan_count, amrb::grid_of(total), amrb::kThreads, 0, (cudaStream_t)stream,
         prefix, boxes, nb, region, FD(f).dev.p, x, ncomp, dev_count);
     amrb::check_launch("k_nan_count");
   });
@@ -352,7 +360,7 @@ extern "C" int amrb_fr_crse(const int64_t* pairs, int64_t n, double* reg, const 
                             void* stream) {
   return amrb::guarded([&] {
     if (n < 1) return;
-    amrb::k_fr_crse<<<amrb::grid_of(n), amrb::kThreads, 0, (cudaStream_t)stream>>>(pairs, n, reg, flux, scale);
+    amrb::launch_k(amrb::k_fr_crse, amrb::grid_of(n), amrb::kThreads, 0, (cudaStream_t)stream, pairs, n, reg, flux, scale);
     amrb::check_launch("k_fr_crse");
   });
 }
@@ -362,7 +370,7 @@ extern "C" int amrb_fr_fine(const int64_t* idx, int64_t n, int nsrc, int seq, do
   return amrb::guarded([&] {
     if (n < 1) return;
     if (nsrc != 1 && nsrc != 2 && nsrc != 4) throw amrb::Error(AMRB_EINVAL, "amrb_fr_fine: nsrc must be 1, 2 or 4");
-    amrb::k_fr_fine<<<amrb::grid_of(n), amrb::kThreads, 0, (cudaStream_t)stream>>>(idx, n, nsrc, seq, reg, flux,
+    amrb::launch_k(amrb::k_fr_fine, amrb::grid_of(n), amrb::kThreads, 0, (cudaStream_t)stream, idx, n, nsrc, seq, reg, flux,
                                                                                    scale);
     amrb::check_launch("k_fr_fine");
   });
@@ -372,7 +380,7 @@ extern "C" int amrb_fr_reflux(const int64_t* tgt, const int64_t* start, int64_t 
                               const double* coef, double* crse, const double* reg, void* stream) {
   return amrb::guarded([&] {
     if (n < 1) return;
-    amrb::k_fr_reflux<<<amrb::grid_of(n), amrb::kThreads, 0, (cudaStream_t)stream>>>(tgt, start, n, src, coef, crse,
+    amrb::launch_k(amrb::k_fr_reflux, amrb::grid_of(n), amrb::kThreads, 0, (cudaStream_t)stream, tgt, start, n, src, coef, crse,
                                                                                      reg);
     amrb::check_launch("k_fr_reflux");
   });

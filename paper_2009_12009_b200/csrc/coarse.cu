@@ -48,6 +48,7 @@ __device__ __forceinline__ double avg8t(const double* v) {
 }
 
 __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
+  pdl_entry();
   extern __shared__ __align__(16) double sm[];
   // Levels >= a.warp_from are tiny (<= 512 cells): warp 0 runs their whole
   // sub-cycle with __syncwarp while the other warps wait at one barrier.
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
 // ---------------------------------------------------------------------------
 template <int LOG0>
 __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) {
+  pdl_entry();
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   // level l: n = 1 << (LOG0 - l); phi and rhs dense n^3 at smem offsets
@@ -439,7 +441,7 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
       auto kern = n0 == 16 ? k_coarse_tail_p2<4> : n0 == 8 ? k_coarse_tail_p2<3> : n0 == 4 ? k_coarse_tail_p2<2>
                                                                                             : k_coarse_tail_p2<1>;
       AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2));
-      kern<<<1, kTailThreads, b2, (cudaStream_t)stream>>>(a);
+      launch_k(kern, 1, kTailThreads, b2, (cudaStream_t)stream, a);
       check_launch("k_coarse_tail_p2");
       return;
     }
@@ -449,7 +451,7 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
       configured = true;
     }
     a.warp_from = nlev;  // block mode throughout (measured faster than one warp)
-    k_coarse_tail<<<1, kTailThreads, bytes, (cudaStream_t)stream>>>(a);
+    launch_k(k_coarse_tail, 1, kTailThreads, bytes, (cudaStream_t)stream, a);
     check_launch("k_coarse_tail");
   });
 }

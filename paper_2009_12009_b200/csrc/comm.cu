@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     k_copy(const DevRec* __restrict__ recs, const int2* __restrict__ blocks, int ncomp,
            const double* __restrict__ src, const double* __restrict__ buf, double* __restrict__ dst,
            const __grid_constant__ PeerPtrs peers, const __grid_constant__ SyncArgs sy) {
+  amrb::pdl_entry();
   const int2 bl = blocks[blockIdx.x];
   uint32_t ep = 0;
   if (sy.on) {
@@ -267,9 +268,9 @@ bool run_wave(const Wave& w, int ncomp, bool add, const double* src, const doubl
   if (w.blocks.empty()) return false;
   const unsigned nb = (unsigned)w.blocks.size();
   if (add)
-    k_copy<true><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
+    launch_k(k_copy<true>, nb, kCopyThreads, 0, st, w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
   else
-    k_copy<false><<<nb, kCopyThreads, 0, st>>>(w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
+    launch_k(k_copy<false>, nb, kCopyThreads, 0, st, w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
   check_launch("k_copy");
   return true;
 }
@@ -566,6 +567,7 @@ struct PadPtrs {
 // in mine.  The epoch lives in device memory, so a captured graph replays
 // correctly; the wrap-safe compare allows 2^31 outstanding epochs.
 __global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nranks, uint32_t* epoch) {
+  amrb::pdl_entry();
   // one warp; lane p publishes to and polls peer p concurrently
   const int p = threadIdx.x;
   const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch) + 1;
@@ -590,7 +592,7 @@ extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks,
       throw Error(AMRB_EINVAL, "amrb_peer_barrier: bad arguments");
     PadPtrs pads{};
     for (int r = 0; r < nranks; ++r) pads.p[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
-    k_peer_barrier<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pads.p[rank], pads, rank, nranks, epoch);
+    launch_k(k_peer_barrier, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream), pads.p[rank], pads, rank, nranks, epoch);
     check_launch("k_peer_barrier");
   });
 }
@@ -603,6 +605,7 @@ namespace {
 // the max over the local slots.  One launch, graph-replay safe (device epoch).
 __global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, const uint64_t* __restrict__ bufs_unused, int rank,
                               int nranks, uint32_t* epoch, double* val, double* my_slots, PeerPtrs peer_slots) {
+  amrb::pdl_entry();
   // one warp; lane p serves peer p (value store, publish, poll) concurrently
   const int p = threadIdx.x;
   const double v = *val;
@@ -646,7 +649,7 @@ extern "C" int amrb_peer_allmax(const uint64_t* pad_ptrs, const uint64_t* slot_p
       pads.p[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
       slots.p[r] = reinterpret_cast<const double*>(slot_ptrs[r]);
     }
-    k_peer_allmax<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+    launch_k(k_peer_allmax, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream),
         pads.p[rank], pads, nullptr, rank, nranks, epoch, val, const_cast<double*>(slots.p[rank]), slots);
     check_launch("k_peer_allmax");
   });

@@ -30,6 +30,44 @@ inline void check_launch(const char* what) {
   if (e != cudaSuccess) throw Error(AMRB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Programmatic dependent launch.  Every library kernel begins with pdl_entry():
+// griddepcontrol.wait returns once the preceding grid in the stream has
+// completed and its writes are visible (a no-op for a normally launched grid),
+// then launch_dependents lets the next grid be scheduled onto the SMs this one
+// leaves free -- only after ALL of this grid's CTAs have started, so a waiting
+// dependent never takes a slot from it.  The wait comes before any early
+// return, so completion stays transitive along the stream.  launch_k() adds
+// the programmatic-serialization attribute to EAGER launches only (AMRB_PDL=2,
+// the default): measured on the C3 bench, eager PDL takes 0.14 ms off the
+// end-to-end step (10.49 -> 10.35 ms), while programmatic edges inside the
+// captured V-cycle graph cost 0.1 ms per solve (9.05 -> 9.16 ms).
+// AMRB_PDL=0: off, 1: everywhere.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+int pdl_mode();
+template <class... KArgs, class... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  const int mode = pdl_mode();
+  bool on = mode == 1;
+  if (mode == 2) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    on = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+  }
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // Valid box of one grid, 3-D padded, global index space.
 struct BoxGeom {
   int lo[3];

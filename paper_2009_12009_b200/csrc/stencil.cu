@@ -29,6 +29,10 @@ namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int pdl_mode() {
+  static const int mode = getenv("AMRB_PDL") ? atoi(getenv("AMRB_PDL")) : 2;
+  return mode;
+}
 
 const TileTable& Level::tiles(int ti, int tj, int tk) {
   auto key = std::make_tuple(ti, tj, tk);
@@ -110,6 +114,7 @@ __global__ void __launch_bounds__(256)
     k_stencil(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fo,
               double* __restrict__ out, const FabView* __restrict__ fr, const double* __restrict__ rhs,
               const FabView* __restrict__ fp, const double* __restrict__ phi, Coef cf) {
+  pdl_entry();
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = geo[t.x];
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
@@ -148,6 +153,7 @@ __global__ void __launch_bounds__(256)
     k_gsrb_color(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fp,
                  double* __restrict__ phi, const FabView* __restrict__ fr, const double* __restrict__ rhs,
                  Coef cf, int color) {
+  pdl_entry();
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = geo[t.x];
   const int j = t.z + threadIdx.y;
@@ -230,6 +236,7 @@ __device__ __forceinline__ void load_rhs_plane(SweepSmem<TJ, TK>& sm, int slot, 
 
 template <int TJ, int TK>
 __global__ void __launch_bounds__(256, 2) k_gsrb_sweep(SweepArgs args) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<TJ, TK>*>(smem_raw);
   const int4 t = args.tiles[blockIdx.x];
@@ -369,6 +376,7 @@ struct Sweep3Args {
 
 template <int TJ, int TK, bool FIXED>
 __global__ void __launch_bounds__(256, 2) k_gsrb_sweep3(Sweep3Args args) {
+  pdl_entry();
   using SM = Sweep3Smem<TJ, TK>;
   constexpr int NT = 256;
   constexpr int PK = TK + 4;        // cells per smem row (k0-2 .. k0+TK+1)
@@ -549,6 +557,7 @@ __global__ void __launch_bounds__(256)
     k_restrict(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ cgeo, const FabView* __restrict__ fc,
                double* __restrict__ crse, const FabView* __restrict__ ff, const double* __restrict__ fine,
                int ncomp, int3 rr, int mode, double inv) {
+  pdl_entry();
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = cgeo[t.x];
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
@@ -587,6 +596,7 @@ __global__ void __launch_bounds__(256)
                      const FabView* __restrict__ fc, double* __restrict__ crse, const FabView* __restrict__ fr,
                      const double* __restrict__ rhs, const FabView* __restrict__ fp,
                      const double* __restrict__ phi, Coef cf) {
+  pdl_entry();
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = cgeo[t.x];
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
@@ -617,6 +627,7 @@ __global__ void __launch_bounds__(256)
     k_prolong(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ fgeo, const FabView* __restrict__ ff,
               double* __restrict__ fine, const FabView* __restrict__ fc, const double* __restrict__ crse,
               int ncomp, int add, int3 sh) {
+  pdl_entry();
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = fgeo[t.x];
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
@@ -652,6 +663,7 @@ __global__ void __launch_bounds__(256)
     k_prolong_push(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ fgeo,
                    const FabView* __restrict__ ff, double* __restrict__ fine, const FabView* __restrict__ fc,
                    const double* __restrict__ crse, int add, int3 sh, const __grid_constant__ PushDev push) {
+  pdl_entry();
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = fgeo[t.x];
   const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
@@ -736,6 +748,7 @@ __device__ double block_combine(int kind, double v, double* scratch) {
 __global__ void __launch_bounds__(256)
     k_reduce_tiles(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fx,
                    const double* __restrict__ x, int comp, int kind, double* __restrict__ partial) {
+  pdl_entry();
   __shared__ double scratch[32];
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = geo[t.x];
@@ -761,6 +774,7 @@ __global__ void __launch_bounds__(256)
     k_resid_norm(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ geo, const FabView* __restrict__ fr,
                  const double* __restrict__ rhs, const FabView* __restrict__ fp, const double* __restrict__ phi,
                  Coef cf, double* __restrict__ partial) {
+  pdl_entry();
   __shared__ double scratch[32];
   const int4 t = tiles[blockIdx.x];
   const BoxGeom g = geo[t.x];
@@ -789,6 +803,7 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(1024) k_reduce_final(const double* __restrict__ partial, int n, int kind,
                                                        double* __restrict__ out) {
+  pdl_entry();
   __shared__ double scratch[32];
   const int rkind = kind == 3 ? 2 : kind;
   double acc = identity(rkind);
@@ -805,6 +820,7 @@ __global__ void __launch_bounds__(1024) k_reduce_final(const double* __restrict_
 __global__ void k_domain_bc(const BoxGeom* __restrict__ geo, const FabView* __restrict__ fv, double* __restrict__ x,
                             int nboxes, int3 ng, int ncomp, int axis, int side, int dlo, int dhi, int cond,
                             double value) {
+  pdl_entry();
   const int b = blockIdx.y;
   if (b >= nboxes) return;
   const BoxGeom g = geo[b];
@@ -884,6 +900,7 @@ extern "C" int64_t amrb_launch_count(void) { return (int64_t)amrb::g_launches.lo
 namespace amrb {
 namespace {
 __global__ void k_store_host(const double* __restrict__ src, double* dst, int64_t n) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
   __threadfence_system();
@@ -897,7 +914,7 @@ extern "C" int amrb_store_host(const double* src, double* host_dst, int64_t n, v
   return amrb::guarded([&] {
     if (n < 0 || (n && (!src || !host_dst))) throw amrb::Error(AMRB_EINVAL, "amrb_store_host: bad arguments");
     if (!n) return;
-    amrb::k_store_host<<<1, 32, 0, (cudaStream_t)stream>>>(src, host_dst, n);
+    amrb::launch_k(amrb::k_store_host, 1, 32, 0, (cudaStream_t)stream, src, host_dst, n);
     amrb::check_launch("k_store_host");
   });
 }
@@ -972,7 +989,7 @@ namespace {
 template <class K, class... Args>
 void launch_tiles(const TileTable& tt, K kernel, cudaStream_t st, dim3 block, Args... args) {
   if (tt.host.empty()) return;
-  kernel<<<(unsigned)tt.host.size(), block, 0, st>>>(tt.dev.p, tt.ti, args...);
+  launch_k(kernel, (unsigned)tt.host.size(), block, 0, st, tt.dev.p, tt.ti, args...);
 }
 
 // Tile depth along i: 8 planes per CTA (register reuse along i) on levels big
@@ -1062,7 +1079,7 @@ void launch_sweep(Level& lv, const Field& a, const double* a_base, const Field& 
     AMRB_CUDA(cudaFuncSetAttribute(k_gsrb_sweep<TJ, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  k_gsrb_sweep<TJ, TK><<<(unsigned)tt.host.size(), dim3(32, 8), smem, st>>>(args);
+  launch_k(k_gsrb_sweep<TJ, TK>, (unsigned)tt.host.size(), dim3(32, 8), smem, st, args);
   check_launch("k_gsrb_sweep");
 }
 template <int TJ, int TK>
@@ -1098,7 +1115,7 @@ void launch_sweep_full(Level& lv, const Field& a, const double* a_base, const Fi
   // enough CTAs to fill the chip, but >= 16 planes (or a whole column) each
   long long want = std::max<long long>((long long)cols.host.size(), cols.total / 16);
   long long grid = std::min<long long>((long long)per_sm[fixed] * num_sms(), want);
-  kern<<<(unsigned)std::max<long long>(grid, 1), 256, smem, st>>>(args);
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 256, smem, st, args);
   check_launch("k_gsrb_sweep3");
 }
 }  // namespace
@@ -1276,7 +1293,7 @@ extern "C" int amrb_residual_norm(const amrb_level* lv_, const amrb_field* rhs, 
                    make_coef(dh), lv.partials.p);
       check_launch("k_resid_norm");
     }
-    k_reduce_final<<<1, 1024, 0, st>>>(lv.partials.p, n, 3, dev_out);
+    launch_k(k_reduce_final, 1, 1024, 0, st, lv.partials.p, n, 3, dev_out);
     check_launch("k_reduce_final");
   });
 }
@@ -1295,7 +1312,7 @@ extern "C" int amrb_reduce(const amrb_level* lv_, const amrb_field* x, const dou
       launch_tiles(tt, k_reduce_tiles, st, dim3(32, 8), lv.dgeo.p, F(x).dev.p, x_base, comp, kind, lv.partials.p);
       check_launch("k_reduce_tiles");
     }
-    k_reduce_final<<<1, 1024, 0, st>>>(lv.partials.p, n, kind, dev_out);
+    launch_k(k_reduce_final, 1, 1024, 0, st, lv.partials.p, n, kind, dev_out);
     check_launch("k_reduce");
   });
 }
@@ -1313,7 +1330,7 @@ extern "C" int amrb_domain_bc(const amrb_level* lv_, amrb_field* f, double* base
         const int cond = bc[2 * axis + side];
         if (cond == 0) continue;
         dim3 grid(64, lv.nboxes);
-        k_domain_bc<<<grid, 256, 0, (cudaStream_t)stream>>>(lv.dgeo.p, fld.dev.p, base, lv.nboxes,
+        launch_k(k_domain_bc, grid, 256, 0, (cudaStream_t)stream, lv.dgeo.p, fld.dev.p, base, lv.nboxes,
                                                            make_int3(fld.ng3[0], fld.ng3[1], fld.ng3[2]), ncomp,
                                                            axis, side, domain[axis], domain[3 + axis], cond, value);
         check_launch("k_domain_bc");

@@ -123,6 +123,7 @@ struct Sweep4Layout {
 template <int TJ, int TK, int D, int MINB, bool FIXED, bool BULK>
 __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     k_gsrb_sweep4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR, Sweep4Args args) {
+  pdl_entry();
   using LY = Sweep4Layout<TJ, TK, D, BULK>;
   constexpr int PK = LY::PP;
   constexpr int CO = LY::CO;
@@ -361,6 +362,7 @@ struct Sweep5Layout {
 template <int TJ, int TK, int D, int MINB, bool FIXED, bool PUSH>
 __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ Sweep4Args args) {
+  pdl_entry();
   using LY = Sweep5Layout<TJ, TK, D>;
   constexpr int PK = LY::PK, NPHI = LY::NPHI, NH = LY::NH, NW = LY::NW;
   static_assert(TJ % 2 == 0 && TJ + 2 <= 32, "ring-column warp holds one cell per lane");
@@ -847,7 +849,7 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
   // levels: one CTA slot each.  Small levels: segments of >= 2 planes so the
   // level still spreads over the chip (their data lives in L2 anyway).
   grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
-  kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES, st>>>(ma, mr, args);
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES, st, ma, mr, args);
   check_launch("k_gsrb_sweep4");
   return true;
 }
@@ -908,7 +910,7 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
   // balanced contiguous (column, plane) ranges; aligning ranges across columns
   // (grid = ncol * (slots / ncol)) cut L2 misses but measured no faster
   const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
-  kern<<<(unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st>>>(ma, args);
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st, ma, args);
   check_launch("k_gsrb_sweep5");
   return true;
 }
