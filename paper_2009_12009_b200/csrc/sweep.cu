@@ -909,7 +909,8 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
   const long long ncol = (long long)cols.host.size();
   // balanced contiguous (column, plane) ranges; aligning ranges across columns
   // (grid = ncol * (slots / ncol)) cut L2 misses but measured no faster
-  const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
+  static const int min_steps = getenv("AMRB_SWEEP_MINSTEPS") ? atoi(getenv("AMRB_SWEEP_MINSTEPS")) : 2;
+  const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / min_steps));
   launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st, ma, args);
   check_launch("k_gsrb_sweep5");
   return true;
@@ -965,7 +966,12 @@ bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Fie
       if (launch5<8, 128, 2, 2>(lv, a, a_base, b, b_base, r, r_base, cf, fixed_lo, fixed_hi, fixed, st, push))
         return true;
   }
-  if (minj >= 32) {
+  // AMRB_SWEEP5_MINCELLS: levels with fewer cells take the k_gsrb_sweep4 tiles (A/B runs)
+  static const long long min5 = getenv("AMRB_SWEEP5_MINCELLS") ? atoll(getenv("AMRB_SWEEP5_MINCELLS")) : 0;
+  long long lcells = 0;
+  for (int bx = 0; bx < lv.nboxes; ++bx)
+    if (lv.resident[bx]) lcells += (long long)lv.geo[bx].n[0] * lv.geo[bx].n[1] * lv.geo[bx].n[2];
+  if (minj >= 32 && lcells >= min5) {
     if (impl == 4) {
       if (minj >= 64) {
         AMRB_TRY4(16, 64)
