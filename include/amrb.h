@@ -198,6 +198,20 @@ int amrb_gsrb_sweep(const amrb_level* lv, const amrb_field* a, const double* a_b
                     const double* rhs_base, const double dh[3],
                     const int32_t* fixed_lohi, void* stream);
 
+/* Prolongation fused into the first post-smoothing sweep of the V-cycle up-leg:
+ * b = GSRB(a + P(c)), P = piecewise-constant interpolation of the coarse
+ * correction c (interp_to_fine(..., "pc"), coarse_fine.py:166-185, then
+ * phi_f += tmp).  c lives on the box-local coarsening (ratio 2) of a's level;
+ * ghosts of a filled to 2, of rhs and c to 1; periodic (no fixed cells).
+ * Bit-identical to amrb_prolong(add) + fill_boundary(a, 2) + amrb_gsrb_sweep;
+ * `a` itself is left unchanged.  AMRB_ENOTSUP when the level does not take the
+ * k_gsrb_sweep5 path (nothing launched). */
+int amrb_gsrb_sweep_prolong(const amrb_level* lv, const amrb_field* a, const double* a_base,
+                            amrb_field* b, double* b_base, const amrb_field* rhs,
+                            const double* rhs_base, const double dh[3],
+                            const amrb_level* clv, const amrb_field* c, const double* c_base,
+                            void* stream);
+
 /* Ghost push: FillBoundary (fabarray.py:364-374) fused into the kernel that
  * produces a field.  A push table holds the fill plan's records whose source
  * box this rank owns (rec11 = amrb_plan_records rows; fabtab = the GLOBAL fab

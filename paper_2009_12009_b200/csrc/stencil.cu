@@ -1201,6 +1201,33 @@ extern "C" int amrb_gsrb_sweep_push(const amrb_level* lv_, const amrb_field* a, 
   });
 }
 
+extern "C" int amrb_gsrb_sweep_prolong(const amrb_level* lv_, const amrb_field* a, const double* a_base,
+                                          amrb_field* b, double* b_base, const amrb_field* rhs, const double* rhs_base,
+                                          const double dh[3], const amrb_level* clv_, const amrb_field* c,
+                                          const double* c_base, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    const Level& clv = L(clv_);
+    need_ghost(F(a), 2, "gsrb_sweep_prolong (phi in)");
+    need_ghost(F(rhs), 1, "gsrb_sweep_prolong (rhs)");
+    need_ghost(F(c), 1, "gsrb_sweep_prolong (coarse)");
+    for (auto* f : {a, (const amrb_field*)b, rhs}) need_same_level(F(f), lv, "gsrb_sweep_prolong");
+    need_same_level(F(c), clv, "gsrb_sweep_prolong (coarse)");
+    if (!lv.all_even()) throw Error(AMRB_EINVAL, "gsrb_sweep_prolong needs even box extents");
+    // coarse box b must be the box-local coarsening (ratio 2) of fine box b
+    if (clv.nboxes != lv.nboxes) throw Error(AMRB_EINVAL, "gsrb_sweep_prolong: box counts differ");
+    for (int x = 0; x < lv.nboxes; ++x) {
+      if (clv.resident[x] != lv.resident[x]) throw Error(AMRB_EINVAL, "gsrb_sweep_prolong: residency differs");
+      for (int d = 0; d < 3; ++d)
+        if (lv.geo[x].lo[d] % 2 || clv.geo[x].lo[d] * 2 != lv.geo[x].lo[d] || clv.geo[x].n[d] * 2 != lv.geo[x].n[d])
+          throw Error(AMRB_EINVAL, "gsrb_sweep_prolong: coarse box is not the coarsened fine box");
+    }
+    if (!launch_sweep_prolong_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), clv, F(c), c_base,
+                                  (cudaStream_t)stream))
+      throw Error(AMRB_ENOTSUP, "gsrb_sweep_prolong: level does not take the k_gsrb_sweep5 path");
+  });
+}
+
 namespace {
 int3 ratio3(const int32_t* ratio) {
   int3 r = make_int3(2, 2, 2);

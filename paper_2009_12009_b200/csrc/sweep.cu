@@ -55,6 +55,7 @@ struct Sweep4Args {
   int r_kc, r_jc, r_ic;  // rhs: rows from j0-1, cols from k0-2
   int fixed_lo[3], fixed_hi[3];
   PushDev push;  // k_gsrb_sweep5<..., PUSH>: fill b's ghosts as planes are written
+  int c_kc, c_jc, c_ic;  // k_gsrb_sweep5<..., PROL>: coarse tensor-map offsets (tile from (j0/2-1, k0/2-1))
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -357,15 +358,28 @@ struct Sweep5Layout {
   // interior-plane ghost destinations
   static constexpr int PDEL_OFF = BYTES;
   static constexpr int BYTES_PUSH = PDEL_OFF + NW * 3 * NH * 32 * 8;  // + NW flag words
+  // PROL: ring of NC coarse plane tiles, rows (j0-2)/2 .. (j0+TJ+1)/2, cols
+  // (k0-2)/2 - kshift .. : a TMA box must start on a 16-byte boundary in its
+  // inner dimension, so the tile starts at the even tensor column at or below
+  // (k0-2)/2 (kshift = 0 or 1) and is TK/2 + 4 wide
+  // NC = 5: a segment prologue issues fine planes i0-2 .. i0+5, i.e. up to five
+  // coarse planes (odd i0); in steady state <= 2 are needed at once
+  static constexpr int CJ = TJ / 2 + 2, CK = TK / 2 + 4, NC = 5;
+  static constexpr int CBYTES = CJ * CK * 8;
+  static constexpr int CSTRIDE = (CBYTES + 127) / 128 * 128;
+  static constexpr int C_OFF = (BYTES + 127) / 128 * 128;
+  static constexpr int BYTES_PROL = C_OFF + NC * CSTRIDE;
 };
 
-template <int TJ, int TK, int D, int MINB, bool FIXED, bool PUSH>
+template <int TJ, int TK, int D, int MINB, bool FIXED, bool PUSH, bool PROL = false>
 __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
-    k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ Sweep4Args args) {
+    k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+                  const __grid_constant__ Sweep4Args args) {
   pdl_entry();
   using LY = Sweep5Layout<TJ, TK, D>;
   constexpr int PK = LY::PK, NPHI = LY::NPHI, NH = LY::NH, NW = LY::NW;
   static_assert(TJ % 2 == 0 && TJ + 2 <= 32, "ring-column warp holds one cell per lane");
+  static_assert(!PROL || (!FIXED && !PUSH && D >= 3), "PROL: periodic levels, corrects plane p+4 in step p");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + LY::BAR_OFF);
   const int tid = threadIdx.x;
@@ -376,6 +390,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
   const Coef cf = args.cf;
   auto slot = [&](int idx) { return reinterpret_cast<double*>(smem_raw + idx * LY::PSTRIDE); };
   auto wrap = [](int x) { return x >= NPHI ? x - NPHI : x; };
+  auto cslot = [&](int idx) { return reinterpret_cast<double*>(smem_raw + LY::C_OFF + idx * LY::CSTRIDE); };
 
   const long long G = gridDim.x;
   long long s = args.total * blockIdx.x / G;
@@ -409,6 +424,9 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     const int jk0 = g.lo[1] + j0 + g.lo[2] + k0;
     // smem cell (row, c) of plane ip is red iff ((g.lo[0] + ip + jk0 + row + c) & 1) == 0
     const int par0 = (g.lo[0] + i0 + jk0) & 1;  // parity base of plane i0
+    const int cbase = (i0 - 2) >> 1;            // PROL: coarse plane of ring slot 0
+    const int ckx = (k0 >> 1) + args.c_kc;      // PROL: tensor column of coarse cell (k0-2)/2
+    const int cshift = ckx & 1;                 //       the tile starts cshift columns before it
 
     __syncthreads();
     if (tid == producer) {
@@ -422,9 +440,36 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     __syncthreads();
 
     // plane ip lives in slot (ip - i0 + 2) % NPHI
+    // PROL: the first fine plane of each coarse plane also brings that coarse
+    // tile, on the same mbarrier (coarse plane ip>>1 lives in coarse slot
+    // ((ip>>1) - cbase) % NC; the coarse plane of slot x is rewritten only by
+    // the TMA issued with fine plane 2((ip>>1) + NC), six steps after its last reader)
     auto issue = [&](int ip, int idx) {
-      mbar_expect_tx(&bars[idx], LY::PBYTES);
+      const bool cl = PROL && (ip == i0 - 2 || (ip & 1) == 0);
+      mbar_expect_tx(&bars[idx], LY::PBYTES + (cl ? LY::CBYTES : 0));
       tma_load4(slot(idx), &tmA, &bars[idx], k0 + args.a_kc, j0 + args.a_jc, ip + args.a_ic, bslot);
+      if (cl)
+        tma_load4(cslot(((ip >> 1) - cbase) % LY::NC), &tmC, &bars[idx], ckx - cshift, (j0 >> 1) + args.c_jc,
+                  (ip >> 1) + args.c_ic, bslot);
+    };
+    // PROL: plane tile P (plane ip) += coarse parent, rows 0..TJ+3, cols 0..TK+3 --
+    // the same single addition as k_prolong, so the sweep sees exactly the
+    // prolongated field and its (periodic) ghosts.  Warp w corrects row w, the
+    // two ring warps also rows TJ+2 and TJ+3.
+    auto correct = [&](double* P, int ip) {
+      const double* Cc = cslot(((ip >> 1) - cbase) % LY::NC);
+      auto row = [&](int rr) {
+        double* Pr = P + rr * PK;
+        const double* Cr = Cc + (rr >> 1) * LY::CK;
+#pragma unroll
+        for (int h = 0; h < (TK + 4 + 31) / 32; ++h) {
+          const int c = lane + 32 * h;
+          if (c < TK + 4) Pr[c] = Pr[c] + Cr[(c >> 1) + cshift];
+        }
+      };
+      row(warp);
+      if (warp == 0) row(NW);
+      if (warp == NW - 1) row(NW + 1);
     };
     if (tid == producer)
       for (int ip = i0 - 2; ip <= min(i0 + 2 + D, i1 + 1); ++ip) issue(ip, ip - i0 + 2);
@@ -443,6 +488,11 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     const int64_t rs0 = RV.s0, rs1 = RV.s1;
 
     for (int ip = i0 - 2; ip <= i0 + 2; ++ip) mbar_wait(&bars[ip - i0 + 2], 0);
+    if constexpr (PROL) {  // planes i0-2 .. i0+3 corrected before anything reads them
+      if (i0 + 3 <= i1 + 1) mbar_wait(&bars[5], 0);
+      for (int ip = i0 - 2; ip <= min(i0 + 3, i1 + 1); ++ip) correct(slot(ip - i0 + 2), ip);
+      __syncthreads();
+    }
     // prologue: red of planes i0-1, i0, i0+1 over rows 1..TJ+2, cols 1..TK+2
     // (independent: red reads only black cells).  Red cells only, loads first.
     {
@@ -553,8 +603,9 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     // slots of planes p-1 .. p+3 (rotated each step); nidx = slot of plane p+4
     double *sm_ = slot(1), *s0_ = slot(2), *s1_ = slot(3), *s2_ = slot(4), *s3_ = slot(5);
     int nidx = 6 % NPHI;
-    int widx = 5 % NPHI;                // slot of plane p+3 (awaited)
-    unsigned wph = (5 / NPHI) & 1;
+    constexpr int W0 = PROL ? 6 : 5;    // slot of plane p+3 (PROL: p+4) (awaited)
+    int widx = W0 % NPHI;
+    unsigned wph = (W0 / NPHI) & 1;
     int iidx = 0;                       // slot of plane p+3+D (issued)
     double* out = args.b + B.off + (int64_t)i0 * B.s0 + (int64_t)(j0 - 2 + r) * B.s1 + (k0 + lk);
     const int64_t bs0 = B.s0;
@@ -584,7 +635,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     auto step = [&](int p, double (&vp)[NH]) {
       const int q = p - i0;
       const bool do_red = p + 2 <= i1;
-      if (do_red) mbar_wait(&bars[widx], wph);
+      if (PROL ? p + 4 <= i1 + 1 : do_red) mbar_wait(&bars[widx], wph);
       widx = wrap(widx + 1);
       wph ^= widx == 0 ? 1u : 0u;
       __syncthreads();
@@ -685,6 +736,9 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
           }
           if (a) S2[o[h]] = nv[h];
         }
+      }
+      if constexpr (PROL) {  // s3_ is plane p+4's slot now; first read in step p+1
+        if (p + 4 <= i1 + 1) correct(s3_, p + 4);
       }
       out += bs0;
       load_rhs(p + 1, rv);
@@ -911,12 +965,82 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
   // (grid = ncol * (slots / ncol)) cut L2 misses but measured no faster
   static const int min_steps = getenv("AMRB_SWEEP_MINSTEPS") ? atoi(getenv("AMRB_SWEEP_MINSTEPS")) : 2;
   const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / min_steps));
-  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st, ma, args);
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st, ma, ma, args);
   check_launch("k_gsrb_sweep5");
   return true;
 }
 
+// Fused prolongation + first post-smoothing sweep: B = sweep(A + P(C)), where
+// P(C) is the piecewise-constant parent value of the coarse field C on the
+// box-local coarsening of A's level (A's ghosts filled to 2, C's to 1,
+// periodic).  Bit-identical to prolong_add; fill_boundary(A, 2); sweep.
+template <int TJ, int TK>
+bool launch5p(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
+              const double* r_base, const Coef& cf, const Level& clv, const Field& c, const double* c_base,
+              cudaStream_t st) {
+  constexpr int D = 3;
+  using LY = Sweep5Layout<TJ, TK, D>;
+  for (auto& gg : lv.geo)
+    if (gg.n[1] % TJ || gg.n[2] % TK) return false;
+  if (a.ngrow < 2 || r.ngrow < 1 || c.ngrow < 1) return false;
+  TmaDesc da = describe(lv, a), dc = describe(clv, c);
+  if (!da.ok || da.slot != lv.slot || !dc.ok || dc.slot != da.slot) return false;
+  int nres = 0;
+  for (auto x : lv.resident) nres += x ? 1 : 0;
+  CUtensorMap ma, mc;
+  std::memset(&ma, 0, sizeof ma);
+  std::memset(&mc, 0, sizeof mc);
+  if (!make_map(&ma, a_base, da, nres, LY::PJ, LY::PK)) return false;
+  if (!make_map(&mc, c_base, dc, nres, LY::CJ, LY::CK)) return false;
+  Sweep4Args args;
+  std::memset(&args, 0, sizeof args);
+  args.a_kc = -2 + da.g + da.f;
+  args.a_jc = -2 + da.g;
+  args.a_ic = da.g;
+  args.c_kc = -1 + dc.g + dc.f;
+  args.c_jc = -1 + dc.g;
+  args.c_ic = dc.g;
+  const auto& cols = lv.columns(TJ, TK);
+  if (cols.host.empty()) return true;
+  args.cols = cols.dev.p;
+  args.fa = a.dev.p;
+  args.fr = r.dev.p;
+  args.a = a_base;
+  args.rhs = r_base;
+  args.slot = lv.dslot.p;
+  args.ncols = (int)cols.host.size();
+  args.total = cols.total;
+  args.geo = lv.dgeo.p;
+  args.fb = b.dev.p;
+  args.b = b_base;
+  args.cf = cf;
+  auto kern = k_gsrb_sweep5<TJ, TK, D, 2, false, false, true>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES_PROL));
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * LY::NW, LY::BYTES_PROL));
+    per_sm = std::max(per_sm, 1);
+  }
+  const long long slots = (long long)per_sm * num_sms();
+  const long long ncol = (long long)cols.host.size();
+  const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES_PROL, st, ma, mc, args);
+  check_launch("k_gsrb_sweep5<PROL>");
+  return true;
+}
+
 }  // namespace
+
+bool launch_sweep_prolong_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
+                              const Field& r, const double* r_base, const Coef& cf, const Level& clv, const Field& c,
+                              const double* c_base, cudaStream_t st) {
+  int minj = 1 << 30;
+  for (auto& g : lv.geo) minj = std::min(minj, g.n[1]);
+  if (minj < 32) return false;
+  if (launch5p<16, 64>(lv, a, a_base, b, b_base, r, r_base, cf, clv, c, c_base, st)) return true;
+  if (launch5p<16, 32>(lv, a, a_base, b, b_base, r, r_base, cf, clv, c, c_base, st)) return true;
+  return false;
+}
 
 bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                       const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],

@@ -26,6 +26,7 @@ runs the identical bottom solve.  Results are bit-identical for any GPU count.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -38,6 +39,7 @@ from .geometry import Geometry
 from .interlevel import coarsened_layout, prolong_from
 from .layout import BoxArray, DistributionMapping
 from .push import PushTable, prolong_push
+from .stencil import gsrb_sweep_prolong
 from .multifab import FabArray, MultiFab, world_size
 
 __all__ = ["MLMG", "mg_hierarchy"]
@@ -132,7 +134,7 @@ class MLMG:
     """
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
-                 ghost_push=False, agg_cells=128**3):
+                 ghost_push=False, agg_cells=128**3, fuse_prolong=None):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
         if not all(geom.periodic):
@@ -204,6 +206,15 @@ class MLMG:
             lv.push, lv.push_local = False, lv.replicated or not self.dist
             if ghost_push:
                 self._make_push(lv)
+        # up-leg: prolongation fused into the first post-smoothing sweep
+        # (k_gsrb_sweep5<PROL>, box-local level pairs): no separate read+write
+        # pass over the fine phi and no fill after it; the restriction fills the
+        # fine phi to width 2 instead of 1 and the coarse phi gets a width-1 fill
+        if fuse_prolong is None:  # AMRB_FUSE_PROLONG=0: separate prolongation (A/B runs)
+            fuse_prolong = os.environ.get("AMRB_FUSE_PROLONG", "1") != "0"
+        for l, lv in enumerate(self.levels):
+            lv.fuse = (fuse_prolong and l < len(self.levels) - 1 and lv.boxlocal_next and not lv.push
+                       and self.nu2 >= 1)
         self._ghost = {}  # id(field) -> ghost width known to be current
         self._pending = False  # pushes to peers since the last device barrier
         self._reads = set()  # fields whose ghosts were read since the last barrier
@@ -303,7 +314,7 @@ class MLMG:
     def _resid_restrict(self, l):
         lv, nx = self.levels[l], self.levels[l + 1]
         phi = lv.phi[lv.cur]
-        self._need_ghosts(lv, phi, 1)
+        self._need_ghosts(lv, phi, 2 if lv.fuse else 1)  # the fused up-leg sweep reuses width 2
         dst = nx.rhs if lv.boxlocal_next else lv.tmp
         check(
             lib().amrb_residual_restrict(
@@ -357,6 +368,24 @@ class MLMG:
         else:
             prolong_from(fine, crse, (2, 2, 2), add=True)
             self._produced(fine, 0)
+
+    def _prolong_sweep(self, l):
+        """Fused up-leg step: lv.phi <- GSRB(lv.phi + P(nx.phi)).  False (nothing
+        launched) when the level does not take the fused TMA sweep path."""
+        lv, nx = self.levels[l], self.levels[l + 1]
+        a, b = lv.phi[lv.cur], lv.phi[1 - lv.cur]
+        crse = nx.phi[nx.cur]
+        self._need_ghosts(lv, a, 2)
+        self._need_ghosts(lv, lv.rhs, 1)
+        self._need_ghosts(nx, crse, 1)
+        try:
+            gsrb_sweep_prolong(a, b, lv.rhs, lv.dh, crse)
+        except NotImplementedError:
+            lv.fuse = False
+            return False
+        self._produced(b, 0)
+        lv.cur = 1 - lv.cur
+        return True
 
     def _residual_norm(self):
         top = self.levels[0]
@@ -422,8 +451,11 @@ class MLMG:
         if T < n:
             self._coarse_tail()
         for l in range(min(T, n - 1) - 1, -1, -1):
-            self._prolong(l)
-            self._smooth(L[l], self.nu2)
+            if L[l].fuse and self._prolong_sweep(l):
+                self._smooth(L[l], self.nu2 - 1)
+            else:
+                self._prolong(l)
+                self._smooth(L[l], self.nu2)
 
     def _cycle_and_norm(self):
         self.vcycle()

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-from ._native import check, i32p, lib
+from ._native import AMRB_ENOTSUP, check, i32p, lib
 from .device import dh_array, field_of, level_of, stream_ptr
 
 __all__ = ["laplacian", "residual", "gsrb_color", "gsrb_sweep", "residual_restrict", "dh_of"]
@@ -73,6 +73,24 @@ def gsrb_sweep(a, b, rhs, dh, fixed=None):
         _keep, fp = i32p(arr)
     check(lib().amrb_gsrb_sweep(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
                                 field_of(rhs).handle, _p(rhs), dh_array(dh), fp, stream_ptr()))
+
+
+def gsrb_sweep_prolong(a, b, rhs, dh, crse):
+    """b = one fused red+black sweep of (a + pc-interpolated crse), periodic;
+    crse on the box-local coarsened layout of a (ghosts width 1), a's ghosts
+    width 2, rhs's width 1.  Same bits as prolong_from(a, crse, add=True);
+    fill_boundary(a, 2); gsrb_sweep(a, b, rhs), but a is left unchanged.
+    Raises NotImplementedError (nothing launched) when the level does not take
+    the fused TMA sweep path."""
+    _same_layout(a, b, rhs)
+    if len(crse.ba) != len(a.ba):
+        raise ValueError("crse must live on the box-local coarsened layout")
+    rc = lib().amrb_gsrb_sweep_prolong(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
+                                       field_of(rhs).handle, _p(rhs), dh_array(dh), level_of(crse).handle,
+                                       field_of(crse).handle, _p(crse), stream_ptr())
+    if rc == AMRB_ENOTSUP:
+        raise NotImplementedError("gsrb_sweep_prolong: level does not take the fused TMA sweep path")
+    check(rc)
 
 
 def residual_restrict(crse, rhs, phi, dh):

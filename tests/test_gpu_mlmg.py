@@ -111,3 +111,25 @@ def test_ghost_push_solve_matches_oracle_bitwise(n, m):
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
+
+
+@pytest.mark.parametrize("n,m", [(128, 64), (256, 64)])
+def test_fused_prolong_sweep_solve_identical(n, m):
+    """MLMG(fuse_prolong=True) (default: prolongation inside the first
+    post-smoothing sweep) == fuse_prolong=False, bit for bit, same history."""
+    dom, ba, dm, geom, rhs = _problem(n, m, 5)
+    out = []
+    for fuse in (True, False):
+        phi = A.MultiFab(ba, dm, 1, 1)
+        b = A.MultiFab(ba, dm, 1, 0)
+        b.load_valid_from(dom, rhs)
+        mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), fuse_prolong=fuse)
+        if fuse:
+            assert any(lv.fuse for lv in mg.levels)
+        mg.solve(phi, b, rtol=1e-10, max_iter=100)
+        if fuse:
+            assert any(lv.fuse for lv in mg.levels)  # the fused path ran (no ENOTSUP fallback)
+        out.append((mg.iterations, list(mg.history), A.gather_global(phi, dom)))
+    assert out[0][0] == out[1][0]
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][2], out[1][2])

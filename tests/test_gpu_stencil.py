@@ -162,3 +162,53 @@ def test_sweep_and_prolong_push_equal_fill(n, m):
     P.prolong_push(b2, c, tab, add=True)
     for i in b1.fabs:
         assert torch.equal(b1.fab(i).data, b2.fab(i).data), i
+
+
+@pytest.mark.parametrize("n,m,lo", [(128, 128, 0), (128, 64, 0), (64, 32, 0), (64, 64, -32)])
+def test_sweep_prolong_equals_prolong_fill_sweep(n, m, lo):
+    """k_gsrb_sweep5<PROL>: GSRB(a + pc(c)) == prolong_from(add); fill(2);
+    gsrb_sweep, bit for bit on every valid cell; `a` is left unchanged."""
+    from paper_2009_12009_b200.interlevel import coarsened_layout, prolong_from
+
+    dom, ba, dm = _layout(n, m, lo)
+    tr = A.Transport(1)
+    g = torch.Generator(device="cuda").manual_seed(11)
+
+    def rnd(fa):
+        fa.storage.copy_(torch.randn(fa.storage.shape, generator=g, device="cuda", dtype=torch.float64))
+
+    a = A.MultiFab(ba, dm, 1, 2)
+    rhs = A.MultiFab(ba, dm, 1, 1)
+    rnd(a)
+    rnd(rhs)
+    cba = coarsened_layout(ba, 2)
+    c = A.MultiFab(cba, dm, 1, 2)
+    rnd(c)
+    A.fill_boundary(a, tr, dom, True, ngrow=2)
+    A.fill_boundary(rhs, tr, dom, True)
+    A.fill_boundary(c, tr, dom.coarsen(2), True, ngrow=1)
+    a0 = a.storage.clone()
+    dh = (float(n * n), 0.5 * n * n, 2.0 * n * n)
+    fused = A.MultiFab(ba, dm, 1, 2)
+    S.gsrb_sweep_prolong(a, fused, rhs, dh, c)
+    assert torch.equal(a.storage, a0)  # the input is not modified
+    ref = A.MultiFab(ba, dm, 1, 2)
+    prolong_from(a, c, (2, 2, 2), add=True)
+    A.fill_boundary(a, tr, dom, True, ngrow=2)
+    S.gsrb_sweep(a, ref, rhs, dh)
+    torch.cuda.synchronize()
+    for i in ref.fabs:
+        assert torch.equal(ref.fab(i).valid(), fused.fab(i).valid()), i
+
+
+def test_sweep_prolong_rejects_non_coarsened_layout():
+    dom, ba, dm = _layout(64, 32)
+    a = A.MultiFab(ba, dm, 1, 2)
+    rhs = A.MultiFab(ba, dm, 1, 1)
+    b = A.MultiFab(ba, dm, 1, 2)
+    # same box count, but the "coarse" boxes are shifted by one cell: not the
+    # coarsened fine boxes
+    wrong = A.MultiFab(A.BoxArray([A.Box((1, 0, 0), (32, 31, 31))]).max_size(16), dm, 1, 1)
+    assert len(wrong.ba) == len(ba)
+    with pytest.raises(ValueError):
+        S.gsrb_sweep_prolong(a, b, rhs, (1.0, 1.0, 1.0), wrong)
