@@ -454,22 +454,30 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     };
     // PROL: plane tile P (plane ip) += coarse parent, rows 0..TJ+3, cols 0..TK+3 --
     // the same single addition as k_prolong, so the sweep sees exactly the
-    // prolongated field and its (periodic) ghosts.  Warp w corrects row w, the
-    // two ring warps also rows TJ+2 and TJ+3.
+    // prolongated field and its (periodic) ghosts.  Warp w corrects row w.
     auto correct = [&](double* P, int ip) {
       const double* Cc = cslot(((ip >> 1) - cbase) % LY::NC);
       auto row = [&](int rr) {
         double* Pr = P + rr * PK;
-        const double* Cr = Cc + (rr >> 1) * LY::CK;
+        const double* Cr = Cc + (rr >> 1) * LY::CK + cshift;
 #pragma unroll
         for (int h = 0; h < (TK + 4 + 31) / 32; ++h) {
           const int c = lane + 32 * h;
-          if (c < TK + 4) Pr[c] = Pr[c] + Cr[(c >> 1) + cshift];
+          if (c < TK + 4) Pr[c] = Pr[c] + Cr[c >> 1];
         }
       };
       row(warp);
-      if (warp == 0) row(NW);
-      if (warp == NW - 1) row(NW + 1);
+      // rows TJ+2, TJ+3: one cell per thread, on the highest thread ids (the
+      // ring-column warp relaxes the fewest cells).  Measured: 8.80-8.84 ms C3
+      // solve vs 8.88 with both extra rows on the two ring warps; 16-byte
+      // pair loads/stores measured no faster (8.85-8.86).
+      constexpr int NT = 32 * NW, NX = 2 * (TK + 4);
+      static_assert(NX <= NT, "two extra rows fit one pass");
+      const int x = NT - 1 - tid;
+      if (x < NX) {
+        const int rr = NW + x / (TK + 4), c = x % (TK + 4);
+        P[rr * PK + c] = P[rr * PK + c] + Cc[(rr >> 1) * LY::CK + (c >> 1) + cshift];
+      }
     };
     if (tid == producer)
       for (int ip = i0 - 2; ip <= min(i0 + 2 + D, i1 + 1); ++ip) issue(ip, ip - i0 + 2);
