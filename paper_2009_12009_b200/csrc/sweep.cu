@@ -56,6 +56,8 @@ struct Sweep4Args {
   int fixed_lo[3], fixed_hi[3];
   PushDev push;  // k_gsrb_sweep5<..., PUSH>: fill b's ghosts as planes are written
   int c_kc, c_jc, c_ic;  // k_gsrb_sweep5<..., PROL>: coarse tensor-map offsets (tile from (j0/2-1, k0/2-1))
+  int rpf;               // k_gsrb_sweep5: rhs plane prefetch distance into L2 (0: off)
+  int q_kc, q_jc, q_ic;  // rhs tensor-map offsets (prefetch box from (j0-1, k0-1), even start column)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -91,6 +93,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch4(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
@@ -374,7 +381,7 @@ struct Sweep5Layout {
 template <int TJ, int TK, int D, int MINB, bool FIXED, bool PUSH, bool PROL = false>
 __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     k_gsrb_sweep5(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
-                  const __grid_constant__ Sweep4Args args) {
+                  const __grid_constant__ CUtensorMap tmR, const __grid_constant__ Sweep4Args args) {
   pdl_entry();
   using LY = Sweep5Layout<TJ, TK, D>;
   constexpr int PK = LY::PK, NPHI = LY::NPHI, NH = LY::NH, NW = LY::NW;
@@ -425,6 +432,7 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
     // smem cell (row, c) of plane ip is red iff ((g.lo[0] + ip + jk0 + row + c) & 1) == 0
     const int par0 = (g.lo[0] + i0 + jk0) & 1;  // parity base of plane i0
     const int cbase = (i0 - 2) >> 1;            // PROL: coarse plane of ring slot 0
+    const int qkx = (k0 + args.q_kc) & ~1;      // rhs prefetch box: even start column
     const int ckx = (k0 >> 1) + args.c_kc;      // PROL: tensor column of coarse cell (k0-2)/2
     const int cshift = ckx & 1;                 //       the tile starts cshift columns before it
 
@@ -648,6 +656,10 @@ __global__ void __launch_bounds__(32 * (TJ + 2), MINB)
       wph ^= widx == 0 ? 1u : 0u;
       __syncthreads();
       if (tid == producer && p + 3 + D <= i1 + 1) issue(p + 3 + D, iidx);
+      // rhs plane x is first read by load_rhs at the end of step x-3: warm L2
+      // with plane p + rpf (no registers; the per-lane loads then hit L2)
+      if (tid == producer && args.rpf && p + args.rpf < i1 + 2)
+        tma_prefetch4(&tmR, qkx, j0 + args.q_jc, p + args.rpf + args.q_ic, bslot);
       iidx = wrap(iidx + 1);
       const double* Sm = sm_;
       const double* S0 = s0_;
@@ -916,6 +928,31 @@ bool launch4(Level& lv, const Field& a, const double* a_base, const Field& b, do
   return true;
 }
 
+// rhs tensor map for the L2 prefetch of k_gsrb_sweep5 (box TJ+2 rows x TK+4
+// columns from (j0-1, even column <= k0-1)); rpf = 0 when it cannot be made.
+// Distance in planes: AMRB_RHS_PREFETCH (plain sweep, default 0) and
+// AMRB_RHS_PREFETCH_PROL (fused prolongation sweep, default 3).  Measured on
+// the C3 solve (bench.py): PROL 3 -> 8.84 to 8.67 ms (2: no gain, 5: same as
+// 3); on the plain fine-level sweep 3 costs 3 us per launch (104.5 -> 107.5),
+// 2 is neutral, so it stays off there.
+template <int TJ, int TK>
+void rhs_prefetch_map(const Level& lv, const Field& r, const double* r_base, int nres, CUtensorMap* mq,
+                      Sweep4Args& args, bool prol) {
+  static const int dist_plain = getenv("AMRB_RHS_PREFETCH") ? atoi(getenv("AMRB_RHS_PREFETCH")) : 0;
+  static const int dist_prol = getenv("AMRB_RHS_PREFETCH_PROL") ? atoi(getenv("AMRB_RHS_PREFETCH_PROL")) : 3;
+  const int dist = prol ? dist_prol : dist_plain;
+  std::memset(mq, 0, sizeof *mq);
+  args.rpf = 0;
+  if (dist <= 0) return;
+  TmaDesc dr = describe(lv, r);
+  if (!dr.ok || dr.slot != lv.slot) return;
+  if (!make_map(mq, r_base, dr, nres, TJ + 2, TK + 4)) return;
+  args.q_kc = -1 + dr.g + dr.f;
+  args.q_jc = -1 + dr.g;
+  args.q_ic = dr.g;
+  args.rpf = dist;
+}
+
 template <int TJ, int TK, int D, int MINB>
 bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
              const double* r_base, const Coef& cf, const int fixed_lo[3], const int fixed_hi[3], bool fixed,
@@ -955,6 +992,8 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
     args.fixed_hi[x] = fixed_hi[x];
   }
   if (push) args.push = *push;
+  CUtensorMap mq;
+  rhs_prefetch_map<TJ, TK>(lv, r, r_base, nres, &mq, args, false);
   const int kv = (fixed ? 1 : 0) + (push ? 2 : 0);
   auto kern = kv == 0   ? k_gsrb_sweep5<TJ, TK, D, MINB, false, false>
               : kv == 1 ? k_gsrb_sweep5<TJ, TK, D, MINB, true, false>
@@ -973,7 +1012,7 @@ bool launch5(Level& lv, const Field& a, const double* a_base, const Field& b, do
   // (grid = ncol * (slots / ncol)) cut L2 misses but measured no faster
   static const int min_steps = getenv("AMRB_SWEEP_MINSTEPS") ? atoi(getenv("AMRB_SWEEP_MINSTEPS")) : 2;
   const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / min_steps));
-  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st, ma, ma, args);
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, bytes, st, ma, ma, mq, args);
   check_launch("k_gsrb_sweep5");
   return true;
 }
@@ -1022,6 +1061,8 @@ bool launch5p(Level& lv, const Field& a, const double* a_base, const Field& b, d
   args.fb = b.dev.p;
   args.b = b_base;
   args.cf = cf;
+  CUtensorMap mq;
+  rhs_prefetch_map<TJ, TK>(lv, r, r_base, nres, &mq, args, true);
   auto kern = k_gsrb_sweep5<TJ, TK, D, 2, false, false, true>;
   static int per_sm = 0;
   if (!per_sm) {
@@ -1032,7 +1073,7 @@ bool launch5p(Level& lv, const Field& a, const double* a_base, const Field& b, d
   const long long slots = (long long)per_sm * num_sms();
   const long long ncol = (long long)cols.host.size();
   const long long grid = std::min<long long>(slots, std::max<long long>(ncol, cols.total / 2));
-  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES_PROL, st, ma, mc, args);
+  launch_k(kern, (unsigned)std::max<long long>(grid, 1), 32 * LY::NW, LY::BYTES_PROL, st, ma, mc, mq, args);
   check_launch("k_gsrb_sweep5<PROL>");
   return true;
 }
