@@ -390,7 +390,9 @@ class MLMG:
     def _residual_norm(self):
         top = self.levels[0]
         phi = top.phi[top.cur]
-        self._need_ghosts(top, phi, 1)
+        # width 2, not 1: the next cycle's first sweep reads this phi's ghosts
+        # to width 2, so one fill serves both (one fine fill less per cycle)
+        self._need_ghosts(top, phi, 2)
         check(
             lib().amrb_residual_norm(
                 level_of(phi).handle,
