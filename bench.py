@@ -263,6 +263,9 @@ def run_ours(args):
     # every level's smoother relaxations, counted once for the whole job (replicated
     # bottom levels run redundantly on every rank but are counted once)
     updates_job = mg.cell_updates_per_cycle * sum(iters)
+    # plain (unfused) fine-level sweeps per solve: nu1 + nu2 per cycle, one of
+    # them fused with the prolongation when the up-leg is fused
+    fine_per_step = (mg.nu1 + mg.nu2 - (1 if mg.levels[0].fuse else 0)) * sum(iters) / len(iters)
     value = updates_job / t_dev
     ms = 1e3 * t_dev / args.steps
 
@@ -401,7 +404,11 @@ def run_ours(args):
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "us_per_launch": t_sweep * 1e6,
-                         "kernel_cell_updates_per_s": nloc / t_sweep},
+                         "kernel_cell_updates_per_s": nloc / t_sweep,
+                         # plain fine-level sweeps per solve x this launch time / solve time
+                         # (the ncu launch list's share of the same kernel should agree)
+                         "launches_per_step": fine_per_step,
+                         "share_of_step": fine_per_step * t_sweep / (ms / 1e3)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
