@@ -13,6 +13,8 @@
 // else), and every update uses the shared lap7 / relax / avg8 expressions,
 // so results are bit-identical to the oracle's fill / red / fill / black
 // sequence (oracle/mlmg_ref.py) and to the device multi-kernel path.
+#include <cooperative_groups.h>
+
 #include <cstring>
 
 #include "stencil_common.cuh"
@@ -238,10 +240,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail(TailArgs a) {
 // enough threads (one per cell of a colour, capped at the block) and syncs on
 // a named barrier sized to them (one warp: __syncwarp).
 // ---------------------------------------------------------------------------
-template <int LOG0>
-__global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) {
-  pdl_entry();
-  extern __shared__ __align__(16) double sm[];
+// GIO: level-0 rhs comes from / phi goes to global memory (false: both stay
+// in shared memory, the cluster kernel below owns them).  base: first TailArgs
+// level this body runs (its level 0).
+template <int LOG0, bool GIO>
+__device__ __forceinline__ void tail_p2_body(const TailArgs& a, double* sm, int base) {
   const int tid = threadIdx.x;
   // level l: n = 1 << (LOG0 - l); phi and rhs dense n^3 at smem offsets
   auto cells = [](int l) { return 1 << (3 * (LOG0 - l)); };
@@ -255,15 +258,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
     else
       asm volatile("bar.sync 1, %0;\n" ::"r"(na) : "memory");
   };
-  auto PHI = [&](int l) { return sm + a.lv[l].phi_off; };
-  auto RHS = [&](int l) { return sm + a.lv[l].rhs_off; };
+  auto PHI = [&](int l) { return sm + a.lv[base + l].phi_off; };
+  auto RHS = [&](int l) { return sm + a.lv[base + l].rhs_off; };
 
   auto color = [&](int l, int c) {
     const int s = LOG0 - l, n = 1 << s, m = n - 1;
     double* p = PHI(l);
     const double* r = RHS(l);
-    const Coef cf = a.lv[l].cf;
-    const int lp = a.lv[l].lo_par;
+    const Coef cf = a.lv[base + l].cf;
+    const int lp = a.lv[base + l].lo_par;
     const int np = cells(l) / 2;
     for (int e = tid; e < np; e += nact(l)) {
       const int kp = e & ((n >> 1) - 1), ij = e >> (s - 1);
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
     const double* p = PHI(l);
     const double* r = RHS(l);
     double* rc = RHS(l + 1);
-    const Coef cf = a.lv[l].cf;
+    const Coef cf = a.lv[base + l].cf;
     for (int e = tid; e < cells(l + 1); e += nact(l)) {
       const int K = e & ((1 << cs) - 1), J = (e >> cs) & ((1 << cs) - 1), I = e >> (2 * cs);
       double v[8];
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
     for (int e = tid; e < cells(l); e += nact(l)) p[e] = 0.0;
   };
 
-  {  // level-0 rhs from global
+  if (GIO) {  // level-0 rhs from global
     const int s = LOG0, n = 1 << s;
     double* r = RHS(0);
     for (int e = tid; e < cells(0); e += kTailThreads) {
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
     }
   }
   __syncthreads();
-  const int L = a.nlev;
+  const int L = a.nlev - base;
   for (int l = 0; l < L; ++l) {
     if (tid < nact(l)) {
       zero(l);
@@ -356,13 +359,137 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
     }
     __syncthreads();
   }
-  {  // level-0 phi to global
+  if (GIO) {  // level-0 phi to global
     const int s = LOG0, n = 1 << s;
     const double* p = PHI(0);
     for (int e = tid; e < cells(0); e += kTailThreads) {
       const int k = e & (n - 1), j = (e >> s) & (n - 1), i = e >> (2 * s);
       a.phi[i * a.ps0 + j * a.ps1 + k] = p[e];
     }
+  }
+}
+
+template <int LOG0>
+__global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) {
+  pdl_entry();
+  extern __shared__ __align__(16) double sm[];
+  tail_p2_body<LOG0, true>(a, sm, 0);
+}
+
+// ---------------------------------------------------------------------------
+// 32^3 top level + 16^3 .. tail in ONE cluster of 8 CTAs.  The 32^3 level
+// (phi + rhs = 512 KB) does not fit one CTA, but it does fit a cluster: CTA r
+// holds planes [4r, 4r+4) of phi and rhs in its shared memory and reads the
+// two neighbouring planes (4r-1, 4r+4, periodic) from its cluster peers'
+// shared memory (DSMEM); cluster barriers separate the colours.  The
+// restriction writes the 16^3 rhs straight into CTA 0's shared memory, CTA 0
+// runs the power-of-two tail body on it, and every CTA prolongs from CTA 0's
+// 16^3 phi.  The 32^3 phi leaves with its width-1 periodic ghost layer
+// written, so the next finer level's fused prolongation sweep needs no fill.
+// This replaces 16 launches per V-cycle (fills, sweeps, residual-restrict,
+// gather copies, prolongation at 32^3) with one.  Same lap7 / relax / avg8
+// operand order as every other path: bit-identical results.
+// ---------------------------------------------------------------------------
+constexpr int kClCtas = 8;
+constexpr int kClN = 32;                  // top-level extent
+constexpr int kClPl = kClN / kClCtas;     // planes per CTA
+constexpr int kClSlab = kClPl * kClN * kClN;
+
+__global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 1)
+    k_coarse_tail_cl(TailArgs a, int slab_off) {
+  pdl_entry();
+  extern __shared__ __align__(16) double sm[];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  constexpr int M = kClN - 1;
+  double* p = sm + slab_off;  // phi [kClPl][32][32]
+  double* rh = p + kClSlab;   // rhs, same shape
+  const double* pm = cl.map_shared_rank(p, (r + kClCtas - 1) % kClCtas) + (kClPl - 1) * kClN * kClN;  // plane 4r-1
+  const double* pp = cl.map_shared_rank(p, (r + 1) % kClCtas);                                        // plane 4r+4
+  const TailLevel& L = a.lv[0];
+  const Coef cf = L.cf;
+  const int i0 = kClPl * r;
+
+  for (int e = tid; e < kClSlab; e += kTailThreads) {
+    const int k = e & M, j = (e >> 5) & M, li = e >> 10;
+    rh[e] = a.rhs[(int64_t)(i0 + li) * a.rs0 + (int64_t)j * a.rs1 + k];
+    p[e] = 0.0;
+  }
+  cl.sync();
+
+  auto color = [&](int c) {
+    for (int e = tid; e < kClSlab / 2; e += kTailThreads) {
+      const int kp = e & 15, j = (e >> 4) & M, li = e >> 9;
+      const int k = 2 * kp + ((L.lo_par + i0 + li + j + c) & 1);
+      const int jk = (j << 5) | k;
+      const int o = (li << 10) | jk;
+      const double v = p[o];
+      const double xm = li > 0 ? p[o - kClN * kClN] : pm[jk];
+      const double xp = li < kClPl - 1 ? p[o + kClN * kClN] : pp[jk];
+      const double lap = lap7(v, xm, xp, p[(li << 10) | (((j - 1) & M) << 5) | k], p[(li << 10) | (((j + 1) & M) << 5) | k],
+                              p[(li << 10) | (j << 5) | ((k - 1) & M)], p[(li << 10) | (j << 5) | ((k + 1) & M)], cf);
+      p[o] = relax(v, rh[o], lap, cf.rgamma);
+    }
+  };
+  auto smooth = [&](int nsw) {
+    for (int q = 0; q < nsw; ++q) {
+      color(0);
+      cl.sync();
+      color(1);
+      cl.sync();
+    }
+  };
+
+  smooth(a.nu1);
+  {  // rhs_16 = avg8(rhs_32 - L phi_32), coarse planes [2r, 2r+2), into CTA 0
+    double* rc = cl.map_shared_rank(sm + a.lv[1].rhs_off, 0);
+    for (int e = tid; e < kClSlab / 8; e += kTailThreads) {
+      const int K = e & 15, J = (e >> 4) & 15, dI = e >> 8;
+      double v[8];
+#pragma unroll
+      for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+          for (int dk = 0; dk < 2; ++dk) {
+            const int li = 2 * dI + di, j = 2 * J + dj, k = 2 * K + dk;
+            const int jk = (j << 5) | k;
+            const int o = (li << 10) | jk;
+            const double xm = li > 0 ? p[o - kClN * kClN] : pm[jk];
+            const double xp = li < kClPl - 1 ? p[o + kClN * kClN] : pp[jk];
+            v[di * 4 + dj * 2 + dk] =
+                rh[o] - lap7(p[o], xm, xp, p[(li << 10) | (((j - 1) & M) << 5) | k],
+                             p[(li << 10) | (((j + 1) & M) << 5) | k], p[(li << 10) | (j << 5) | ((k - 1) & M)],
+                             p[(li << 10) | (j << 5) | ((k + 1) & M)], cf);
+          }
+      rc[((i0 / 2 + dI) << 8) | (J << 4) | K] = avg8t(v);
+    }
+  }
+  cl.sync();
+  if (r == 0) tail_p2_body<4, false>(a, sm, 1);
+  cl.sync();
+  {  // phi_32 += phi_16(parent), from CTA 0
+    const double* pc = cl.map_shared_rank(sm + a.lv[1].phi_off, 0);
+    for (int e = tid; e < kClSlab; e += kTailThreads) {
+      const int k = e & M, j = (e >> 5) & M, li = e >> 10;
+      p[e] = p[e] + pc[(((i0 + li) >> 1) << 8) | ((j >> 1) << 4) | (k >> 1)];
+    }
+  }
+  cl.sync();
+  smooth(a.nu2);
+  // valid cells + the width-1 periodic ghost layer (the full grown box, as a
+  // width-1 FillBoundary of a single periodic box writes it)
+  constexpr int E = kClN + 2;
+  for (int e = tid; e < kClPl * E * E; e += kTailThreads) {
+    const int kk = e % E, jj = (e / E) % E, li = e / (E * E);
+    const int j = jj - 1, k = kk - 1;
+    const double v = p[(li << 10) | ((j & M) << 5) | (k & M)];
+    const int64_t jko = (int64_t)j * a.ps1 + k;
+    a.phi[(int64_t)(i0 + li) * a.ps0 + jko] = v;
+    if (i0 + li == 0) a.phi[(int64_t)kClN * a.ps0 + jko] = v;
+    if (i0 + li == kClN - 1) a.phi[-a.ps0 + jko] = v;
   }
 }
 
@@ -404,7 +531,6 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
           if (a.lv[l - 1].n[x] != 2 * L.n[x]) throw Error(AMRB_EINVAL, "tail levels must halve");
     }
     const size_t bytes = (size_t)off * sizeof(double);
-    if (bytes > 227 * 1024) throw Error(AMRB_EINVAL, "coarse tail does not fit in shared memory");
     const FabView& vr = fr.host[0];
     const FabView& vp = fp.host[0];
     a.warp_from = nlev;
@@ -425,6 +551,26 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
     // power-of-two cubic chain (each level >= 4 per side except possibly the
     // bottom, which must be >= 2): dense layout, masked periodic indexing
     const int n0 = a.lv[0].n[0];
+    bool cl = n0 == kClN && nlev >= 2 && (n0 >> (nlev - 1)) >= 2 && fp.ng3[0] >= 1 &&
+              fp.ng3[1] >= 1 && fp.ng3[2] >= 1;
+    for (int l = 0; l < nlev && cl; ++l)
+      cl = a.lv[l].n[0] == (n0 >> l) && a.lv[l].n[1] == (n0 >> l) && a.lv[l].n[2] == (n0 >> l);
+    if (cl) {  // 32^3 top level on a cluster, the 16^3 .. chain in CTA 0
+      int o2 = 0;
+      for (int l = 1; l < nlev; ++l) {
+        const int c = (n0 >> l) * (n0 >> l) * (n0 >> l);
+        a.lv[l].phi_off = o2;
+        o2 += c;
+        a.lv[l].rhs_off = o2;
+        o2 += c;
+      }
+      const int slab_off = (o2 + 15) & ~15;
+      const size_t b2 = (size_t)(slab_off + 2 * kClSlab) * sizeof(double);
+      AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2));
+      launch_k(k_coarse_tail_cl, kClCtas, kTailThreads, b2, (cudaStream_t)stream, a, slab_off);
+      check_launch("k_coarse_tail_cl");
+      return;
+    }
     bool p2 = n0 >= 2 && n0 <= 16 && (n0 & (n0 - 1)) == 0 && (n0 >> (nlev - 1)) >= 2;
     for (int l = 0; l < nlev && p2; ++l)
       p2 = a.lv[l].n[0] == (n0 >> l) && a.lv[l].n[1] == (n0 >> l) && a.lv[l].n[2] == (n0 >> l);
@@ -445,6 +591,7 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
       check_launch("k_coarse_tail_p2");
       return;
     }
+    if (bytes > 227 * 1024) throw Error(AMRB_EINVAL, "coarse tail does not fit in shared memory");
     static bool configured = false;
     if (!configured) {
       AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));

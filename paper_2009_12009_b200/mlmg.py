@@ -134,7 +134,7 @@ class MLMG:
     """
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
-                 ghost_push=False, agg_cells=128**3, fuse_prolong=None):
+                 ghost_push=False, agg_cells=128**3, fuse_prolong=None, cluster_tail=None):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
         if not all(geom.periodic):
@@ -185,6 +185,19 @@ class MLMG:
             ) <= 200 * 1024 and n - t <= 8 and t > 0:
                 self.tail = t
                 break
+        # a 32^3 single-box level above a 16^3 .. tail joins it: the cluster
+        # variant of the tail kernel (8 CTAs, the 32^3 level split in slabs
+        # across their shared memory) runs it too (AMRB_CLUSTER_TAIL=0: off)
+        self.cluster_tail = False
+        if (cluster_tail is None and os.environ.get("AMRB_CLUSTER_TAIL", "1") != "0") or cluster_tail:
+            t = self.tail
+            if 1 < t < n and n - t + 1 <= 8:
+                top = self.levels[t - 1]
+                ext = [tuple(self.levels[x].domain.extents()) for x in range(t - 1, n)]
+                chain = all(e == (32 >> x,) * 3 for x, e in enumerate(ext)) and ext[-1][0] >= 2
+                if chain and len(top.ba) == 1 and (top.replicated or not self.dist):
+                    self.tail = t - 1
+                    self.cluster_tail = True
         if self.tail < n:
             tl = self.levels[self.tail:]
             lohi = np.zeros((len(tl), 6), dtype=np.int32)
@@ -332,7 +345,8 @@ class MLMG:
         if not lv.boxlocal_next:
             self._gather_replica(lv, nx)
         self._produced(nx.rhs, 0)
-        self._need_ghosts(nx, nx.rhs, 1)
+        if l + 1 != self.tail:  # the coarse tail reads valid rhs cells only
+            self._need_ghosts(nx, nx.rhs, 1)
 
     def _gather_replica(self, lv, nx):
         """tmp (coarsened layout of lv, maybe distributed) -> nx.rhs (one box)."""
@@ -417,7 +431,7 @@ class MLMG:
         """All tail levels in one kernel: reads rhs, writes phi of levels[tail]."""
         lv = self.levels[self.tail]
         phi = lv.phi[lv.cur]
-        self._produced(phi, 0)
+        self._produced(phi, 1 if self.cluster_tail else 0)  # the cluster variant writes the width-1 ghosts
         lohi, lp = i32p(self._tail_lohi)
         dh = np.ascontiguousarray(self._tail_dh)
         check(

@@ -133,3 +133,27 @@ def test_fused_prolong_sweep_solve_identical(n, m):
     assert out[0][0] == out[1][0]
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][2], out[1][2])
+
+
+@pytest.mark.parametrize("n,m", [(64, 32), (128, 64), (256, 64)])
+def test_cluster_tail_solve_identical(n, m):
+    """MLMG(cluster_tail=True) (default: the 32^3 level joins the coarse tail on
+    an 8-CTA cluster) == cluster_tail=False, bit for bit, same history; at 64^3
+    also == the oracle."""
+    dom, ba, dm, geom, rhs = _problem(n, m, 7)
+    out = []
+    for ct in (True, False):
+        phi = A.MultiFab(ba, dm, 1, 1)
+        b = A.MultiFab(ba, dm, 1, 0)
+        b.load_valid_from(dom, rhs)
+        mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), cluster_tail=ct)
+        assert mg.cluster_tail == ct
+        mg.solve(phi, b, rtol=1e-10, max_iter=100)
+        out.append((mg.iterations, list(mg.history), A.gather_global(phi, dom)))
+    assert out[0][0] == out[1][0]
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][2], out[1][2])
+    if n == 64:
+        ref = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), tboxes(ba)).solve(rhs, rtol=1e-10, max_iter=100)
+        assert out[0][0] == ref["iterations"] and out[0][1] == ref["history"]
+        assert np.array_equal(out[0][2], ref["phi"])
