@@ -332,6 +332,20 @@ int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
                      const amrb_field* rhs, const double* rhs_base, amrb_field* phi,
                      double* phi_base, int nu1, int nu2, int nbottom, void* stream);
 
+/* One single-box periodic MLMG level's half V-cycle in one grid-synchronised
+ * (cooperative) launch -- the per-level steps of the reference-semantics
+ * V-cycle (oracle/mlmg_ref.py) for a level small enough
+ * to be launch-latency bound.  up == 0: zero phi, nsweeps in-place GSRB
+ * sweeps, then crse (the next coarser level's rhs, valid cells) =
+ * avg8(rhs - L phi).  up == 1: phi += crse(parent) (crse = coarser phi, valid
+ * cells read), nsweeps sweeps, then phi's width-1 periodic ghost layer.
+ * lohi: the level's box (6 ints), dh: 1/h^2 per axis.  Extents must be even.
+ * Bit-identical to fill + amrb_gsrb_sweep / amrb_residual_restrict /
+ * amrb_prolong. */
+int amrb_level_grid(int up, const int32_t* lohi, const double* dh, const amrb_field* rhs,
+                    const double* rhs_base, amrb_field* phi, double* phi_base, const amrb_field* crse,
+                    double* crse_base, int nsweeps, void* stream);
+
 /* reduce (fabarray.py:409-440) over valid cells of one component on this
  * device: kind 0 sum, 1 min, 2 max, 3 max|x| (inf-norm).  Deterministic:
  * fixed-shape per-tile partials then one ordered pass.  Result (one double)

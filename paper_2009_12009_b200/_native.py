@@ -86,6 +86,7 @@ _SIGS = {
     "amrb_reduce": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
     "amrb_residual_norm": (C.c_int, [vp, vp, vp, vp, vp, P(f64), vp, vp]),
     "amrb_coarse_tail": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    "amrb_level_grid": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, vp, vp, C.c_int, vp]),
     "amrb_domain_bc": (C.c_int, [vp, vp, vp, C.c_int, P(i32), P(i32), f64, vp]),
     "amrb_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
     "amrb_nccl_comm_create": (C.c_int, [P(C.c_uint8), C.c_int, C.c_int, P(vp)]),

@@ -493,6 +493,119 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// One small single-box periodic level's half of the V-cycle in ONE grid-
+// synchronised launch (cooperative: every CTA resident, grid.sync() between
+// phases).  Down: zero phi, nu1 in-place GSRB sweeps (red, sync, black,
+// sync), rhs_c = avg8(rhs - L phi) into the next coarser level.  Up: phi +=
+// phi_c(parent), nu2 sweeps, then the width-1 periodic ghost layer.  The
+// periodic neighbour is read by index wrap (the cell a ghost fill would have
+// copied), so no fill kernels run; the level stays in L2 (64^3: 2 MB phi).
+// Replaces per sweep a fill + a sweep launch (~15 us of launch-latency-bound
+// work at 64^3) with two grid barriers.  Same lap7 / relax / avg8 operand
+// order: bit-identical to the multi-kernel path and the oracle.
+// ---------------------------------------------------------------------------
+struct GridLevelArgs {
+  int n0, n1, n2, lo_par, nsw, up;
+  Coef cf;
+  double* phi;  // valid lo cell
+  int ps0, ps1;  // 32-bit strides: these levels are small (checked on the host)
+  const double* rhs;
+  int rs0, rs1;
+  double* c;  // down: coarse rhs (written); up: coarse phi (read); valid lo cell
+  int cs0, cs1;
+};
+
+__global__ void __launch_bounds__(512, 2) k_level_grid(GridLevelArgs a) {
+  pdl_entry();
+  namespace cg = cooperative_groups;
+  cg::grid_group g = cg::this_grid();
+  const int nt = (int)gridDim.x * blockDim.x;
+  const int t0 = (int)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n0 = a.n0, n1 = a.n1, n2 = a.n2, h = n2 >> 1;
+  const int ncell = (int)n0 * n1 * n2;
+  double* const p = a.phi;
+  auto P = [&](int i, int j, int k) -> double& { return p[i * a.ps0 + j * a.ps1 + k]; };
+  auto lapw = [&](int i, int j, int k) {
+    const int im = i ? i - 1 : n0 - 1, ip = i + 1 < n0 ? i + 1 : 0;
+    const int jm = j ? j - 1 : n1 - 1, jp = j + 1 < n1 ? j + 1 : 0;
+    const int km = k ? k - 1 : n2 - 1, kp = k + 1 < n2 ? k + 1 : 0;
+    return lap7(P(i, j, k), P(im, j, k), P(ip, j, k), P(i, jm, k), P(i, jp, k), P(i, j, km), P(i, j, kp), a.cf);
+  };
+  auto color = [&](int c) {
+    for (int e = t0; e < ncell / 2; e += nt) {
+      const int kq = (int)(e % h);
+      const int ij = e / h;
+      const int j = (int)(ij % n1), i = (int)(ij / n1);
+      const int k = 2 * kq + ((a.lo_par + i + j + c) & 1);
+      const double v = P(i, j, k);
+      const double lap = lapw(i, j, k);
+      P(i, j, k) = relax(v, a.rhs[i * a.rs0 + j * a.rs1 + k], lap, a.cf.rgamma);
+    }
+  };
+  auto smooth = [&]() {
+    for (int q = 0; q < a.nsw; ++q) {
+      color(0);
+      g.sync();
+      color(1);
+      g.sync();
+    }
+  };
+  auto cell = [&](int e, int& i, int& j, int& k) {
+    k = (int)(e % n2);
+    const int ij = e / n2;
+    j = (int)(ij % n1);
+    i = (int)(ij / n1);
+  };
+  if (!a.up) {
+    for (int e = t0; e < ncell; e += nt) {
+      int i, j, k;
+      cell(e, i, j, k);
+      P(i, j, k) = 0.0;
+    }
+    g.sync();
+    smooth();
+    const int c0 = n0 >> 1, c1 = n1 >> 1, c2 = n2 >> 1;
+    for (int e = t0; e < ncell / 8; e += nt) {
+      const int K = (int)(e % c2);
+      const int IJ = e / c2;
+      const int J = (int)(IJ % c1), I = (int)(IJ / c1);
+      double v[8];
+#pragma unroll
+      for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+          for (int dk = 0; dk < 2; ++dk) {
+            const int i = 2 * I + di, j = 2 * J + dj, k = 2 * K + dk;
+            v[di * 4 + dj * 2 + dk] = a.rhs[i * a.rs0 + j * a.rs1 + k] - lapw(i, j, k);
+          }
+      a.c[I * a.cs0 + J * a.cs1 + K] = avg8t(v);
+    }
+    return;
+  }
+  for (int e = t0; e < ncell; e += nt) {
+    int i, j, k;
+    cell(e, i, j, k);
+    P(i, j, k) = P(i, j, k) + a.c[(i >> 1) * a.cs0 + (j >> 1) * a.cs1 + (k >> 1)];
+  }
+  g.sync();
+  smooth();
+  // width-1 ghost layer of the grown box (valid cells are final)
+  const int E1 = n1 + 2, E2 = n2 + 2, ng = (int)(n0 + 2) * E1 * E2;
+  for (int e = t0; e < ng; e += nt) {
+    const int kk = (int)(e % E2) - 1;
+    const int q = e / E2;
+    const int jj = (int)(q % E1) - 1, ii = (int)(q / E1) - 1;
+    if (ii >= 0 && ii < n0 && jj >= 0 && jj < n1 && kk >= 0 && kk < n2) continue;
+    const int i = ii < 0 ? n0 - 1 : ii >= n0 ? 0 : ii;
+    const int j = jj < 0 ? n1 - 1 : jj >= n1 ? 0 : jj;
+    const int k = kk < 0 ? n2 - 1 : kk >= n2 ? 0 : kk;
+    p[ii * a.ps0 + jj * a.ps1 + kk] = P(i, j, k);
+  }
+}
+
 }  // namespace
 }  // namespace amrb
 
@@ -600,5 +713,62 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
     a.warp_from = nlev;  // block mode throughout (measured faster than one warp)
     launch_k(k_coarse_tail, 1, kTailThreads, bytes, (cudaStream_t)stream, a);
     check_launch("k_coarse_tail");
+  });
+}
+
+extern "C" int amrb_level_grid(int up, const int32_t* lohi, const double* dh, const amrb_field* rhs,
+                               const double* rhs_base, amrb_field* phi, double* phi_base, const amrb_field* crse,
+                               double* crse_base, int nsweeps, void* stream) {
+  return guarded([&] {
+    if (!lohi || !dh || !rhs || !phi || !crse || nsweeps < 0) throw Error(AMRB_EINVAL, "amrb_level_grid: bad arguments");
+    const Field& fr = *reinterpret_cast<const Field*>(rhs);
+    const Field& fp = *reinterpret_cast<const Field*>(phi);
+    const Field& fc = *reinterpret_cast<const Field*>(crse);
+    if (fr.host.size() != 1 || fp.host.size() != 1 || fc.host.size() != 1)
+      throw Error(AMRB_EINVAL, "amrb_level_grid needs single-box fields");
+    GridLevelArgs a;
+    std::memset(&a, 0, sizeof a);
+    int par = 0, n[3];
+    for (int x = 0; x < 3; ++x) {
+      n[x] = lohi[3 + x] - lohi[x] + 1;
+      par += lohi[x];
+      if (n[x] < 2 || n[x] % 2) throw Error(AMRB_EINVAL, "amrb_level_grid: extents must be even");
+      if (up && fp.ng3[x] < 1) throw Error(AMRB_EINVAL, "amrb_level_grid: phi needs a ghost layer");
+    }
+    a.n0 = n[0];
+    a.n1 = n[1];
+    a.n2 = n[2];
+    a.lo_par = par & 1;
+    a.nsw = nsweeps;
+    a.up = up;
+    a.cf = make_coef(dh);
+    const FabView &vr = fr.host[0], &vp = fp.host[0], &vc = fc.host[0];
+    const int64_t span = (int64_t)(n[0] + 2) * vp.s0 + (int64_t)(n[0] + 2) * vr.s0 + (int64_t)(n[0] / 2 + 2) * vc.s0;
+    if (span >= (int64_t)1 << 30) throw Error(AMRB_EINVAL, "amrb_level_grid: level too large");
+    a.phi = phi_base + vp.off;
+    a.ps0 = vp.s0;
+    a.ps1 = vp.s1;
+    a.rhs = rhs_base + vr.off;
+    a.rs0 = vr.s0;
+    a.rs1 = vr.s1;
+    a.c = crse_base + vc.off;
+    a.cs0 = vc.s0;
+    a.cs1 = vc.s1;
+    static int per_sm = 0;
+    if (!per_sm) {
+      AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_level_grid, 512, 0));
+      per_sm = per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms() * per_sm);
+    cfg.blockDim = dim3(512);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    AMRB_CUDA(cudaLaunchKernelEx(&cfg, k_level_grid, a));
+    check_launch("k_level_grid");
   });
 }

@@ -134,7 +134,8 @@ class MLMG:
     """
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
-                 ghost_push=False, agg_cells=128**3, fuse_prolong=None, cluster_tail=None):
+                 ghost_push=False, agg_cells=128**3, fuse_prolong=None, cluster_tail=None,
+                 grid_level_cells=None):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
         if not all(geom.periodic):
@@ -198,6 +199,24 @@ class MLMG:
                 if chain and len(top.ba) == 1 and (top.replicated or not self.dist):
                     self.tail = t - 1
                     self.cluster_tail = True
+        # single-box levels just above the tail, small enough to be launch-
+        # latency bound, run each half V-cycle as ONE grid-synchronised launch
+        # (amrb_level_grid: in-place sweeps with periodic index wrap, no fills)
+        # instead of ~7 fill / sweep / transfer launches
+        # (AMRB_GRID_LEVEL_CELLS: largest such level, 0 = off)
+        gmax = grid_level_cells if grid_level_cells is not None else int(
+            os.environ.get("AMRB_GRID_LEVEL_CELLS", str(64**3)))
+        self.grid_from = self.tail
+        for l in range(self.tail - 1, 0, -1) if self.tail < n else ():
+            lv, nx = self.levels[l], self.levels[l + 1]
+            ext = tuple(lv.domain.extents())
+            if (len(lv.ba) == 1 and len(nx.ba) == 1 and (lv.replicated or not self.dist)
+                    and lv.ncells <= gmax and all(e % 2 == 0 for e in ext)
+                    and tuple(nx.domain.extents()) == tuple(e // 2 for e in ext)):
+                self.grid_from = l
+                lv.lohi_c = i32p([*lv.domain.lo, *lv.domain.hi])
+            else:
+                break
         if self.tail < n:
             tl = self.levels[self.tail:]
             lohi = np.zeros((len(tl), 6), dtype=np.int32)
@@ -345,7 +364,7 @@ class MLMG:
         if not lv.boxlocal_next:
             self._gather_replica(lv, nx)
         self._produced(nx.rhs, 0)
-        if l + 1 != self.tail:  # the coarse tail reads valid rhs cells only
+        if l + 1 < self.grid_from:  # the coarse tail / grid levels read valid rhs cells only
             self._need_ghosts(nx, nx.rhs, 1)
 
     def _gather_replica(self, lv, nx):
@@ -450,11 +469,36 @@ class MLMG:
             )
         )
 
+    def _level_grid(self, l, up):
+        """Half V-cycle of grid level l in one launch (amrb_level_grid)."""
+        lv, nx = self.levels[l], self.levels[l + 1]
+        phi = lv.phi[lv.cur]
+        crse = nx.phi[nx.cur] if up else nx.rhs
+        check(
+            lib().amrb_level_grid(
+                int(up),
+                lv.lohi_c[1],
+                lv.dhc,
+                field_of(lv.rhs).handle,
+                C.c_void_p(lv.rhs.storage.data_ptr()),
+                field_of(phi).handle,
+                C.c_void_p(phi.storage.data_ptr()),
+                field_of(crse).handle,
+                C.c_void_p(crse.storage.data_ptr()),
+                self.nu2 if up else self.nu1,
+                stream_ptr(),
+            )
+        )
+        self._produced(phi, 1 if up else 0)
+        if not up:
+            self._produced(nx.rhs, 0)
+
     def vcycle(self):
         L = self.levels
         n = len(L)
         T = self.tail  # first level handled by the coarse-tail kernel (n: none)
-        for l in range(T):
+        G = self.grid_from  # first grid-synchronised level (T: none)
+        for l in range(G):
             lv = L[l]
             if l > 0:
                 _zero(lv.phi[lv.cur])
@@ -464,9 +508,13 @@ class MLMG:
                 break
             self._smooth(lv, self.nu1)
             self._resid_restrict(l)
+        for l in range(G, T):
+            self._level_grid(l, up=False)
         if T < n:
             self._coarse_tail()
-        for l in range(min(T, n - 1) - 1, -1, -1):
+        for l in range(T - 1, G - 1, -1):
+            self._level_grid(l, up=True)
+        for l in range(min(G, n - 1) - 1, -1, -1):
             if L[l].fuse and self._prolong_sweep(l):
                 self._smooth(L[l], self.nu2 - 1)
             else:

@@ -157,3 +157,28 @@ def test_cluster_tail_solve_identical(n, m):
         ref = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), tboxes(ba)).solve(rhs, rtol=1e-10, max_iter=100)
         assert out[0][0] == ref["iterations"] and out[0][1] == ref["history"]
         assert np.array_equal(out[0][2], ref["phi"])
+
+
+_REF = {}
+
+
+@pytest.mark.parametrize("ct,gcells", [(True, 64**3), (False, 64**3), (True, 0), (False, 128**3)])
+def test_grid_levels_solve_matches_oracle(ct, gcells):
+    """Small single-box levels as one grid-synchronised launch per half cycle
+    (amrb_level_grid), alone, chained (64^3 -> 32^3 above the one-CTA tail) and
+    off, with and without the cluster tail: same iterations, history and
+    bit-identical solution as the oracle (128^3, 64^3 boxes)."""
+    n, m = 128, 64
+    dom, ba, dm, geom, rhs = _problem(n, m, 11)
+    if "r128" not in _REF:  # one oracle solve (~11 s) shared by the cases
+        _REF["r128"] = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), tboxes(ba)).solve(rhs, rtol=1e-10, max_iter=100)
+    ref = _REF["r128"]
+    phi = A.MultiFab(ba, dm, 1, 1)
+    b = A.MultiFab(ba, dm, 1, 0)
+    b.load_valid_from(dom, rhs)
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), cluster_tail=ct, grid_level_cells=gcells)
+    ngrid = mg.tail - mg.grid_from
+    assert ngrid == (0 if gcells == 0 else (1 if ct else 2))
+    mg.solve(phi, b, rtol=1e-10, max_iter=100)
+    assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
+    assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
