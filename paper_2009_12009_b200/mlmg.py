@@ -205,7 +205,7 @@ class MLMG:
         # instead of ~7 fill / sweep / transfer launches
         # (AMRB_GRID_LEVEL_CELLS: largest such level, 0 = off)
         gmax = grid_level_cells if grid_level_cells is not None else int(
-            os.environ.get("AMRB_GRID_LEVEL_CELLS", str(64**3)))
+            os.environ.get("AMRB_GRID_LEVEL_CELLS", str(128**3 // 2)))
         self.grid_from = self.tail
         for l in range(self.tail - 1, 0, -1) if self.tail < n else ():
             lv, nx = self.levels[l], self.levels[l + 1]

@@ -182,3 +182,13 @@ def test_grid_levels_solve_matches_oracle(ct, gcells):
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
+
+
+def test_grid_and_cluster_levels_eager_equals_graph():
+    """The cooperative grid-level and cluster-tail launches behave the same
+    eagerly (PDL on the neighbouring launches) and inside the captured graph."""
+    dom, ba, dm, geom, rhs = _problem(128, 64, seed=13)
+    mg1, rn1, phi1 = _solve_device(dom, ba, dm, geom, rhs, use_graph=True)
+    mg2, rn2, phi2 = _solve_device(dom, ba, dm, geom, rhs, use_graph=False)
+    assert mg1.cluster_tail and mg1.tail > mg1.grid_from
+    assert mg1.history == mg2.history and np.array_equal(phi1, phi2)
