@@ -15,7 +15,9 @@
 // sequence (oracle/mlmg_ref.py) and to the device multi-kernel path.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 
 #include "stencil_common.cuh"
 
@@ -758,6 +760,8 @@ extern "C" int amrb_level_grid(int up, const int32_t* lohi, const double* dh, co
     if (!per_sm) {
       AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_level_grid, 512, 0));
       per_sm = per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm;
+      if (const char* e = getenv("AMRB_GRID_PER_SM"))  // A/B knob: CTAs per SM (grid.sync cost vs threads)
+        per_sm = std::max(1, std::min(per_sm, atoi(e)));
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms() * per_sm);
