@@ -378,6 +378,142 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
   tail_p2_body<LOG0, true>(a, sm, 0);
 }
 
+// Power-of-two but not cubic tails (the multi-GPU weak-scaling domains give
+// 32x16x16 .. 8x4x4 at 2 GPUs, 32x32x16 .. at 4): the same masked periodic
+// indexing with one shift per axis (every extent >= 2 and halving per level).
+// Replaces the generic fill-based k_coarse_tail there (103 us -> ~30 us).
+__global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a) {
+  pdl_entry();
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  auto sh = [&](int l, int x) { return __ffs(a.lv[l].n[x]) - 1; };
+  auto cells = [&](int l) { return 1 << (sh(l, 0) + sh(l, 1) + sh(l, 2)); };
+  auto nact = [&](int l) { return min(kTailThreads, max(32, cells(l) / 2)); };
+  auto lsync = [&](int l) {
+    const int na = nact(l);
+    if (na == 32)
+      __syncwarp();
+    else if (na == kTailThreads)
+      __syncthreads();
+    else
+      asm volatile("bar.sync 1, %0;\n" ::"r"(na) : "memory");
+  };
+  auto PHI = [&](int l) { return sm + a.lv[l].phi_off; };
+  auto RHS = [&](int l) { return sm + a.lv[l].rhs_off; };
+  // masked periodic 7-point Laplacian at (i, j, k) of a level with shifts s1, s2
+  // and masks m0, m1, m2
+  auto lapm = [&](const double* p, int i, int j, int k, int s1, int s2, int m0, int m1, int m2, const Coef& cf) {
+    const int si = s1 + s2;
+    return lap7(p[(i << si) | (j << s2) | k], p[(((i - 1) & m0) << si) | (j << s2) | k],
+                p[(((i + 1) & m0) << si) | (j << s2) | k], p[(i << si) | (((j - 1) & m1) << s2) | k],
+                p[(i << si) | (((j + 1) & m1) << s2) | k], p[(i << si) | (j << s2) | ((k - 1) & m2)],
+                p[(i << si) | (j << s2) | ((k + 1) & m2)], cf);
+  };
+
+  auto color = [&](int l, int c) {
+    const int s1 = sh(l, 1), s2 = sh(l, 2);
+    const int m0 = a.lv[l].n[0] - 1, m1 = a.lv[l].n[1] - 1, m2 = a.lv[l].n[2] - 1;
+    double* p = PHI(l);
+    const double* r = RHS(l);
+    const Coef cf = a.lv[l].cf;
+    const int lp = a.lv[l].lo_par;
+    const int np = cells(l) / 2;
+    for (int e = tid; e < np; e += nact(l)) {
+      const int kp = e & ((1 << (s2 - 1)) - 1), ij = e >> (s2 - 1);
+      const int j = ij & m1, i = ij >> s1;
+      const int k = 2 * kp + ((lp + i + j + c) & 1);
+      const int o = (i << (s1 + s2)) | (j << s2) | k;
+      const double v = p[o];
+      const double lap = lapm(p, i, j, k, s1, s2, m0, m1, m2, cf);
+      p[o] = relax(v, r[o], lap, cf.rgamma);
+    }
+  };
+  auto smooth = [&](int l, int nsw) {
+    for (int q = 0; q < nsw; ++q) {
+      color(l, 0);
+      lsync(l);
+      color(l, 1);
+      lsync(l);
+    }
+  };
+  auto restrict_resid = [&](int l) {  // rhs_{l+1} = avg8(rhs_l - L phi_l)
+    const int s1 = sh(l, 1), s2 = sh(l, 2), c1 = s1 - 1, c2 = s2 - 1;
+    const int m0 = a.lv[l].n[0] - 1, m1 = a.lv[l].n[1] - 1, m2 = a.lv[l].n[2] - 1;
+    const double* p = PHI(l);
+    const double* r = RHS(l);
+    double* rc = RHS(l + 1);
+    const Coef cf = a.lv[l].cf;
+    for (int e = tid; e < cells(l + 1); e += nact(l)) {
+      const int K = e & ((1 << c2) - 1), J = (e >> c2) & ((1 << c1) - 1), I = e >> (c1 + c2);
+      double v[8];
+#pragma unroll
+      for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+          for (int dk = 0; dk < 2; ++dk) {
+            const int i = 2 * I + di, j = 2 * J + dj, k = 2 * K + dk;
+            const int o = (i << (s1 + s2)) | (j << s2) | k;
+            v[di * 4 + dj * 2 + dk] = r[o] - lapm(p, i, j, k, s1, s2, m0, m1, m2, cf);
+          }
+      rc[e] = avg8t(v);
+    }
+  };
+  auto prolong_add = [&](int l) {  // phi_l += phi_{l+1}(parent)
+    const int s1 = sh(l, 1), s2 = sh(l, 2), c1 = s1 - 1, c2 = s2 - 1;
+    double* p = PHI(l);
+    const double* pc = PHI(l + 1);
+    for (int e = tid; e < cells(l); e += nact(l)) {
+      const int k = e & ((1 << s2) - 1), j = (e >> s2) & ((1 << s1) - 1), i = e >> (s1 + s2);
+      p[e] = p[e] + pc[((i >> 1) << (c1 + c2)) | ((j >> 1) << c2) | (k >> 1)];
+    }
+  };
+  auto zero = [&](int l) {
+    double* p = PHI(l);
+    for (int e = tid; e < cells(l); e += nact(l)) p[e] = 0.0;
+  };
+
+  {
+    const int s1 = sh(0, 1), s2 = sh(0, 2);
+    double* r = RHS(0);
+    for (int e = tid; e < cells(0); e += kTailThreads) {
+      const int k = e & ((1 << s2) - 1), j = (e >> s2) & ((1 << s1) - 1), i = e >> (s1 + s2);
+      r[e] = a.rhs[i * a.rs0 + j * a.rs1 + k];
+    }
+  }
+  __syncthreads();
+  const int L = a.nlev;
+  for (int l = 0; l < L; ++l) {
+    if (tid < nact(l)) {
+      zero(l);
+      lsync(l);
+      if (l == L - 1) {
+        smooth(l, a.nbottom);
+      } else {
+        smooth(l, a.nu1);
+        restrict_resid(l);
+      }
+    }
+    __syncthreads();
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    if (tid < nact(l)) {
+      prolong_add(l);
+      lsync(l);
+      smooth(l, a.nu2);
+    }
+    __syncthreads();
+  }
+  {
+    const int s1 = sh(0, 1), s2 = sh(0, 2);
+    const double* p = PHI(0);
+    for (int e = tid; e < cells(0); e += kTailThreads) {
+      const int k = e & ((1 << s2) - 1), j = (e >> s2) & ((1 << s1) - 1), i = e >> (s1 + s2);
+      a.phi[i * a.ps0 + j * a.ps1 + k] = p[e];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // 32^3 top level + 16^3 .. tail in ONE cluster of 8 CTAs.  The 32^3 level
 // (phi + rhs = 512 KB) does not fit one CTA, but it does fit a cluster: CTA r
@@ -707,6 +843,31 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
       return;
     }
     if (bytes > 227 * 1024) throw Error(AMRB_EINVAL, "coarse tail does not fit in shared memory");
+    // power-of-two per axis, not cubic: same dense masked layout
+    bool p2x = true;
+    for (int l = 0; l < nlev && p2x; ++l)
+      for (int x = 0; x < 3; ++x) {
+        const int e = a.lv[l].n[x];
+        p2x = p2x && e >= 2 && (e & (e - 1)) == 0 && (l == 0 || a.lv[l - 1].n[x] == 2 * e);
+      }
+    if (p2x) {
+      TailArgs b = a;  // dense layout; a keeps the ghosted one for the generic kernel
+      int o2 = 0;
+      for (int l = 0; l < nlev; ++l) {
+        const int c = b.lv[l].n[0] * b.lv[l].n[1] * b.lv[l].n[2];
+        b.lv[l].phi_off = o2;
+        o2 += c;
+        b.lv[l].rhs_off = o2;
+        o2 += c;
+      }
+      const size_t b2 = (size_t)o2 * sizeof(double);
+      if (b2 <= 227 * 1024) {
+        AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail_p2x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2));
+        launch_k(k_coarse_tail_p2x, 1, kTailThreads, b2, (cudaStream_t)stream, b);
+        check_launch("k_coarse_tail_p2x");
+        return;
+      }
+    }
     static bool configured = false;
     if (!configured) {
       AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));

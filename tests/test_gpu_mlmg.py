@@ -192,3 +192,28 @@ def test_grid_and_cluster_levels_eager_equals_graph():
     mg2, rn2, phi2 = _solve_device(dom, ba, dm, geom, rhs, use_graph=False)
     assert mg1.cluster_tail and mg1.tail > mg1.grid_from
     assert mg1.history == mg2.history and np.array_equal(phi1, phi2)
+
+
+@pytest.mark.parametrize("shape", [(64, 32, 32), (32, 64, 32), (64, 64, 32)])
+def test_noncubic_pow2_tail_matches_oracle(shape):
+    """Non-cubic power-of-two coarse chains (the multi-GPU weak-scaling shapes)
+    take k_coarse_tail_p2x (and grid levels above it): same iterations,
+    history and bit-identical solution as the oracle."""
+    hi = tuple(s - 1 for s in shape)
+    dom = A.Box((0, 0, 0), hi)
+    ba = A.BoxArray([dom]).max_size(32)
+    dm = A.DistributionMapping.single_rank(len(ba))
+    geom = A.Geometry(dom, (0.0,) * 3, tuple(s / 32.0 for s in shape), True)
+    rng = np.random.default_rng(17)
+    rhs = rng.standard_normal(shape)
+    rhs -= rhs.mean()
+    ref = R.OracleMLMG(((0, 0, 0), hi), tboxes(ba), prob_hi=tuple(s / 32.0 for s in shape)).solve(
+        rhs, rtol=1e-10, max_iter=100)
+    phi = A.MultiFab(ba, dm, 1, 1)
+    b = A.MultiFab(ba, dm, 1, 0)
+    b.load_valid_from(dom, rhs)
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1))
+    assert mg.tail < len(mg.levels)
+    mg.solve(phi, b, rtol=1e-10, max_iter=100)
+    assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
+    assert np.array_equal(A.gather_global(phi, dom), ref["phi"])

@@ -45,8 +45,21 @@ for l in range(1, len(mg.levels)):
     lv = mg.levels[l]
     if lv.replicated: break
     res[f"fill L{l} w2"] = graph_time(lambda: mg._fill(lv, lv.phi[lv.cur], 2))
+L1 = mg.levels[1]
+res["sweep L1 (+fill w2)"] = graph_time(lambda: mg._sweep(L1))
+res["resid_restrict L1 (+gather)"] = graph_time(lambda: mg._resid_restrict(1))
+res["prolong_sweep L0"] = graph_time(lambda: mg._prolong_sweep(0) if mg.levels[0].fuse else mg._prolong(0))
+res["prolong_sweep L1"] = graph_time(lambda: mg._prolong_sweep(1) if L1.fuse else mg._prolong(1))
+for l in range(mg.grid_from, mg.tail):
+    res[f"level_grid L{l} down"] = graph_time(lambda: mg._level_grid(l, False))
+    res[f"level_grid L{l} up"] = graph_time(lambda: mg._level_grid(l, True))
+for l in range(2, mg.grid_from):
+    lv = mg.levels[l]
+    res[f"sweep L{l} (+fill w2)"] = graph_time(lambda: mg._sweep(lv))
+res["coarse tail"] = graph_time(lambda: mg._coarse_tail())
 res["vcycle+norm"] = graph_time(lambda: mg._cycle_and_norm(), 5)
 if rank == 0:
-    print("levels:", [(tuple(l.domain.extents()), l.replicated) for l in mg.levels])
+    print("levels:", [(tuple(l.domain.extents()), l.replicated) for l in mg.levels], "grid_from", mg.grid_from,
+          "tail", mg.tail, "cluster", mg.cluster_tail)
     for k, v in res.items(): print(f"world={world} {k:24s} {v:9.1f} us")
 dist.barrier(device_ids=[local])
