@@ -32,6 +32,8 @@ convergence factor.
 
 from __future__ import annotations
 
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from . import mesh_ref as M
@@ -116,8 +118,14 @@ class OracleMLMG:
     """CPU V-cycle solver; data per level as mesh_ref dicts (ncomp = 1)."""
 
     def __init__(self, domain, boxes, prob_lo=(0.0, 0.0, 0.0), prob_hi=(1.0, 1.0, 1.0), nu1=2, nu2=2,
-                 bottom_sweeps=32):
+                 bottom_sweeps=32, threads=1):
+        """threads > 1 runs the per-box loops (GSRB colours, residuals, ghost
+        fills grouped by destination box) on a thread pool; numpy releases the
+        GIL inside the array ops and boxes of one phase are independent, so the
+        results are bit-identical to threads=1 (tests/test_oracle_mlmg.py)."""
         self.periodic = (True, True, True)
+        self.threads = max(1, int(threads))
+        self._pool = ThreadPoolExecutor(self.threads) if self.threads > 1 else None
         self.nu1, self.nu2, self.bottom_sweeps = nu1, nu2, bottom_sweeps
         self.levels = []
         for dom, bxs, kind in mg_levels(domain, boxes):
@@ -136,21 +144,49 @@ class OracleMLMG:
         self.cell_updates = 0
 
     # -- primitives ------------------------------------------------------------
+    def _map(self, fn, items):
+        items = list(items)
+        if self._pool is None or len(items) < 2:
+            return [fn(x) for x in items]
+        return list(self._pool.map(fn, items))
+
     def fill(self, lv):
-        M.execute(lv["fill"], lv["boxes"], lv["phi"], 1, lv["boxes"], lv["phi"], 1)
+        if self._pool is None:
+            M.execute(lv["fill"], lv["boxes"], lv["phi"], 1, lv["boxes"], lv["phi"], 1)
+            return
+        # a width-1 fill writes ghost cells only and reads valid cells only, so
+        # the two-phase staging of M.execute is not needed; records are applied
+        # per destination box in plan order.
+        by_dst = lv.get("fill_by_dst")
+        if by_dst is None:
+            by_dst = {}
+            for rec in lv["fill"]:
+                by_dst.setdefault(rec[1], []).append(rec)
+            lv["fill_by_dst"] = by_dst = list(by_dst.items())
+        bx, ph = lv["boxes"], lv["phi"]
+
+        def one(item):
+            j, recs = item
+            for i, _, ov, s in recs:
+                ph[j][(slice(None),) + M.region_index(bx[j], 1, M.shift(ov, s))] = \
+                    ph[i][(slice(None),) + M.region_index(bx[i], 1, ov)]
+
+        self._map(one, by_dst)
 
     def smooth(self, lv, n):
         for _ in range(n):
             for color in (0, 1):
                 self.fill(lv)
-                for i, b in enumerate(lv["boxes"]):
-                    gsrb_color(b, lv["phi"][i][0], lv["rhs"][i][0], lv["dh"], color)
+                self._map(lambda ib: gsrb_color(ib[1], lv["phi"][ib[0]][0], lv["rhs"][ib[0]][0], lv["dh"], color),
+                          enumerate(lv["boxes"]))
             self.sweeps += 1
             self.cell_updates += sum(int(np.prod(M.ext(b))) for b in lv["boxes"])
 
     def residual(self, lv):
         self.fill(lv)
-        return {i: (lv["rhs"][i][0] - laplacian(lv["phi"][i][0], lv["dh"]))[None] for i in range(len(lv["boxes"]))}
+        rs = self._map(lambda i: (lv["rhs"][i][0] - laplacian(lv["phi"][i][0], lv["dh"]))[None],
+                       range(len(lv["boxes"])))
+        return dict(enumerate(rs))
 
     def norm_inf(self, fabs, boxes):
         mx = M.reduce(boxes, fabs, 0, "max", 0)

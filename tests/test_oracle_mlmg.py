@@ -93,3 +93,20 @@ def test_hierarchy_levels():
     lv = R.mg_levels(dom, boxes)
     assert [M.ext(d)[0] for d, _, _ in lv] == [256, 128, 64, 32, 16, 8, 4]
     assert [k for _, _, k in lv] == ["base", "boxlocal", "boxlocal", "boxlocal", "boxlocal", "agglom", "single"]
+
+
+def test_threaded_oracle_is_bit_identical():
+    """The thread-pooled per-box loops (bench.py's reference arm) give the same
+    bits, iteration count and residual history as the serial oracle."""
+    n, m = 32, 8
+    rng = np.random.default_rng(5)
+    rhs = rng.standard_normal((n, n, n))
+    rhs -= rhs.mean()
+    boxes = [((i, j, k), (i + m - 1, j + m - 1, k + m - 1)) for i in range(0, n, m) for j in range(0, n, m)
+             for k in range(0, n, m)]
+    dom = ((0, 0, 0), (n - 1,) * 3)
+    a = R.OracleMLMG(dom, boxes).solve(rhs, rtol=1e-10, max_iter=40)
+    b = R.OracleMLMG(dom, boxes, threads=4).solve(rhs, rtol=1e-10, max_iter=40)
+    assert a["iterations"] == b["iterations"]
+    assert a["history"] == b["history"]
+    assert np.array_equal(a["phi"], b["phi"])
