@@ -573,7 +573,7 @@ def run_c5(args):
 
 def _c5_cpu_sample():
     """Oracle GSRB sweeps (fill, red, fill, black) on a 256^3 domain of C5's
-    32^3 boxes, 1 core (a few seconds)."""
+    32^3 boxes, colour updates on every host thread (a few seconds)."""
     from oracle import mesh_ref as M
     from oracle import mlmg_ref as R
 
@@ -588,17 +588,20 @@ def _c5_cpu_sample():
         f[...] = rng.standard_normal(f.shape)
     recs = M.fill_records(boxes, 1, dom, (True, True, True))
     dh = (512.0 * 512.0,) * 3
+    from concurrent.futures import ThreadPoolExecutor
+
+    threads = os.cpu_count() or 1
     t0 = time.perf_counter()
     sweeps = 2
-    for _ in range(sweeps):
-        for color in (0, 1):
-            M.execute(recs, boxes, phi, 1, boxes, phi, 1)
-            for i, b in enumerate(boxes):
-                R.gsrb_color(b, phi[i][0], rhs[i][0], dh, color)
+    with ThreadPoolExecutor(threads) as pool:
+        for _ in range(sweeps):
+            for color in (0, 1):
+                M.execute(recs, boxes, phi, 1, boxes, phi, 1)
+                list(pool.map(lambda i: R.gsrb_color(boxes[i], phi[i][0], rhs[i][0], dh, color), range(len(boxes))))
     dt = time.perf_counter() - t0
-    return {"value": sweeps * n ** 3 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+    return {"value": sweeps * n ** 3 / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{sweeps} oracle GSRB sweeps (fill, red, fill, black) over 256^3 in 512 boxes of 32^3 "
-                      f"({dt:.1f} s)"}
+                      f"({dt:.1f} s; per-box colour updates on {threads} threads, fills serial)"}
 
 
 def main():
