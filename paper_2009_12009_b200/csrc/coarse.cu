@@ -382,11 +382,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2(TailArgs a) 
 // 32x16x16 .. 8x4x4 at 2 GPUs, 32x32x16 .. at 4): the same masked periodic
 // indexing with one shift per axis (every extent >= 2 and halving per level).
 // Replaces the generic fill-based k_coarse_tail there (103 us -> ~30 us).
-__global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a) {
-  pdl_entry();
-  extern __shared__ __align__(16) double sm[];
+// GIO / base as for tail_p2_body.
+template <bool GIO>
+__device__ __forceinline__ void tail_p2x_body(const TailArgs& a, double* sm, int base) {
   const int tid = threadIdx.x;
-  auto sh = [&](int l, int x) { return __ffs(a.lv[l].n[x]) - 1; };
+  auto sh = [&](int l, int x) { return __ffs(a.lv[base + l].n[x]) - 1; };
   auto cells = [&](int l) { return 1 << (sh(l, 0) + sh(l, 1) + sh(l, 2)); };
   auto nact = [&](int l) { return min(kTailThreads, max(32, cells(l) / 2)); };
   auto lsync = [&](int l) {
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
     else
       asm volatile("bar.sync 1, %0;\n" ::"r"(na) : "memory");
   };
-  auto PHI = [&](int l) { return sm + a.lv[l].phi_off; };
-  auto RHS = [&](int l) { return sm + a.lv[l].rhs_off; };
+  auto PHI = [&](int l) { return sm + a.lv[base + l].phi_off; };
+  auto RHS = [&](int l) { return sm + a.lv[base + l].rhs_off; };
   // masked periodic 7-point Laplacian at (i, j, k) of a level with shifts s1, s2
   // and masks m0, m1, m2
   auto lapm = [&](const double* p, int i, int j, int k, int s1, int s2, int m0, int m1, int m2, const Coef& cf) {
@@ -412,11 +412,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
 
   auto color = [&](int l, int c) {
     const int s1 = sh(l, 1), s2 = sh(l, 2);
-    const int m0 = a.lv[l].n[0] - 1, m1 = a.lv[l].n[1] - 1, m2 = a.lv[l].n[2] - 1;
+    const int m0 = a.lv[base + l].n[0] - 1, m1 = a.lv[base + l].n[1] - 1, m2 = a.lv[base + l].n[2] - 1;
     double* p = PHI(l);
     const double* r = RHS(l);
-    const Coef cf = a.lv[l].cf;
-    const int lp = a.lv[l].lo_par;
+    const Coef cf = a.lv[base + l].cf;
+    const int lp = a.lv[base + l].lo_par;
     const int np = cells(l) / 2;
     for (int e = tid; e < np; e += nact(l)) {
       const int kp = e & ((1 << (s2 - 1)) - 1), ij = e >> (s2 - 1);
@@ -438,11 +438,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
   };
   auto restrict_resid = [&](int l) {  // rhs_{l+1} = avg8(rhs_l - L phi_l)
     const int s1 = sh(l, 1), s2 = sh(l, 2), c1 = s1 - 1, c2 = s2 - 1;
-    const int m0 = a.lv[l].n[0] - 1, m1 = a.lv[l].n[1] - 1, m2 = a.lv[l].n[2] - 1;
+    const int m0 = a.lv[base + l].n[0] - 1, m1 = a.lv[base + l].n[1] - 1, m2 = a.lv[base + l].n[2] - 1;
     const double* p = PHI(l);
     const double* r = RHS(l);
     double* rc = RHS(l + 1);
-    const Coef cf = a.lv[l].cf;
+    const Coef cf = a.lv[base + l].cf;
     for (int e = tid; e < cells(l + 1); e += nact(l)) {
       const int K = e & ((1 << c2) - 1), J = (e >> c2) & ((1 << c1) - 1), I = e >> (c1 + c2);
       double v[8];
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
     for (int e = tid; e < cells(l); e += nact(l)) p[e] = 0.0;
   };
 
-  {
+  if (GIO) {
     const int s1 = sh(0, 1), s2 = sh(0, 2);
     double* r = RHS(0);
     for (int e = tid; e < cells(0); e += kTailThreads) {
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
     }
   }
   __syncthreads();
-  const int L = a.nlev;
+  const int L = a.nlev - base;
   for (int l = 0; l < L; ++l) {
     if (tid < nact(l)) {
       zero(l);
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
     }
     __syncthreads();
   }
-  {
+  if (GIO) {
     const int s1 = sh(0, 1), s2 = sh(0, 2);
     const double* p = PHI(0);
     for (int e = tid; e < cells(0); e += kTailThreads) {
@@ -512,6 +512,12 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
       a.phi[i * a.ps0 + j * a.ps1 + k] = p[e];
     }
   }
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a) {
+  pdl_entry();
+  extern __shared__ __align__(16) double sm[];
+  tail_p2x_body<true>(a, sm, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -529,45 +535,53 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
 // operand order as every other path: bit-identical results.
 // ---------------------------------------------------------------------------
 constexpr int kClCtas = 8;
-constexpr int kClN = 32;                  // top-level extent
+constexpr int kClN = 32;                  // top-level extent along i
 constexpr int kClPl = kClN / kClCtas;     // planes per CTA
-constexpr int kClSlab = kClPl * kClN * kClN;
+constexpr int kClSlab = kClPl * kClN * kClN;  // largest slab (32 x 32 planes)
 
+// The top level may also be 32 x n1 x n2 with n1, n2 powers of two <= 32 (the
+// multi-GPU weak-scaling chains 32x16x16 .. and 32x32x16 ..): planes are
+// n1 x n2, indexed with shifts s1, s2; CTA 0 then runs the non-cubic chain
+// body (tail_p2x_body) on the levels below.
 __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 1)
-    k_coarse_tail_cl(TailArgs a, int slab_off) {
+    k_coarse_tail_cl(TailArgs a, int slab_off, int cubic) {
   pdl_entry();
   extern __shared__ __align__(16) double sm[];
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
   const int tid = threadIdx.x;
-  constexpr int M = kClN - 1;
-  double* p = sm + slab_off;  // phi [kClPl][32][32]
-  double* rh = p + kClSlab;   // rhs, same shape
-  const double* pm = cl.map_shared_rank(p, (r + kClCtas - 1) % kClCtas) + (kClPl - 1) * kClN * kClN;  // plane 4r-1
-  const double* pp = cl.map_shared_rank(p, (r + 1) % kClCtas);                                        // plane 4r+4
   const TailLevel& L = a.lv[0];
+  const int s1 = __ffs(L.n[1]) - 1, s2 = __ffs(L.n[2]) - 1, si = s1 + s2;
+  const int m1 = L.n[1] - 1, m2 = L.n[2] - 1;
+  const int c1 = s1 - 1, c2 = s2 - 1;  // next level's shifts
+  const int plane = 1 << si, slab = kClPl << si;
+  double* p = sm + slab_off;  // phi [kClPl][n1][n2]
+  double* rh = p + slab;      // rhs, same shape
+  const double* pm = cl.map_shared_rank(p, (r + kClCtas - 1) % kClCtas) + (kClPl - 1) * plane;  // plane 4r-1
+  const double* pp = cl.map_shared_rank(p, (r + 1) % kClCtas);                                   // plane 4r+4
   const Coef cf = L.cf;
   const int i0 = kClPl * r;
 
-  for (int e = tid; e < kClSlab; e += kTailThreads) {
-    const int k = e & M, j = (e >> 5) & M, li = e >> 10;
+  for (int e = tid; e < slab; e += kTailThreads) {
+    const int k = e & m2, j = (e >> s2) & m1, li = e >> si;
     rh[e] = a.rhs[(int64_t)(i0 + li) * a.rs0 + (int64_t)j * a.rs1 + k];
     p[e] = 0.0;
   }
   cl.sync();
 
+  auto at = [&](int li, int j, int k) { return p[(li << si) | (j << s2) | k]; };
   auto color = [&](int c) {
-    for (int e = tid; e < kClSlab / 2; e += kTailThreads) {
-      const int kp = e & 15, j = (e >> 4) & M, li = e >> 9;
+    for (int e = tid; e < slab / 2; e += kTailThreads) {
+      const int kp = e & ((1 << c2) - 1), j = (e >> c2) & m1, li = e >> (si - 1);
       const int k = 2 * kp + ((L.lo_par + i0 + li + j + c) & 1);
-      const int jk = (j << 5) | k;
-      const int o = (li << 10) | jk;
+      const int jk = (j << s2) | k;
+      const int o = (li << si) | jk;
       const double v = p[o];
-      const double xm = li > 0 ? p[o - kClN * kClN] : pm[jk];
-      const double xp = li < kClPl - 1 ? p[o + kClN * kClN] : pp[jk];
-      const double lap = lap7(v, xm, xp, p[(li << 10) | (((j - 1) & M) << 5) | k], p[(li << 10) | (((j + 1) & M) << 5) | k],
-                              p[(li << 10) | (j << 5) | ((k - 1) & M)], p[(li << 10) | (j << 5) | ((k + 1) & M)], cf);
+      const double xm = li > 0 ? p[o - plane] : pm[jk];
+      const double xp = li < kClPl - 1 ? p[o + plane] : pp[jk];
+      const double lap = lap7(v, xm, xp, at(li, (j - 1) & m1, k), at(li, (j + 1) & m1, k), at(li, j, (k - 1) & m2),
+                              at(li, j, (k + 1) & m2), cf);
       p[o] = relax(v, rh[o], lap, cf.rgamma);
     }
   };
@@ -581,10 +595,10 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
   };
 
   smooth(a.nu1);
-  {  // rhs_16 = avg8(rhs_32 - L phi_32), coarse planes [2r, 2r+2), into CTA 0
+  {  // rhs_c = avg8(rhs - L phi), coarse planes [2r, 2r+2), into CTA 0
     double* rc = cl.map_shared_rank(sm + a.lv[1].rhs_off, 0);
-    for (int e = tid; e < kClSlab / 8; e += kTailThreads) {
-      const int K = e & 15, J = (e >> 4) & 15, dI = e >> 8;
+    for (int e = tid; e < slab / 8; e += kTailThreads) {
+      const int K = e & ((1 << c2) - 1), J = (e >> c2) & ((1 << c1) - 1), dI = e >> (c1 + c2);
       double v[8];
 #pragma unroll
       for (int di = 0; di < 2; ++di)
@@ -593,44 +607,46 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
 #pragma unroll
           for (int dk = 0; dk < 2; ++dk) {
             const int li = 2 * dI + di, j = 2 * J + dj, k = 2 * K + dk;
-            const int jk = (j << 5) | k;
-            const int o = (li << 10) | jk;
-            const double xm = li > 0 ? p[o - kClN * kClN] : pm[jk];
-            const double xp = li < kClPl - 1 ? p[o + kClN * kClN] : pp[jk];
-            v[di * 4 + dj * 2 + dk] =
-                rh[o] - lap7(p[o], xm, xp, p[(li << 10) | (((j - 1) & M) << 5) | k],
-                             p[(li << 10) | (((j + 1) & M) << 5) | k], p[(li << 10) | (j << 5) | ((k - 1) & M)],
-                             p[(li << 10) | (j << 5) | ((k + 1) & M)], cf);
+            const int jk = (j << s2) | k;
+            const int o = (li << si) | jk;
+            const double xm = li > 0 ? p[o - plane] : pm[jk];
+            const double xp = li < kClPl - 1 ? p[o + plane] : pp[jk];
+            v[di * 4 + dj * 2 + dk] = rh[o] - lap7(p[o], xm, xp, at(li, (j - 1) & m1, k), at(li, (j + 1) & m1, k),
+                                                   at(li, j, (k - 1) & m2), at(li, j, (k + 1) & m2), cf);
           }
-      rc[((i0 / 2 + dI) << 8) | (J << 4) | K] = avg8t(v);
+      rc[((i0 / 2 + dI) << (c1 + c2)) | (J << c2) | K] = avg8t(v);
     }
   }
   cl.sync();
-  if (r == 0) tail_p2_body<4, false>(a, sm, 1);
+  if (r == 0) {
+    if (cubic)
+      tail_p2_body<4, false>(a, sm, 1);
+    else
+      tail_p2x_body<false>(a, sm, 1);
+  }
   cl.sync();
-  {  // phi_32 += phi_16(parent), from CTA 0
+  {  // phi += phi_c(parent), from CTA 0
     const double* pc = cl.map_shared_rank(sm + a.lv[1].phi_off, 0);
-    for (int e = tid; e < kClSlab; e += kTailThreads) {
-      const int k = e & M, j = (e >> 5) & M, li = e >> 10;
-      p[e] = p[e] + pc[(((i0 + li) >> 1) << 8) | ((j >> 1) << 4) | (k >> 1)];
+    for (int e = tid; e < slab; e += kTailThreads) {
+      const int k = e & m2, j = (e >> s2) & m1, li = e >> si;
+      p[e] = p[e] + pc[(((i0 + li) >> 1) << (c1 + c2)) | ((j >> 1) << c2) | (k >> 1)];
     }
   }
   cl.sync();
   smooth(a.nu2);
   // valid cells + the width-1 periodic ghost layer (the full grown box, as a
   // width-1 FillBoundary of a single periodic box writes it)
-  constexpr int E = kClN + 2;
-  for (int e = tid; e < kClPl * E * E; e += kTailThreads) {
-    const int kk = e % E, jj = (e / E) % E, li = e / (E * E);
+  const int E1 = L.n[1] + 2, E2 = L.n[2] + 2;
+  for (int e = tid; e < kClPl * E1 * E2; e += kTailThreads) {
+    const int kk = e % E2, jj = (e / E2) % E1, li = e / (E1 * E2);
     const int j = jj - 1, k = kk - 1;
-    const double v = p[(li << 10) | ((j & M) << 5) | (k & M)];
+    const double v = at(li, j & m1, k & m2);
     const int64_t jko = (int64_t)j * a.ps1 + k;
     a.phi[(int64_t)(i0 + li) * a.ps0 + jko] = v;
     if (i0 + li == 0) a.phi[(int64_t)kClN * a.ps0 + jko] = v;
     if (i0 + li == kClN - 1) a.phi[-a.ps0 + jko] = v;
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // One small single-box periodic level's half of the V-cycle in ONE grid-
@@ -802,25 +818,42 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
     // power-of-two cubic chain (each level >= 4 per side except possibly the
     // bottom, which must be >= 2): dense layout, masked periodic indexing
     const int n0 = a.lv[0].n[0];
-    bool cl = n0 == kClN && nlev >= 2 && (n0 >> (nlev - 1)) >= 2 && fp.ng3[0] >= 1 &&
-              fp.ng3[1] >= 1 && fp.ng3[2] >= 1;
+    // 32 x n1 x n2 top level (n1, n2 powers of two <= 32) halving per level
+    // down to extents >= 2: the top level on a cluster, the chain below in CTA 0
+    // (AMRB_CLUSTER_TAIL=0 keeps the one-CTA kernels, for A/B runs).  Default:
+    // cubic chains only -- the non-cubic top levels (AMRB_CLUSTER_TAIL=2) are
+    // bit-identical but measured slower than k_coarse_tail_p2x (C4 weak
+    // scaling, 2 GPUs 10.18 -> 10.35 ms, 4 GPUs 10.99 -> 11.02 ms)
+    static const int cl_mode = getenv("AMRB_CLUSTER_TAIL") ? atoi(getenv("AMRB_CLUSTER_TAIL")) : 1;
+    bool cl = cl_mode != 0 && n0 == kClN && nlev >= 2 && fp.ng3[0] >= 1 && fp.ng3[1] >= 1 && fp.ng3[2] >= 1;
     for (int l = 0; l < nlev && cl; ++l)
-      cl = a.lv[l].n[0] == (n0 >> l) && a.lv[l].n[1] == (n0 >> l) && a.lv[l].n[2] == (n0 >> l);
-    if (cl) {  // 32^3 top level on a cluster, the 16^3 .. chain in CTA 0
+      for (int x = 0; x < 3; ++x) {
+        const int e = a.lv[l].n[x];
+        cl = cl && e >= 2 && e <= kClN && (e & (e - 1)) == 0 && (l == 0 || a.lv[l - 1].n[x] == 2 * e);
+      }
+    if (cl && cl_mode < 2)
+      for (int l = 0; l < nlev && cl; ++l) cl = a.lv[l].n[1] == a.lv[l].n[0] && a.lv[l].n[2] == a.lv[l].n[0];
+    if (cl) {
+      bool cubic = true;
       int o2 = 0;
       for (int l = 1; l < nlev; ++l) {
-        const int c = (n0 >> l) * (n0 >> l) * (n0 >> l);
+        const int c = a.lv[l].n[0] * a.lv[l].n[1] * a.lv[l].n[2];
+        cubic = cubic && a.lv[l].n[0] == a.lv[l].n[1] && a.lv[l].n[1] == a.lv[l].n[2];
         a.lv[l].phi_off = o2;
         o2 += c;
         a.lv[l].rhs_off = o2;
         o2 += c;
       }
+      cubic = cubic && a.lv[1].n[0] == 16;  // tail_p2_body<4>: a 16^3 .. chain
       const int slab_off = (o2 + 15) & ~15;
-      const size_t b2 = (size_t)(slab_off + 2 * kClSlab) * sizeof(double);
-      AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2));
-      launch_k(k_coarse_tail_cl, kClCtas, kTailThreads, b2, (cudaStream_t)stream, a, slab_off);
-      check_launch("k_coarse_tail_cl");
-      return;
+      const int slab = kClPl * a.lv[0].n[1] * a.lv[0].n[2];
+      const size_t b2 = (size_t)(slab_off + 2 * slab) * sizeof(double);
+      if (b2 <= 227 * 1024) {
+        AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        launch_k(k_coarse_tail_cl, kClCtas, kTailThreads, b2, (cudaStream_t)stream, a, slab_off, cubic ? 1 : 0);
+        check_launch("k_coarse_tail_cl");
+        return;
+      }
     }
     bool p2 = n0 >= 2 && n0 <= 16 && (n0 & (n0 - 1)) == 0 && (n0 >> (nlev - 1)) >= 2;
     for (int l = 0; l < nlev && p2; ++l)

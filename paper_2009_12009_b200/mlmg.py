@@ -189,14 +189,26 @@ class MLMG:
         # a 32^3 single-box level above a 16^3 .. tail joins it: the cluster
         # variant of the tail kernel (8 CTAs, the 32^3 level split in slabs
         # across their shared memory) runs it too (AMRB_CLUSTER_TAIL=0: off)
+        # (AMRB_CLUSTER_TAIL=2: 32 x n1 x n2 levels too, n1, n2 powers of two
+        # <= 32, the multi-GPU weak-scaling chains 32x16x16 .. and 32x32x16 ..;
+        # bit-identical but measured slower than the one-CTA non-cubic tail,
+        # DESIGN.md §6; libamrb picks the cluster kernel from the same shape test)
         self.cluster_tail = False
+        noncubic = os.environ.get("AMRB_CLUSTER_TAIL", "1") == "2"
+
+        def _cl_chain(t0):
+            ext = [tuple(self.levels[x].domain.extents()) for x in range(t0, n)]
+            return (len(ext) >= 2 and ext[0][0] == 32 and (noncubic or all(e[0] == e[1] == e[2] for e in ext))
+                    and all(2 <= e <= 32 and e & (e - 1) == 0 for es in ext for e in es)
+                    and all(ext[x][d] == 2 * ext[x + 1][d] for x in range(len(ext) - 1) for d in range(3)))
+
         if (cluster_tail is None and os.environ.get("AMRB_CLUSTER_TAIL", "1") != "0") or cluster_tail:
             t = self.tail
-            if 1 < t < n and n - t + 1 <= 8:
+            if 0 < t < n and _cl_chain(t):
+                self.cluster_tail = True
+            elif 1 < t < n and n - t + 1 <= 8:
                 top = self.levels[t - 1]
-                ext = [tuple(self.levels[x].domain.extents()) for x in range(t - 1, n)]
-                chain = all(e == (32 >> x,) * 3 for x, e in enumerate(ext)) and ext[-1][0] >= 2
-                if chain and len(top.ba) == 1 and (top.replicated or not self.dist):
+                if _cl_chain(t - 1) and len(top.ba) == 1 and (top.replicated or not self.dist):
                     self.tail = t - 1
                     self.cluster_tail = True
         # single-box levels just above the tail, small enough to be launch-

@@ -1,6 +1,8 @@
 """MLMG solve on the device vs the oracle V-cycle: same iteration count, same
 residual history and bit-identical solution."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -197,7 +199,8 @@ def test_grid_and_cluster_levels_eager_equals_graph():
 @pytest.mark.parametrize("shape", [(64, 32, 32), (32, 64, 32), (64, 64, 32)])
 def test_noncubic_pow2_tail_matches_oracle(shape):
     """Non-cubic power-of-two coarse chains (the multi-GPU weak-scaling shapes)
-    take k_coarse_tail_p2x (and grid levels above it): same iterations,
+    take k_coarse_tail_p2x (or, with AMRB_CLUSTER_TAIL=2, k_coarse_tail_cl for
+    a 32 x n1 x n2 top level) and grid levels above: same iterations,
     history and bit-identical solution as the oracle."""
     hi = tuple(s - 1 for s in shape)
     dom = A.Box((0, 0, 0), hi)
@@ -214,6 +217,8 @@ def test_noncubic_pow2_tail_matches_oracle(shape):
     b.load_valid_from(dom, rhs)
     mg = A.MLMG(geom, ba, dm, transport=A.Transport(1))
     assert mg.tail < len(mg.levels)
+    # the non-cubic cluster tail is opt-in (AMRB_CLUSTER_TAIL=2)
+    assert mg.cluster_tail == (os.environ.get("AMRB_CLUSTER_TAIL") == "2" and shape[0] == 64)
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
