@@ -543,6 +543,8 @@ constexpr int kClSlab = kClPl * kClN * kClN;  // largest slab (32 x 32 planes)
 // multi-GPU weak-scaling chains 32x16x16 .. and 32x32x16 ..): planes are
 // n1 x n2, indexed with shifts s1, s2; CTA 0 then runs the non-cubic chain
 // body (tail_p2x_body) on the levels below.
+// CUBIC: 32^3 top level with compile-time plane shifts (the default path).
+template <bool CUBIC>
 __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 1)
     k_coarse_tail_cl(TailArgs a, int slab_off, int cubic) {
   pdl_entry();
@@ -552,8 +554,8 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
   const int r = (int)cl.block_rank();
   const int tid = threadIdx.x;
   const TailLevel& L = a.lv[0];
-  const int s1 = __ffs(L.n[1]) - 1, s2 = __ffs(L.n[2]) - 1, si = s1 + s2;
-  const int m1 = L.n[1] - 1, m2 = L.n[2] - 1;
+  const int s1 = CUBIC ? 5 : __ffs(L.n[1]) - 1, s2 = CUBIC ? 5 : __ffs(L.n[2]) - 1, si = s1 + s2;
+  const int m1 = (1 << s1) - 1, m2 = (1 << s2) - 1;
   const int c1 = s1 - 1, c2 = s2 - 1;  // next level's shifts
   const int plane = 1 << si, slab = kClPl << si;
   double* p = sm + slab_off;  // phi [kClPl][n1][n2]
@@ -619,7 +621,7 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
   }
   cl.sync();
   if (r == 0) {
-    if (cubic)
+    if (CUBIC || cubic)
       tail_p2_body<4, false>(a, sm, 1);
     else
       tail_p2x_body<false>(a, sm, 1);
@@ -636,7 +638,7 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
   smooth(a.nu2);
   // valid cells + the width-1 periodic ghost layer (the full grown box, as a
   // width-1 FillBoundary of a single periodic box writes it)
-  const int E1 = L.n[1] + 2, E2 = L.n[2] + 2;
+  const int E1 = m1 + 3, E2 = m2 + 3;
   for (int e = tid; e < kClPl * E1 * E2; e += kTailThreads) {
     const int kk = e % E2, jj = (e / E2) % E1, li = e / (E1 * E2);
     const int j = jj - 1, k = kk - 1;
@@ -849,8 +851,10 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
       const int slab = kClPl * a.lv[0].n[1] * a.lv[0].n[2];
       const size_t b2 = (size_t)(slab_off + 2 * slab) * sizeof(double);
       if (b2 <= 227 * 1024) {
-        AMRB_CUDA(cudaFuncSetAttribute(k_coarse_tail_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        launch_k(k_coarse_tail_cl, kClCtas, kTailThreads, b2, (cudaStream_t)stream, a, slab_off, cubic ? 1 : 0);
+        const bool top_cubic = a.lv[0].n[1] == kClN && a.lv[0].n[2] == kClN;
+        auto kern = top_cubic && cubic ? k_coarse_tail_cl<true> : k_coarse_tail_cl<false>;
+        AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        launch_k(kern, kClCtas, kTailThreads, b2, (cudaStream_t)stream, a, slab_off, cubic ? 1 : 0);
         check_launch("k_coarse_tail_cl");
         return;
       }
