@@ -537,7 +537,6 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_coarse_tail_p2x(TailArgs a)
 constexpr int kClCtas = 8;
 constexpr int kClN = 32;                  // top-level extent along i
 constexpr int kClPl = kClN / kClCtas;     // planes per CTA
-constexpr int kClSlab = kClPl * kClN * kClN;  // largest slab (32 x 32 planes)
 
 // The top level may also be 32 x n1 x n2 with n1, n2 powers of two <= 32 (the
 // multi-GPU weak-scaling chains 32x16x16 .. and 32x32x16 ..): planes are
