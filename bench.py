@@ -20,6 +20,7 @@ problem per step.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -29,6 +30,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from golden.make_mlmg_golden import headline_rhs  # noqa: E402  (the synthetic-input recipe, numpy only)
 
 METRIC = "fp64 cell-updates/s (GSRB, %HBM roofline); MLMG 256^3 solve time @1/2/4/8 GPU"
 UNIT = "cell-updates/s"
@@ -46,6 +49,11 @@ def _traffic(alg_bytes):
     except (OSError, ValueError, KeyError):
         pass
     return None
+
+
+def _golden_iterations(case):
+    with open(os.path.join(ROOT, "tests", "golden", "mlmg_golden.json")) as f:
+        return json.load(f)[case]["iterations"]
 
 
 def _peaks():
@@ -135,9 +143,7 @@ def run_reference(args):
     n, m = 256, 64
     boxes = [((i, j, k), (i + m - 1, j + m - 1, k + m - 1)) for i in range(0, n, m) for j in range(0, n, m)
              for k in range(0, n, m)]
-    rng = np.random.default_rng(2)
-    rhs = rng.standard_normal((n, n, n))
-    rhs -= rhs.mean()
+    rhs = headline_rhs(n, 2)
     threads = os.cpu_count() or 1
     s = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), boxes, threads=threads)
     times = []
@@ -172,9 +178,7 @@ def cpu_baseline_sample():
     n, m = 256, 64
     boxes = [((i, j, k), (i + m - 1, j + m - 1, k + m - 1)) for i in range(0, n, m) for j in range(0, n, m)
              for k in range(0, n, m)]
-    rng = np.random.default_rng(2)
-    rhs = rng.standard_normal((n, n, n))
-    rhs -= rhs.mean()
+    rhs = headline_rhs(n, 2)
     threads = os.cpu_count() or 1
     s = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), boxes, threads=threads)
     t0 = time.perf_counter()
@@ -210,18 +214,14 @@ def run_ours(args):
     # (dx = 1/256 in every direction at every GPU count)
     geom = A.Geometry(dom, (0.0,) * 3, tuple(e / 256.0 for e in ext), True)
 
-    # synthetic rhs: per-box seeded normals on device, centred globally
+    # synthetic rhs: SURVEY 8(d)'s recipe, the same numpy bits the reference arm
+    # and the golden oracle solve (tests/golden/make_mlmg_golden.py): seeded
+    # standard normals over the global domain, host-centred (C3 seed 2, C4 seed 3)
+    rhs_np = headline_rhs(ext, 2 if world == 1 else 3)
     rhs = A.MultiFab(ba, dm, 1, 0)
-    gen = torch.Generator(device="cuda")
-    for i, f in rhs.fabs.items():
-        gen.manual_seed(1000003 * (2 if world == 1 else 3) + i)
-        f.valid().copy_(torch.randn(tuple(f.valid().shape), generator=gen, device="cuda", dtype=torch.float64))
-    tot = torch.tensor([A.device_reduce(rhs, "sum").item()], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tot)
-    mean = tot.item() / dom.num_cells()
-    for f in rhs.fabs.values():
-        f.valid().sub_(mean)
+    rhs.load_valid_from(dom, rhs_np)
+    rhs_sha = hashlib.sha256(rhs_np.tobytes()).hexdigest()
+    del rhs_np
     phi = A.MultiFab(ba, dm, 1, 1)
     mg = A.MLMG(geom, ba, dm, transport=tr)
 
@@ -393,6 +393,10 @@ def run_ours(args):
                              f"C4 weak-scaling MLMG Poisson {ext[0]}x{ext[1]}x{ext[2]} (256^3 per GPU), 64^3 boxes"),
                 "domain": list(ext), "box": 64, "boxes": len(ba), "levels": len(mg.levels), "cycle": "V(2,2)",
                 "bottom_sweeps": mg.bottom_sweeps, "rtol": 1e-10, "iterations": iters,
+                "rhs": "np.random.default_rng(%d).standard_normal over the global domain, host-centred "
+                       "(sha256 %s...)" % (2 if world == 1 else 3, rhs_sha[:16]),
+                # the CPU oracle's iteration count on the same rhs bits (tests/golden/mlmg_golden.json)
+                "oracle_iterations": _golden_iterations("c3") if world == 1 else None,
                 "mlmg_solve_ms": ms, "global_batch": 1, "seq_len": dom.num_cells(),
                 "parallelism": f"dp{world} (boxes by Morton SFC)",
                 "l2": "working set (phi x2 + rhs, 256^3 fp64 per GPU = 0.4 GB) exceeds the 126 MB L2",

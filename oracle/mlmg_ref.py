@@ -114,16 +114,77 @@ def gsrb_color(box, p, rhs_valid, dh, color):
     np.copyto(c, new, where=color_mask(box[0], c.shape, color))
 
 
+def reflect_alpha(level):
+    """Coarse-level homogeneous Dirichlet factor: ghost = -alpha * mirror."""
+    r = float(1 << level)
+    return (r - 1.0) / (r + 1.0)
+
+
+def reflect_ghosts(boxes, fabs, ngrow, domain, lo_conds, hi_conds, alpha):
+    """Every ghost cell outside an 'external' face (ghost layer t = 1..ngrow)
+    <- -alpha * the valid cell mirrored across that face (layer t-1 inside),
+    one (axis, side) at a time in the order of apply_domain_boundary
+    (amr_core.py:118-146); cells outside two faces (edges / corners, never read
+    by the 7-point operator) take the last axis' value.  The product is the
+    single rounded operation (-alpha) * x."""
+    dim = len(domain[0])
+    na = -alpha
+    for i, b in enumerate(boxes):
+        f = fabs[i]
+        g = M.grow(b, ngrow)
+        for d in range(dim):
+            n = g[1][d] - g[0][d] + 1
+            for side, cond in (("lo", lo_conds[d]), ("hi", hi_conds[d])):
+                if cond == "periodic":
+                    continue
+                width = domain[0][d] - g[0][d] if side == "lo" else g[1][d] - domain[1][d]
+                for t in range(1, width + 1):
+                    o = [slice(None)] * (dim + 1)
+                    m = [slice(None)] * (dim + 1)
+                    if side == "lo":
+                        o[1 + d] = slice(width - t, width - t + 1)
+                        m[1 + d] = slice(width + t - 1, width + t)
+                    else:
+                        o[1 + d] = slice(n - width + t - 1, n - width + t)
+                        m[1 + d] = slice(n - width - t, n - width - t + 1)
+                    f[tuple(o)] = na * f[tuple(m)]
+
+
 class OracleMLMG:
     """CPU V-cycle solver; data per level as mesh_ref dicts (ncomp = 1)."""
 
     def __init__(self, domain, boxes, prob_lo=(0.0, 0.0, 0.0), prob_hi=(1.0, 1.0, 1.0), nu1=2, nu2=2,
-                 bottom_sweeps=32, threads=1):
-        """threads > 1 runs the per-box loops (GSRB colours, residuals, ghost
+                 bottom_sweeps=32, threads=1, bc="periodic"):
+        """bc: "periodic" (all periodic, the SURVEY 8(c) parity case),
+        "dirichlet" (every side BoundaryRecord 'external' with value 0), or
+        (lo_conds, hi_conds, value) with per-dimension 'periodic' / 'external'
+        conditions (a dimension is periodic iff both its sides are).  After
+        every fill the ghost cells outside the domain take the external value
+        on the finest level (apply_domain_boundary, amr_core.py:111-146,
+        mesh_ref.apply_domain_boundary): the boundary value sits at the ghost
+        cell centre, h/2 outside the face.  The coarse levels solve the
+        homogeneous correction equation with the boundary at that SAME point:
+        level l (spacing H = 2^l h) sets each outside ghost to
+        -alpha_l * (its mirror cell across the face), alpha_l = (H-h)/(H+h)
+        (linear interpolation through the ghost and first interior centres
+        vanishes at -h/2) -- see reflect_ghosts.  A plain ghost = 0 on every
+        level puts the coarse boundaries at different points and the V-cycle
+        diverges at 128^3.
+
+        threads > 1 runs the per-box loops (GSRB colours, residuals, ghost
         fills grouped by destination box) on a thread pool; numpy releases the
         GIL inside the array ops and boxes of one phase are independent, so the
         results are bit-identical to threads=1 (tests/test_oracle_mlmg.py)."""
-        self.periodic = (True, True, True)
+        if bc == "periodic":
+            bc = (("periodic",) * 3, ("periodic",) * 3, 0.0)
+        elif bc == "dirichlet":
+            bc = (("external",) * 3, ("external",) * 3, 0.0)
+        lo_c, hi_c, value = bc
+        for d in range(3):
+            if (lo_c[d] == "periodic") != (hi_c[d] == "periodic") or {lo_c[d], hi_c[d]} - {"periodic", "external"}:
+                raise ValueError(f"unsupported boundary conditions {bc!r}")
+        self.bc = (tuple(lo_c), tuple(hi_c), float(value))
+        self.periodic = tuple(c == "periodic" for c in lo_c)
         self.threads = max(1, int(threads))
         self._pool = ThreadPoolExecutor(self.threads) if self.threads > 1 else None
         self.nu1, self.nu2, self.bottom_sweeps = nu1, nu2, bottom_sweeps
@@ -151,6 +212,16 @@ class OracleMLMG:
         return list(self._pool.map(fn, items))
 
     def fill(self, lv):
+        self._fill(lv)
+        if not all(self.periodic):
+            lo_c, hi_c, value = self.bc
+            lev = self.levels.index(lv)
+            if lev == 0:
+                M.apply_domain_boundary(lv["boxes"], lv["phi"], 1, lv["domain"], lo_c, hi_c, value)
+            else:
+                reflect_ghosts(lv["boxes"], lv["phi"], 1, lv["domain"], lo_c, hi_c, reflect_alpha(lev))
+
+    def _fill(self, lv):
         if self._pool is None:
             M.execute(lv["fill"], lv["boxes"], lv["phi"], 1, lv["boxes"], lv["phi"], 1)
             return

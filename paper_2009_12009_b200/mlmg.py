@@ -35,7 +35,7 @@ from ._native import check, i32p, lib
 from .boxes import Box, IntVect
 from .comm import Transport, copy_into, device_reduce, fill_boundary, parallel_copy
 from .device import dh_array, field_of, level_of, stream_ptr
-from .geometry import Geometry
+from .geometry import BoundaryRecord, Geometry, apply_domain_boundary
 from .interlevel import coarsened_layout, prolong_from
 from .layout import BoxArray, DistributionMapping
 from .push import PushTable, prolong_push
@@ -135,11 +135,23 @@ class MLMG:
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
                  ghost_push=False, agg_cells=128**3, fuse_prolong=None, cluster_tail=None,
-                 grid_level_cells=None):
+                 grid_level_cells=None, bc=None):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
-        if not all(geom.periodic):
-            raise ValueError("MLMG currently supports all-periodic domains")
+        # boundary conditions: 'periodic' dimensions, or 'external' sides (a
+        # fixed ghost value on the finest level, 0 in the coarse-level
+        # correction equations) -- BoundaryRecord, amr_core.py:73-108
+        if bc is None:
+            if not all(geom.periodic):
+                raise ValueError("a non-periodic MLMG needs a BoundaryRecord with 'external' sides")
+            bc = BoundaryRecord.all_periodic(3)
+        bc.check_against(geom)
+        for d in range(3):
+            if not geom.periodic[d] and (bc.lo[d] != "external" or bc.hi[d] != "external"):
+                raise ValueError(f"MLMG supports 'periodic' and 'external' boundaries (dimension {d}: "
+                                 f"{bc.lo[d]!r}/{bc.hi[d]!r})")
+        self.bc = bc
+        self.all_periodic = all(geom.periodic)
         self.geom = geom
         self.nu1, self.nu2, self.bottom_sweeps = int(nu1), int(nu2), int(bottom_sweeps)
         self.transport = transport if transport is not None else Transport(dm.nranks)
