@@ -44,7 +44,7 @@ def _traffic(alg_bytes):
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "fine_sweep_traffic.json")) as f:
             t = json.load(f)
-        if "k_gsrb_sweep5" in t.get("kernel", "") and t.get("alg_bytes_per_launch", alg_bytes) == alg_bytes:
+        if "k_gsrb_stream" in t.get("kernel", "") and t.get("alg_bytes_per_launch", alg_bytes) == alg_bytes:
             return t["traffic_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
@@ -406,7 +406,7 @@ def run_ours(args):
                     "mode": "pipelined: double-buffered rhs/phi (FabArray host images), step s+1 upload and step s-1 "
                             "download on two copy streams during step s's solve (all copies inside the timed region)",
                     "serial": {"value": e2e_serial, "ms_per_step": 1e3 * t_serial / args.steps}},
-            "roofline": {"bound": "hbm", "kernel": "k_gsrb_sweep5 (fine level, fused red+black, TMA-fed)",
+            "roofline": {"bound": "hbm", "kernel": "k_gsrb_stream (fine level, fused red+black, register-streamed, TMA-fed)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "us_per_launch": t_sweep * 1e6,

@@ -55,6 +55,21 @@ int amrb_version(void);
 /* Kernel launches issued so far by this process (host-side count; launches
  * replayed from a captured CUDA graph are not included). */
 int64_t amrb_launch_count(void);
+/* Library options: process-wide, set explicitly by the caller (the library
+ * reads no environment variables).  Names and defaults:
+ *   "pdl"          2  programmatic dependent launch: 0 off, 1 always, 2 eager
+ *                     launches only (not inside stream capture)
+ *   "sweep_kernel" 0  fused GSRB sweep: 0 k_gsrb_stream wherever the layout
+ *                     allows it, 1 the previous TMA kernels (A/B runs)
+ *   "grid_per_sm"  0  CTAs per SM of the grid-synchronised level kernel
+ *                     (0: the occupancy maximum)
+ *   "stream_segments"  0  plane segments per tile column of k_gsrb_stream
+ *                     (0: enough for one wave of CTAs)
+ *   "stream_alternate" 1  odd segments stream downward (L2 halo sharing)
+ *   "stream_config"    0  k_gsrb_stream tile / strip / depth variant (A/B runs)
+ * AMRB_EINVAL for an unknown name. */
+int amrb_set_option(const char* name, int64_t value);
+int amrb_get_option(const char* name, int64_t* value);
 /* Zero n doubles (cudaMemsetAsync on `stream`; a memset node in a graph). */
 int amrb_zero(double* ptr, int64_t n, void* stream);
 /* host_dst[0..n) <- src (device) by a kernel storing through UVA into pinned
@@ -197,6 +212,17 @@ int amrb_gsrb_sweep(const amrb_level* lv, const amrb_field* a, const double* a_b
                     amrb_field* b, double* b_base, const amrb_field* rhs,
                     const double* rhs_base, const double dh[3],
                     const int32_t* fixed_lohi, void* stream);
+
+/* amrb_gsrb_sweep that also reduces the residual of its INPUT:
+ * *norm = max(*norm, max over valid cells of |rhs - L(a)|), stored as the
+ * uint64 bit pattern of a non-negative double (the caller zeroes *norm; a NaN
+ * residual propagates).  Same result as amrb_residual_norm(a) followed by
+ * amrb_gsrb_sweep, in one pass over a and rhs.  AMRB_ENOTSUP (nothing
+ * launched) when the level does not take the k_gsrb_stream path. */
+int amrb_gsrb_sweep_norm(const amrb_level* lv, const amrb_field* a, const double* a_base,
+                         amrb_field* b, double* b_base, const amrb_field* rhs,
+                         const double* rhs_base, const double dh[3],
+                         const int32_t* fixed_lohi, uint64_t* norm, void* stream);
 
 /* Prolongation fused into the first post-smoothing sweep of the V-cycle up-leg:
  * b = GSRB(a + P(c)), P = piecewise-constant interpolation of the coarse

@@ -13,7 +13,8 @@ import threading
 
 import numpy as np
 
-__all__ = ["lib", "check", "LIB_PATH", "AmrbError", "ptr", "i32p", "i64p", "u8p", "f64p"]
+__all__ = ["lib", "check", "LIB_PATH", "AmrbError", "ptr", "i32p", "i64p", "u8p", "f64p", "get_option", "set_option",
+           "option"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libamrb.so")
 
@@ -36,6 +37,8 @@ _SIGS = {
     "amrb_last_error": (C.c_char_p, []),
     "amrb_version": (C.c_int, []),
     "amrb_launch_count": (i64, []),
+    "amrb_set_option": (C.c_int, [C.c_char_p, i64]),
+    "amrb_get_option": (C.c_int, [C.c_char_p, P(i64)]),
     "amrb_zero": (C.c_int, [vp, i64, vp]),
     "amrb_store_host": (C.c_int, [vp, vp, i64, vp]),
     "amrb_plan_fill_create": (C.c_int, [C.c_int, C.c_int, P(i32), C.c_int, P(i32), P(C.c_uint8), P(vp)]),
@@ -67,6 +70,7 @@ _SIGS = {
     "amrb_residual": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
     "amrb_gsrb_color": (C.c_int, [vp, vp, vp, vp, vp, P(f64), C.c_int, vp]),
     "amrb_gsrb_sweep": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp]),
+    "amrb_gsrb_sweep_norm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, vp]),
     "amrb_gsrb_sweep_prolong": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp, vp, vp, vp]),
     "amrb_restrict": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
     "amrb_residual_restrict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
@@ -166,3 +170,31 @@ def u8p(a):
 def f64p(a):
     a = np.ascontiguousarray(a, dtype=np.float64)
     return a, _np_ptr(a, f64)
+
+
+def get_option(name):
+    """Current value of a library option (include/amrb.h amrb_set_option)."""
+    v = i64(0)
+    check(lib().amrb_get_option(name.encode(), C.byref(v)))
+    return int(v.value)
+
+
+def set_option(name, value):
+    """Set a library option; returns the previous value."""
+    old = get_option(name)
+    check(lib().amrb_set_option(name.encode(), int(value)))
+    return old
+
+
+class option:
+    """``with option("sweep_kernel", 1): ...`` -- scoped library option (A/B runs, tests)."""
+
+    def __init__(self, name, value):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        self.old = set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.old)

@@ -953,13 +953,14 @@ extern "C" int amrb_level_grid(int up, const int32_t* lohi, const double* dh, co
     a.c = crse_base + vc.off;
     a.cs0 = vc.s0;
     a.cs1 = vc.s1;
-    static int per_sm = 0;
-    if (!per_sm) {
-      AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_level_grid, 512, 0));
-      per_sm = per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm;
-      if (const char* e = getenv("AMRB_GRID_PER_SM"))  // A/B knob: CTAs per SM (grid.sync cost vs threads)
-        per_sm = std::max(1, std::min(per_sm, atoi(e)));
+    static int max_per_sm = 0;
+    if (!max_per_sm) {
+      AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, k_level_grid, 512, 0));
+      max_per_sm = max_per_sm < 1 ? 1 : max_per_sm > 2 ? 2 : max_per_sm;
     }
+    int per_sm = max_per_sm;
+    if (const int64_t want = option("grid_per_sm"))  // CTAs per SM (grid.sync cost vs threads), A/B runs
+      per_sm = std::max(1, std::min(per_sm, (int)want));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms() * per_sm);
     cfg.blockDim = dim3(512);

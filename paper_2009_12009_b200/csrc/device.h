@@ -47,6 +47,7 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 int pdl_mode();
+int64_t option(const char* name);  // amrb_set_option registry (stencil.cu)
 template <class... KArgs, class... Args>
 void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -116,18 +117,27 @@ struct TileTable {
   DevArray<int4> dev;
 };
 
+// Streaming-sweep work items, 8 ints each (gsrb_stream.cu seg_table)
+struct SegTable {
+  std::vector<int> host;
+  DevArray<int> dev;
+  int n = 0;
+};
+
 struct Level {
   int nboxes = 0;
   std::vector<BoxGeom> geo;
   std::vector<uint8_t> resident;
   DevArray<BoxGeom> dgeo;
   std::map<std::tuple<int, int, int>, TileTable*> tables;
+  std::map<std::tuple<int, int, int>, SegTable*> segtabs;
   DevArray<double> partials;  // reduction scratch
   // block index of each resident box inside a FabArray allocation (resident order)
   std::vector<int> slot;
   DevArray<int> dslot;
   ~Level() {
     for (auto& kv : tables) delete kv.second;
+    for (auto& kv : segtabs) delete kv.second;
   }
   const TileTable& tiles(int ti, int tj, int tk);
   // (box, j0, k0, first plane-step) per TJ x TK column of the valid region

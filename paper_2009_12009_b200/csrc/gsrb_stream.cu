@@ -1,0 +1,631 @@
+// k_gsrb_stream: the fused red+black GSRB sweep, register-streamed (sm_100a).
+//
+// Same result as the oracle's "fill; red; fill; black" (oracle/mlmg_ref.py
+// gsrb_color), bit for bit, written out of place A -> B.  The
+// design goal is a kernel bound by HBM, not by the SM:
+//
+//  * Work unit: a tile column TJ x TK of one box streamed along i over a
+//    SEGMENT of planes.  One CTA per (column, segment), all resident at once
+//    (one wave), and neighbouring segments stream in opposite directions, so
+//    every halo a CTA loads -- the j/k ring of its tile and the two planes past
+//    each segment end -- is loaded by its neighbour at about the same time and
+//    comes out of L2, not HBM.
+//  * Phi (tile + 2-cell halo) and rhs (tile + 1-cell ring) planes arrive by TMA
+//    into a ring of D+3 shared slots (one mbarrier per slot, one elected
+//    producer).
+//  * Each lane owns a k-PAIR (16-byte vectors: LDS.128 / STG.128) in RW rows of
+//    the tile ("strip") and keeps that column's values for planes p-1 .. p+2 in
+//    registers.  With the i-neighbours and the in-strip j-neighbours in
+//    registers, a relaxation reads ~1.5 values from shared memory instead of 7.
+//  * Skew 1: step p relaxes red(p+1) then black(p) in the same column.  red(p+1)
+//    needs only OLD black values; black(p) needs red(p +- 1) -- both the lane's
+//    own -- and the red of plane p's j/k neighbours, stored to shared memory in
+//    step p-1.  So a step has ONE __syncthreads: phase A (arrival, red(p+1),
+//    residual) | barrier | phase B (publish red(p+1), black(p), store plane p).
+//  * Ring warp(s): the red cells of the tile's ghost ring (rows j0-1, j0+TJ and
+//    columns k0-1, k0+TK) are recomputed from the halo exactly as the owning
+//    tile computes them, so "fill; red; fill; black" needs no fill in between.
+//
+// Modes: 0 plain sweep; 1 PROL: B = sweep(A + pc(C)) -- every arriving plane
+// gets its coarse parent added (the single addition of k_prolong) before
+// anything reads it, so the prolongation's read+write pass and its fill
+// disappear; 2 NORM: also max |rhs - L(A)| over the valid cells of A (the
+// residual of the sweep's INPUT, computed from the same registers), atomically
+// max-ed into a u64 (non-negative doubles order like their bit patterns).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+
+#include "tma.cuh"
+
+namespace amrb {
+
+// ---------------------------------------------------------------------------
+// tensor maps (shared with the other TMA kernels)
+// ---------------------------------------------------------------------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+}  // namespace
+
+TmaDesc describe(const Level& lv, const Field& f) {
+  TmaDesc d;
+  const int g = f.ngrow;
+  if (f.ng3[0] != g || f.ng3[1] != g || f.ng3[2] != g) return d;
+  d.g = g;
+  int first = -1, second = -1;
+  for (int b = 0; b < lv.nboxes; ++b)
+    if (lv.resident[b]) {
+      if (first < 0)
+        first = b;
+      else if (second < 0)
+        second = b;
+    }
+  if (first < 0) return d;
+  const BoxGeom& g0 = lv.geo[first];
+  const FabView& v0 = f.host[first];
+  auto grown = [&](const FabView& v) { return v.off - g * v.s0 - g * v.s1 - g; };
+  const int64_t og = grown(v0);
+  d.f = (int)(og & 1);  // shift the tensor origin back to a 16-byte boundary
+  d.base = og - d.f;
+  d.pitch = v0.s1;
+  d.rows = v0.s0 / v0.s1;
+  d.planes = g0.n[0] + 2 * g;
+  if (d.f + g0.n[2] + 2 * g > d.pitch) return d;
+  d.stride = second >= 0 ? grown(f.host[second]) - og : d.planes * v0.s0;
+  if (d.stride <= 0 || d.stride % 2) return d;
+  d.slot.assign(lv.nboxes, 0);
+  int k = 0;
+  for (int b = 0; b < lv.nboxes; ++b) {
+    if (!lv.resident[b]) continue;
+    const BoxGeom& gb = lv.geo[b];
+    const FabView& v = f.host[b];
+    if (gb.n[0] != g0.n[0] || gb.n[1] != g0.n[1] || gb.n[2] != g0.n[2] || v.s0 != v0.s0 || v.s1 != v0.s1) return d;
+    if (grown(v) != og + (int64_t)k * d.stride) return d;
+    d.slot[b] = k++;
+  }
+  d.ok = true;
+  return d;
+}
+
+bool make_map(CUtensorMap* map, const double* base, const TmaDesc& d, int nblocks, int box_rows, int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[4] = {(cuuint64_t)d.pitch, (cuuint64_t)d.rows, (cuuint64_t)d.planes, (cuuint64_t)nblocks};
+  cuuint64_t gstride[3] = {(cuuint64_t)d.pitch * 8, (cuuint64_t)(d.pitch * d.rows) * 8, (cuuint64_t)d.stride * 8};
+  cuuint32_t box[4] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base + d.base), gdim, gstride, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+namespace {
+
+constexpr int kModePlain = 0, kModeProl = 1, kModeNorm = 2;
+
+struct StreamArgs {
+  const int* seg;  // 8 ints per CTA: box, j0, k0, i0, i1, dir, -, -  (box-local valid coords)
+  const BoxGeom* geo;
+  const FabView* fb;  // output views
+  double* b;
+  const int* slot;  // per box: block index in the tensor maps
+  Coef cf;
+  int a_kc, a_jc, a_ic;  // tensor coordinate of phi cell (i, j0-2, k0-2) = (i + a_ic, j0 + a_jc, k0 + a_kc)
+  int r_kc, r_jc, r_ic;  // rhs (i, j0-1, k0-2)
+  int c_kc, c_jc, c_ic;  // coarse (i>>1, j0/2-1, k0/2-1) before the even-column shift
+  int flo[3], fhi[3];    // cells outside [flo, fhi] (global) are never relaxed
+  unsigned long long* norm;  // kModeNorm
+};
+
+constexpr int r128(int x) { return (x + 127) / 128 * 128; }
+
+template <int TJ, int TK, int D, int MODE>
+struct StreamLayout {
+  static constexpr int NS = D + 3;       // ring slots
+  static constexpr int PK = TK + 4;      // smem row pitch: cols k0-2 .. k0+TK+1
+  static constexpr int PJ = TJ + 4;      // phi rows j0-2 .. j0+TJ+1
+  static constexpr int RJ = TJ + 2;      // rhs rows j0-1 .. j0+TJ
+  static constexpr int CJ = TJ / 2 + 2;  // PROL coarse rows j0/2-1 .. j0/2+TJ/2
+  static constexpr int CK = TK / 2 + 4;  // PROL coarse cols from the even column at or below k0/2-1
+  static constexpr int PB = PJ * PK * 8, RB = RJ * PK * 8, CB = CJ * CK * 8;
+  static constexpr int ROFF = r128(PB);
+  static constexpr int COFF = ROFF + r128(RB);
+  static constexpr int SLOT = COFF + (MODE == kModeProl ? r128(CB) : 0);
+  static constexpr int BAR = NS * SLOT;
+  static constexpr int BYTES = BAR + 8 * NS;
+  static constexpr int WK = TK / 64;
+};
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2(double* p, double x, double y) { *reinterpret_cast<double2*>(p) = make_double2(x, y); }
+
+template <int TJ, int TK, int RW, int D, int MODE, int MINB>
+__global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
+    k_gsrb_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
+                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ StreamArgs args) {
+  pdl_entry();
+  using LY = StreamLayout<TJ, TK, D, MODE>;
+  constexpr int WK = LY::WK, NSW = TJ / RW * WK, NS = LY::NS, PK = LY::PK, CK = LY::CK;
+  constexpr bool PROL = MODE == kModeProl, NORM = MODE == kModeNorm;
+  static_assert(TK % 64 == 0 && TJ % RW == 0 && RW % 2 == 0 && TJ + 2 <= 32, "tile shape");
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + LY::BAR);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int producer = 32 * NSW;  // lane 0 of ring warp 0
+  const Coef cf = args.cf;
+
+  const int* sg = args.seg + 8 * blockIdx.x;
+  const int box = sg[0], j0 = sg[1], k0 = sg[2], i0 = sg[3], i1 = sg[4], dir = sg[5];
+  const int L = i1 - i0;
+  const int istart = dir > 0 ? i0 : i1 - 1;  // box-local plane of stream position 0
+  const BoxGeom g = args.geo[box];
+  const int bslot = args.slot[box];
+  const int gj0 = g.lo[1] + j0, gk0 = g.lo[2] + k0;
+  const int cshift = ((k0 >> 1) + args.c_kc) & 1;
+
+  auto plane = [&](int q) { return istart + dir * q; };
+  auto slot_base = [&](int q) { return sm + ((q + 2) % NS) * LY::SLOT; };  // phi position q (q >= -2)
+  auto phi_s = [&](int q) { return reinterpret_cast<double*>(slot_base(q)); };
+  auto rhs_s = [&](int q) { return reinterpret_cast<const double*>(slot_base(q + 1) + LY::ROFF); };  // rides with phi q+1
+  auto crs_s = [&](int q) { return reinterpret_cast<const double*>(slot_base(q) + LY::COFF); };
+  auto wait_pos = [&](int q) { mbar_wait(&bars[(q + 2) % NS], (unsigned)(((q + 2) / NS) & 1)); };
+  auto issue = [&](int q) {  // phi position q, rhs position q-1 (from q = 0), coarse parent plane
+    uint64_t* bar = &bars[(q + 2) % NS];
+    const bool wr = q >= 0;
+    mbar_expect_tx(bar, LY::PB + (wr ? LY::RB : 0) + (PROL ? LY::CB : 0));
+    const int ip = plane(q);
+    tma_load4(slot_base(q), &tmA, bar, k0 + args.a_kc, j0 + args.a_jc, ip + args.a_ic, bslot);
+    if (wr) tma_load4(slot_base(q) + LY::ROFF, &tmR, bar, k0 + args.r_kc, j0 + args.r_jc, plane(q - 1) + args.r_ic, bslot);
+    if (PROL)
+      tma_load4(slot_base(q) + LY::COFF, &tmC, bar, (k0 >> 1) + args.c_kc - cshift, (j0 >> 1) + args.c_jc,
+                (ip >> 1) + args.c_ic, bslot);
+  };
+
+  // never-relaxed (fixed) ring cells: the tile's ring outside the domain
+  auto plane_ok = [&](int q) {
+    const int gi = g.lo[0] + plane(q);
+    return gi >= args.flo[0] && gi <= args.fhi[0];
+  };
+  const bool top_ok = gj0 - 1 >= args.flo[1], bot_ok = gj0 + TJ <= args.fhi[1];
+  const bool lft_ok = gk0 - 1 >= args.flo[2], rgt_ok = gk0 + TK <= args.fhi[2];
+
+  if (tid == producer) {
+    for (int x = 0; x < NS; ++x) mbar_init(&bars[x], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == producer)
+    for (int q = -2; q <= min(NS - 3, L + 1); ++q) issue(q);
+
+  // ---- roles ---------------------------------------------------------------
+  const bool strip = warp < NSW;
+  const int wk = strip ? warp % WK : warp - NSW;
+  const int m = 32 * wk + lane;  // k-pair index in the tile
+  const int c0 = 2 + 2 * m;      // smem column of the pair's first cell
+  const int r0 = 2 + (strip ? (warp / WK) * RW : 0);  // strip: first smem row
+
+  // strip state (row x = smem row r0 + x): pairs of planes p, p+1, p+2
+  double a0[RW][2], a1[RW][2], a2[RW][2], am[RW], rs[RW], ao[RW];
+  // ring-row state (h = 0: row 1, h = 1: row TJ+2)
+  double g0[2][2], g1[2][2], g2[2][2];
+  unsigned long long nmax = 0;  // NORM: max |r| as bit pattern (NaN sorts above +inf)
+
+  double* out = nullptr;
+  int64_t ostep = 0;
+  if (strip) {
+    const FabView B = args.fb[box];
+    out = args.b + B.off + (int64_t)istart * B.s0 + (int64_t)(j0 + r0 - 2) * B.s1 + (k0 + 2 * m);
+    ostep = dir * B.s0;
+  }
+  const int64_t orow = strip ? args.fb[box].s1 : 0;
+
+  // PROL: every cell of plane q's tile += its coarse parent (the single addition
+  // of k_prolong), pairs spread over all threads; a barrier must follow before
+  // anyone reads the plane
+  auto correct_plane = [&](int q) {
+    double* S = phi_s(q);
+    const double* Cq = crs_s(q);
+    constexpr int PP = (TK + 4) / 2, NP = (TJ + 4) * PP, NT = 32 * (NSW + WK);
+    for (int e = tid; e < NP; e += NT) {
+      const int rr = e / PP, pc = e - rr * PP;
+      const double2 v = lds2(S + rr * PK + 2 * pc);
+      const double cp = Cq[(rr >> 1) * CK + pc + cshift];
+      sts2(S + rr * PK + 2 * pc, v.x + cp, v.y + cp);
+    }
+  };
+  // arrival of plane position q: own pairs to registers
+  auto arrive_strip = [&](int q, double (&dst)[RW][2]) {
+    const double* S = phi_s(q);
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const double2 v = lds2(S + (r0 + x) * PK + c0);
+      dst[x][0] = v.x;
+      dst[x][1] = v.y;
+    }
+  };
+  auto arrive_ring = [&](int q, double (&dst)[2][2]) {
+    const double* S = phi_s(q);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double2 v = lds2(S + (h ? TJ + 2 : 1) * PK + c0);
+      dst[h][0] = v.x;
+      dst[h][1] = v.y;
+    }
+  };
+
+  // prologue: positions -2, -1
+  wait_pos(-2);
+  wait_pos(-1);
+  if (PROL) {
+    correct_plane(-2);
+    correct_plane(-1);
+    __syncthreads();
+  }
+  if (strip) {
+    arrive_strip(-2, a0);
+    arrive_strip(-1, a1);
+#pragma unroll
+    for (int x = 0; x < RW; ++x) am[x] = rs[x] = ao[x] = 0.0;
+  } else {
+    arrive_ring(-2, g0);
+    arrive_ring(-1, g1);
+  }
+  __syncthreads();
+
+  // One step per role; PHI = the pair element relaxed in strip row 0
+  // (b = (PHI + x) & 1); UP: the stream runs toward +i.  lap7's operand order
+  // is fixed (i-1 before i+1), so the stream neighbours go in plane order.
+  // Strip and ring warps run separate loops (their register state never
+  // overlaps) that meet at the same __syncthreads once per step.
+  auto strip_step = [&](auto phi_tag, auto up_tag, int p) {
+    constexpr int PHI = decltype(phi_tag)::value;
+    constexpr bool UP = decltype(up_tag)::value;
+    auto lapi = [&](double c, double prev, double next, double ym, double yp, double zm, double zp) {
+      return UP ? lap7(c, prev, next, ym, yp, zm, zp, cf) : lap7(c, next, prev, ym, yp, zm, zp, cf);
+    };
+    wait_pos(p + 2);
+    const double* S0 = phi_s(p);
+    double* S1 = phi_s(p + 1);
+    const double* R1 = rhs_s(p + 1);
+    const bool red_on = (p + 1 >= 0 && p + 1 < L) || plane_ok(p + 1);
+    double nr[RW], rsn[RW];
+    if (PROL) {
+      correct_plane(p + 2);
+      __syncthreads();
+    }
+    arrive_strip(p + 2, a2);
+    // ---- phase A: red(p+1) in column (r, c0 + b); NORM: residual of plane p+1
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const int b = (PHI + x) & 1;  // compile-time after unrolling
+      const int row = (r0 + x) * PK;
+      const double c = a1[x][b];
+      const double ym = x > 0 ? a1[x > 0 ? x - 1 : 0][b] : S1[row - PK + c0 + b];
+      const double yp = x < RW - 1 ? a1[x < RW - 1 ? x + 1 : 0][b] : S1[row + PK + c0 + b];
+      const double kn = b ? S1[row + c0 + 2] : S1[row + c0 - 1];  // the neighbour pair's cell
+      const double zm = b ? a1[x][0] : kn;
+      const double zp = b ? kn : a1[x][1];
+      const double2 rr = lds2(R1 + row - PK + c0);
+      const double rb = b ? rr.y : rr.x;
+      rsn[x] = b ? rr.x : rr.y;
+      const double d = rb - lapi(c, a0[x][b], a2[x][b], ym, yp, zm, zp);
+      nr[x] = c + d * cf.rgamma;
+      if (NORM && p + 1 >= 0 && p + 1 < L) {
+        // the other cell of the pair (black in plane p+1), old values only
+        const int o = 1 - b;
+        const double ym2 = x > 0 ? a1[x > 0 ? x - 1 : 0][o] : S1[row - PK + c0 + o];
+        const double yp2 = x < RW - 1 ? a1[x < RW - 1 ? x + 1 : 0][o] : S1[row + PK + c0 + o];
+        const double kn2 = o ? S1[row + c0 + 2] : S1[row + c0 - 1];
+        const double zm2 = o ? a1[x][0] : kn2;
+        const double zp2 = o ? kn2 : a1[x][1];
+        const double d2 = rsn[x] - lapi(a1[x][o], ao[x], a2[x][o], ym2, yp2, zm2, zp2);
+        nmax = max(nmax, max((unsigned long long)__double_as_longlong(fabs(d)),
+                             (unsigned long long)__double_as_longlong(fabs(d2))));
+      }
+    }
+    __syncthreads();
+    // ---- phase B: publish red(p+1); black(p); plane p out
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const int b = (PHI + x) & 1;
+      if (red_on) S1[(r0 + x) * PK + c0 + b] = nr[x];
+    }
+    if (p >= 0) {
+#pragma unroll
+      for (int x = 0; x < RW; ++x) {
+        const int b = (PHI + x) & 1;
+        const int row = (r0 + x) * PK;
+        const double c = a0[x][b];
+        const double ym = x > 0 ? a0[x > 0 ? x - 1 : 0][b] : S0[row - PK + c0 + b];
+        const double yp = x < RW - 1 ? a0[x < RW - 1 ? x + 1 : 0][b] : S0[row + PK + c0 + b];
+        const double kn = b ? S0[row + c0 + 2] : S0[row + c0 - 1];
+        const double zm = b ? a0[x][0] : kn;
+        const double zp = b ? kn : a0[x][1];
+        const double xp = red_on ? nr[x] : a1[x][b];
+        a0[x][b] = relax(c, rs[x], lapi(c, am[x], xp, ym, yp, zm, zp), cf.rgamma);
+      }
+#pragma unroll
+      for (int x = 0; x < RW; ++x)
+        *reinterpret_cast<double2*>(out + x * orow) = make_double2(a0[x][0], a0[x][1]);
+      out += ostep;
+    }
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const int b = (PHI + x) & 1;
+      am[x] = a0[x][1 - b];
+      ao[x] = a1[x][b];
+      a0[x][0] = a1[x][0];
+      a0[x][1] = a1[x][1];
+      if (red_on) a0[x][b] = nr[x];
+      a1[x][0] = a2[x][0];
+      a1[x][1] = a2[x][1];
+      rs[x] = rsn[x];
+    }
+    if (PROL || p + 1 + NS <= L + 1) fence_proxy_async();  // our shared stores before a later TMA into the slot
+  };
+
+  auto ring_step = [&](auto phi_tag, auto up_tag, int p) {
+    constexpr int PHI = decltype(phi_tag)::value;
+    constexpr bool UP = decltype(up_tag)::value;
+    auto lapi = [&](double c, double prev, double next, double ym, double yp, double zm, double zp) {
+      return UP ? lap7(c, prev, next, ym, yp, zm, zp, cf) : lap7(c, next, prev, ym, yp, zm, zp, cf);
+    };
+    wait_pos(p + 2);
+    const double* S0 = phi_s(p);
+    double* S1 = phi_s(p + 1);
+    const double* S2 = phi_s(p + 2);
+    const double* R1 = rhs_s(p + 1);
+    const bool red_on = (p + 1 >= 0 && p + 1 < L) || plane_ok(p + 1);
+    double rv[2], rc = 0.0;  // ring rows / ring column red(p+1)
+    int rco = 0;             // ring column cell offset
+    bool rcok = false;
+    if (PROL) {
+      correct_plane(p + 2);
+      __syncthreads();
+    }
+    arrive_ring(p + 2, g2);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int b = h ? PHI : 1 - PHI;
+      const int row = (h ? TJ + 2 : 1) * PK;
+      const double kn = b ? S1[row + c0 + 2] : S1[row + c0 - 1];
+      const double zm = b ? g1[h][0] : kn;
+      const double zp = b ? kn : g1[h][1];
+      const double c = g1[h][b];
+      const double rb = R1[row - PK + c0 + b];
+      rv[h] = relax(c, rb, lapi(c, g0[h][b], g2[h][b], S1[row - PK + c0 + b], S1[row + PK + c0 + b], zm, zp),
+                    cf.rgamma);
+    }
+    if (wk == 0 && lane < TJ + 2) {
+      constexpr int HALF = (TJ + 2) / 2;
+      const int side = lane >= HALF;
+      const int idx = lane - side * HALF;
+      const int cc = side ? TK + 2 : 1;
+      const int rr = 1 + 2 * idx + (side ? 1 - PHI : PHI);
+      rco = rr * PK + cc;
+      const double c = S1[rco];
+      rc = relax(c, R1[rco - PK], lapi(c, S0[rco], S2[rco], S1[rco - PK], S1[rco + PK], S1[rco - 1], S1[rco + 1]),
+                 cf.rgamma);
+      rcok = (side ? rgt_ok : lft_ok) && (rr != 1 || top_ok) && (rr != TJ + 2 || bot_ok);
+    }
+    __syncthreads();
+    if (tid == producer && p >= -1 && p - 1 + NS <= L + 1) issue(p - 1 + NS);
+    if (red_on) {
+      if (top_ok) S1[1 * PK + c0 + (1 - PHI)] = rv[0];
+      if (bot_ok) S1[(TJ + 2) * PK + c0 + PHI] = rv[1];
+      if (rcok) S1[rco] = rc;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      g0[h][0] = g1[h][0];
+      g0[h][1] = g1[h][1];
+      g1[h][0] = g2[h][0];
+      g1[h][1] = g2[h][1];
+    }
+    if (PROL || p + 1 + NS <= L + 1) fence_proxy_async();
+  };
+
+  // PHI of stream position p: b of strip row 0 = 1 - ((i + j0 + k0) & 1), global
+  auto run = [&](auto up_tag, auto& stepfn) {
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    int p = -2;
+    const int par = (g.lo[0] + plane(-2) + gj0 + gk0) & 1;  // PHI flips every step
+    if (par == 0) {
+      stepfn(I1{}, up_tag, p);
+      ++p;
+    }
+    for (; p + 1 < L; p += 2) {
+      stepfn(I0{}, up_tag, p);
+      stepfn(I1{}, up_tag, p + 1);
+    }
+    if (p < L) stepfn(I0{}, up_tag, p);
+  };
+  if (strip) {
+    if (dir > 0)
+      run(std::true_type{}, strip_step);
+    else
+      run(std::false_type{}, strip_step);
+  } else {
+    if (dir > 0)
+      run(std::true_type{}, ring_step);
+    else
+      run(std::false_type{}, ring_step);
+  }
+
+  if (NORM) {
+    for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    if (strip && lane == 0 && nmax) atomicMax(args.norm, nmax);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+// (column, segment) work items: every resident box cut into TJ x TK columns,
+// each column into nseg near-equal plane ranges; odd segments stream downward.
+// Cached on the Level.
+const SegTable& seg_table(Level& lv, int tj, int tk, int nseg, bool alternate) {
+  auto key = std::make_tuple(tj, tk, alternate ? nseg : -nseg);
+  auto it = lv.segtabs.find(key);
+  if (it != lv.segtabs.end()) return *it->second;
+  auto* t = new SegTable;
+  for (int b = 0; b < lv.nboxes; ++b) {
+    if (!lv.resident[b]) continue;
+    const BoxGeom& gb = lv.geo[b];
+    const int ns = std::max(1, std::min(nseg, gb.n[0] / 4));
+    for (int j = 0; j < gb.n[1]; j += tj)
+      for (int k = 0; k < gb.n[2]; k += tk)
+        for (int s = 0; s < ns; ++s) {
+          const int a = (int)((long long)gb.n[0] * s / ns), e = (int)((long long)gb.n[0] * (s + 1) / ns);
+          if (e <= a) continue;
+          const int v[8] = {b, j, k, a, e, (alternate && (s & 1)) ? -1 : 1, 0, 0};
+          t->host.insert(t->host.end(), v, v + 8);
+          ++t->n;
+        }
+  }
+  t->dev.upload(t->host);
+  lv.segtabs[key] = t;
+  return *t;
+}
+
+template <int TJ, int TK, int RW, int D, int MODE, int MINB>
+bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
+                   const double* r_base, const Coef& cf, const int flo[3], const int fhi[3], cudaStream_t st,
+                   const Level* clv, const Field* c, const double* c_base, unsigned long long* norm) {
+  using LY = StreamLayout<TJ, TK, D, MODE>;
+  constexpr int NW = (TJ / RW + 1) * (TK / 64);
+  int nres = 0;
+  for (int bx = 0; bx < lv.nboxes; ++bx) {
+    if (!lv.resident[bx]) continue;
+    ++nres;
+    const BoxGeom& gg = lv.geo[bx];
+    if (gg.n[1] % TJ || gg.n[2] % TK || gg.n[0] < 2) return false;
+  }
+  if (a.ngrow < 2 || r.ngrow < 1) return false;
+  if (nres == 0) return true;
+  TmaDesc da = describe(lv, a), dr = describe(lv, r);
+  if (!da.ok || !dr.ok || da.slot != lv.slot || dr.slot != lv.slot) return false;
+  CUtensorMap ma, mr, mc;
+  std::memset(&ma, 0, sizeof ma);
+  std::memset(&mr, 0, sizeof mr);
+  std::memset(&mc, 0, sizeof mc);
+  if (!make_map(&ma, a_base, da, nres, LY::PJ, LY::PK)) return false;
+  if (!make_map(&mr, r_base, dr, nres, LY::RJ, LY::PK)) return false;
+  StreamArgs args;
+  std::memset(&args, 0, sizeof args);
+  args.a_kc = -2 + da.g + da.f;
+  args.a_jc = -2 + da.g;
+  args.a_ic = da.g;
+  args.r_kc = -2 + dr.g + dr.f;
+  args.r_jc = -1 + dr.g;
+  args.r_ic = dr.g;
+  if (MODE == kModeProl) {
+    if (!clv || !c || c->ngrow < 1) return false;
+    TmaDesc dc = describe(*clv, *c);
+    if (!dc.ok || dc.slot != da.slot) return false;
+    if (!make_map(&mc, c_base, dc, nres, LY::CJ, LY::CK)) return false;
+    args.c_kc = -1 + dc.g + dc.f;
+    args.c_jc = -1 + dc.g;
+    args.c_ic = dc.g;
+  } else {
+    mc = ma;
+  }
+  auto kern = k_gsrb_stream<TJ, TK, RW, D, MODE, MINB>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NW, LY::BYTES));
+    per_sm = std::max(per_sm, 1);
+  }
+  long long ncols = 0;
+  for (int bx = 0; bx < lv.nboxes; ++bx)
+    if (lv.resident[bx]) ncols += (long long)(lv.geo[bx].n[1] / TJ) * (lv.geo[bx].n[2] / TK);
+  const long long slots = (long long)per_sm * num_sms();
+  int nseg = (int)std::max<long long>(1, slots / ncols);
+  if (const int64_t want = option("stream_segments")) nseg = (int)want;  // A/B runs
+  const SegTable& t = seg_table(lv, TJ, TK, nseg, option("stream_alternate") != 0);
+  args.seg = t.dev.p;
+  args.geo = lv.dgeo.p;
+  args.fb = b.dev.p;
+  args.b = b_base;
+  args.slot = lv.dslot.p;
+  args.cf = cf;
+  for (int x = 0; x < 3; ++x) {
+    args.flo[x] = flo[x];
+    args.fhi[x] = fhi[x];
+  }
+  args.norm = norm;
+  launch_k(kern, (unsigned)t.n, 32 * NW, LY::BYTES, st, ma, mr, mc, args);
+  check_launch("k_gsrb_stream");
+  return true;
+}
+
+}  // namespace
+
+// mode 0: plain, 1: PROL (clv/c/c_base), 2: NORM (norm)
+bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
+                         const Field& r, const double* r_base, const Coef& cf, const int flo[3], const int fhi[3],
+                         cudaStream_t st, const Level* clv, const Field* c, const double* c_base,
+                         unsigned long long* norm) {
+#define AMRB_STREAM(TJ, TK, RW, D, M, B) \
+  launch_stream<TJ, TK, RW, D, M, B>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, c_base, norm)
+  // variants (library option "stream_config" forces one; measured on the C3 fine
+  // level, tools/mb_stream.py): 1 = 16x64 tiles, 4-row strips; 2 = 16x64, 2-row
+  // strips (two CTAs/SM); 3 = 8x64, 2-row, depth 3; 4 = 16x128, 4-row; 5 = 16x64,
+  // 4-row, depth 3
+#define AMRB_STREAM_CFG(M, CFG)                  \
+  switch (CFG) {                                 \
+    case 1:                                      \
+      return AMRB_STREAM(16, 64, 4, 2, M, 1);    \
+    case 2:                                      \
+      return AMRB_STREAM(16, 64, 2, 2, M, 2);    \
+    case 3:                                      \
+      return AMRB_STREAM(8, 64, 2, 3, M, 3);     \
+    case 4:                                      \
+      return AMRB_STREAM(16, 128, 4, 2, M, 1);   \
+    case 5:                                      \
+      return AMRB_STREAM(16, 64, 4, 3, M, 1);    \
+  }                                              \
+  return false;
+  auto run = [&](int cfg) -> bool {
+    switch (mode) {
+      case kModePlain:
+        AMRB_STREAM_CFG(kModePlain, cfg)
+      case kModeProl:
+        AMRB_STREAM_CFG(kModeProl, cfg)
+      case kModeNorm:
+        AMRB_STREAM_CFG(kModeNorm, cfg)
+    }
+    return false;
+  };
+  if (const int64_t forced = option("stream_config")) return run((int)forced);
+  // defaults per mode, then the narrower tiles when a box does not divide
+  static const int prefs[3][3] = {{1, 2, 3}, {4, 1, 3}, {2, 1, 3}};
+  for (int cfg : prefs[mode])
+    if (run(cfg)) return true;
+  return false;
+#undef AMRB_STREAM_CFG
+
+#undef AMRB_STREAM
+  return false;
+}
+
+}  // namespace amrb

@@ -14,7 +14,9 @@
 #include <atomic>
 #include <cfloat>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 
 #include "stencil_common.cuh"
 
@@ -29,10 +31,21 @@ namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
-int pdl_mode() {
-  static const int mode = getenv("AMRB_PDL") ? atoi(getenv("AMRB_PDL")) : 2;
-  return mode;
+// Library options (amrb_set_option): explicit, process-wide, no environment.
+namespace {
+std::mutex g_opt_mu;
+std::map<std::string, int64_t>& options() {
+  static std::map<std::string, int64_t> o = {{"pdl", 2}, {"sweep_kernel", 0}, {"grid_per_sm", 0}, {"stream_segments", 0}, {"stream_alternate", 1},
+                                               {"stream_config", 0}};
+  return o;
 }
+}  // namespace
+int64_t option(const char* name) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  auto it = options().find(name);
+  return it == options().end() ? 0 : it->second;
+}
+int pdl_mode() { return (int)option("pdl"); }
 
 const TileTable& Level::tiles(int ti, int tj, int tk) {
   auto key = std::make_tuple(ti, tj, tk);
@@ -895,6 +908,24 @@ using namespace amrb;
 
 extern "C" const char* amrb_last_error(void) { return amrb::g_last_error.c_str(); }
 extern "C" int amrb_version(void) { return 1; }
+extern "C" int amrb_set_option(const char* name, int64_t value) {
+  return amrb::guarded([&] {
+    if (!name) throw amrb::Error(AMRB_EINVAL, "set_option: null name");
+    std::lock_guard<std::mutex> lk(amrb::g_opt_mu);
+    auto it = amrb::options().find(name);
+    if (it == amrb::options().end()) throw amrb::Error(AMRB_EINVAL, std::string("unknown option ") + name);
+    it->second = value;
+  });
+}
+extern "C" int amrb_get_option(const char* name, int64_t* value) {
+  return amrb::guarded([&] {
+    if (!name || !value) throw amrb::Error(AMRB_EINVAL, "get_option: null argument");
+    std::lock_guard<std::mutex> lk(amrb::g_opt_mu);
+    auto it = amrb::options().find(name);
+    if (it == amrb::options().end()) throw amrb::Error(AMRB_EINVAL, std::string("unknown option ") + name);
+    *value = it->second;
+  });
+}
 extern "C" int64_t amrb_launch_count(void) { return (int64_t)amrb::g_launches.load(); }
 
 namespace amrb {
@@ -1150,6 +1181,10 @@ extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const
     const bool fixed = fixed_lohi != nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     const Coef cf = make_coef(dh);
+    if (option("sweep_kernel") == 0 &&
+        launch_sweep_stream(0, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, st, nullptr, nullptr,
+                            nullptr, nullptr))
+      return;
     if (launch_sweep_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st)) return;
     if (divides(16, 64))
       launch_sweep_full<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
@@ -1167,6 +1202,30 @@ extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const
       launch_sweep<16, 32>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, st);
     (void)minj;
     (void)mink;
+  });
+}
+
+extern "C" int amrb_gsrb_sweep_norm(const amrb_level* lv_, const amrb_field* a, const double* a_base, amrb_field* b,
+                                    double* b_base, const amrb_field* rhs, const double* rhs_base, const double dh[3],
+                                    const int32_t* fixed_lohi, uint64_t* norm, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(a), 2, "gsrb_sweep_norm (phi in)");
+    need_ghost(F(rhs), 1, "gsrb_sweep_norm (rhs)");
+    for (auto* f : {a, (const amrb_field*)b, rhs}) need_same_level(F(f), lv, "gsrb_sweep_norm");
+    if (!norm) throw Error(AMRB_EINVAL, "gsrb_sweep_norm: null norm");
+    if (!lv.all_even()) throw Error(AMRB_EINVAL, "gsrb_sweep needs even box extents");
+    int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
+    if (fixed_lohi)
+      for (int x = 0; x < 3; ++x) {
+        flo[x] = fixed_lohi[x];
+        fhi[x] = fixed_lohi[3 + x];
+      }
+    if (option("sweep_kernel") != 0 ||
+        !launch_sweep_stream(2, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
+                             (cudaStream_t)stream, nullptr, nullptr, nullptr,
+                             reinterpret_cast<unsigned long long*>(norm)))
+      throw Error(AMRB_ENOTSUP, "gsrb_sweep_norm: level does not take the k_gsrb_stream path");
   });
 }
 
@@ -1222,6 +1281,11 @@ extern "C" int amrb_gsrb_sweep_prolong(const amrb_level* lv_, const amrb_field* 
         if (lv.geo[x].lo[d] % 2 || clv.geo[x].lo[d] * 2 != lv.geo[x].lo[d] || clv.geo[x].n[d] * 2 != lv.geo[x].n[d])
           throw Error(AMRB_EINVAL, "gsrb_sweep_prolong: coarse box is not the coarsened fine box");
     }
+    const int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
+    if (option("sweep_kernel") == 0 &&
+        launch_sweep_stream(1, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
+                            (cudaStream_t)stream, &clv, &F(c), c_base, nullptr))
+      return;
     if (!launch_sweep_prolong_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), clv, F(c), c_base,
                                   (cudaStream_t)stream))
       throw Error(AMRB_ENOTSUP, "gsrb_sweep_prolong: level does not take the k_gsrb_sweep5 path");

@@ -106,6 +106,12 @@ __device__ __forceinline__ void push_deltas_mid(const PushDev& pd, int b, int j,
 bool launch_sweep_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                       const Field& r, const double* r_base, const Coef& cf, const int fixed_lo[3],
                       const int fixed_hi[3], bool fixed, cudaStream_t st, const PushDev* push = nullptr);
+// gsrb_stream.cu: mode 0 plain, 1 fused prolongation (clv / c / c_base),
+// 2 plain + max |rhs - L(a)| into *norm (u64 bit pattern, caller zeroes it)
+bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
+                         const Field& r, const double* r_base, const Coef& cf, const int flo[3], const int fhi[3],
+                         cudaStream_t st, const Level* clv, const Field* c, const double* c_base,
+                         unsigned long long* norm);
 bool launch_sweep_prolong_tma(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                               const Field& r, const double* r_base, const Coef& cf, const Level& clv, const Field& c,
                               const double* c_base, cudaStream_t st);

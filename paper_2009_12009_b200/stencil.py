@@ -14,7 +14,7 @@ import ctypes as C
 from ._native import AMRB_ENOTSUP, check, i32p, lib
 from .device import dh_array, field_of, level_of, stream_ptr
 
-__all__ = ["laplacian", "residual", "gsrb_color", "gsrb_sweep", "residual_restrict", "dh_of"]
+__all__ = ["laplacian", "residual", "gsrb_color", "gsrb_sweep", "gsrb_sweep_norm", "residual_restrict", "dh_of"]
 
 
 def dh_of(geom):
@@ -57,22 +57,51 @@ def gsrb_color(phi, rhs, dh, color):
                                 dh_array(dh), int(color), stream_ptr()))
 
 
+def fixed_lohi(fixed):
+    """int32[6] (global lo, hi, 3-D padded) for the sweeps' ``fixed`` argument:
+    a Box, or a (lo, hi) pair with None entries for unbounded axes."""
+    import numpy as np
+
+    if fixed is None:
+        return None
+    arr = np.array([-(1 << 30)] * 3 + [1 << 30] * 3, dtype=np.int32)
+    lo, hi = (fixed.lo, fixed.hi) if hasattr(fixed, "lo") else fixed
+    pad = 3 - len(lo)
+    for d in range(len(lo)):
+        if lo[d] is not None:
+            arr[pad + d] = lo[d]
+        if hi[d] is not None:
+            arr[3 + pad + d] = hi[d]
+    return arr
+
+
 def gsrb_sweep(a, b, rhs, dh, fixed=None):
     """b = one fused red+black sweep of a (a ghosts width 2, rhs ghosts width 1
     filled).  ``fixed`` = Box outside which cells are never relaxed."""
     _same_layout(a, b, rhs)
-    fp = None
-    if fixed is not None:
-        import numpy as np
-
-        pad = 3 - fixed.dim
-        arr = np.array([-(1 << 30)] * 3 + [1 << 30] * 3, dtype=np.int32)
-        for d in range(fixed.dim):
-            arr[pad + d] = fixed.lo[d]
-            arr[3 + pad + d] = fixed.hi[d]
-        _keep, fp = i32p(arr)
+    fa = fixed_lohi(fixed)
+    fp = None if fa is None else i32p(fa)[1]
     check(lib().amrb_gsrb_sweep(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
                                 field_of(rhs).handle, _p(rhs), dh_array(dh), fp, stream_ptr()))
+    del fa
+
+
+def gsrb_sweep_norm(a, b, rhs, dh, norm, fixed=None):
+    """gsrb_sweep(a, b, rhs) that also max-reduces |rhs - L(a)| over the valid
+    cells of ``a`` into ``norm`` (a 1-element int64/uint64 CUDA tensor holding
+    the bit pattern of a non-negative double; zero it first).  Raises
+    NotImplementedError (nothing launched) when the level does not take the
+    streaming sweep path."""
+    _same_layout(a, b, rhs)
+    fa = fixed_lohi(fixed)
+    fp = None if fa is None else i32p(fa)[1]
+    rc = lib().amrb_gsrb_sweep_norm(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
+                                    field_of(rhs).handle, _p(rhs), dh_array(dh), fp, C.c_void_p(norm.data_ptr()),
+                                    stream_ptr())
+    del fa
+    if rc == AMRB_ENOTSUP:
+        raise NotImplementedError("gsrb_sweep_norm: level does not take the streaming sweep path")
+    check(rc)
 
 
 def gsrb_sweep_prolong(a, b, rhs, dh, crse):

@@ -1,8 +1,8 @@
 """Launch the bench's roofline kernel alone for ncu: the C3 solver's internal
 level-0 layout (one 256^3 box, phi grown by 2, rhs by 1), fill + fused GSRB
-sweep, 12 times.  Only the sweeps launch k_gsrb_sweep5, so
+sweep, 12 times.  Only the sweeps launch k_gsrb_stream, so
 
-    ncu --set full --clock-control none -k regex:k_gsrb_sweep5 -s 4 -c 1 \\
+    ncu --set full --clock-control none -k regex:k_gsrb_stream -s 4 -c 1 \\
         -o gpurun_out/fine_sweep python profiles/prof_fine_sweep.py
 
 captures a warm fine-level launch; `python profiles/prof_fine_sweep.py --summarize
@@ -57,7 +57,7 @@ def summarize(rep):
         return float(val) * scale
 
     res = {
-        "kernel": get["Kernel Name"][1] if "Kernel Name" in get else "k_gsrb_sweep5",
+        "kernel": get["Kernel Name"][1] if "Kernel Name" in get else "k_gsrb_stream",
         "layout": "C3 solver level 0: one 256^3 box, phi ngrow 2, rhs ngrow 1",
         "dram_read_mb": mb("dram__bytes_read.sum"),
         "dram_write_mb": mb("dram__bytes_write.sum"),
