@@ -381,7 +381,10 @@ int amrb_reduce(const amrb_level* lv, const amrb_field* x, const double* x_base,
 
 /* Fill ghost cells outside the physical domain (apply_domain_boundary,
  * amr_core.py:111-146).  bc: int32[3][2] per (axis, side) 0 periodic/skip,
- * 1 external (value), 2 extrap.  domain: int32[6] lo, hi (3-D padded). */
+ * 1 external (value), 2 extrap, 3 reflect: value * the cell mirrored across
+ * the face (the MLMG coarse-level homogeneous Dirichlet ghosts,
+ * oracle/mlmg_ref.py reflect_ghosts).  One pass per (axis, side) in that
+ * order.  domain: int32[6] lo, hi (3-D padded). */
 int amrb_domain_bc(const amrb_level* lv, amrb_field* f, double* base, int ncomp,
                    const int32_t* domain, const int32_t* bc, double value,
                    void* stream);

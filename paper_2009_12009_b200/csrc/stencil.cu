@@ -878,6 +878,10 @@ __global__ void k_domain_bc(const BoxGeom* __restrict__ geo, const FabView* __re
       int src[3] = {gidx[0], gidx[1], gidx[2]};
       src[axis] = edge;
       v = x[addr(src)];
+    } else if (cond == 3) {  // value * the cell mirrored across the face
+      int src[3] = {gidx[0], gidx[1], gidx[2]};
+      src[axis] = side == 0 ? 2 * dlo - 1 - gidx[axis] : 2 * dhi + 1 - gidx[axis];
+      v = value * x[addr(src)];
     }
     x[addr(gidx)] = v;
   }

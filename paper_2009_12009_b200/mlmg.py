@@ -167,7 +167,13 @@ class MLMG:
         for dom, lba, kind in mg_hierarchy(geom.domain, ba, nranks=dm.nranks if self.dist else 1,
                                            agg_cells=agg_cells):
             lv = _Level()
+            lv.index = len(self.levels)
             lv.domain, lv.ba, lv.kind = dom, lba, kind
+            # cells outside [lo, hi] are never relaxed (the sweeps' ghost ring at
+            # an 'external' face); unbounded along periodic axes
+            lv.fixed = None if self.all_periodic else i32p(
+                [dom.lo[d] if not geom.periodic[d] else -(1 << 30) for d in range(3)]
+                + [dom.hi[d] if not geom.periodic[d] else (1 << 30) for d in range(3)])
             lv.replicated = kind in ("agglom", "single")
             lv.dm = dm if not lv.replicated else DistributionMapping([0], dm.nranks)
             cs = [(h - l) / e for l, h, e in zip(geom.prob_lo, geom.prob_hi, dom.extents())]
@@ -192,7 +198,7 @@ class MLMG:
         # coarse tail: the longest suffix of single-box levels that fits one CTA
         n = len(self.levels)
         self.tail = n
-        for t in range(n):
+        for t in range(n if self.all_periodic else 0):
             if all(self.levels[x].kind in ("agglom", "single") for x in range(t, n)) and _tail_bytes(
                 [(self.levels[x].domain, None, None) for x in range(t, n)]
             ) <= 200 * 1024 and n - t <= 8 and t > 0:
@@ -214,7 +220,7 @@ class MLMG:
                     and all(2 <= e <= 32 and e & (e - 1) == 0 for es in ext for e in es)
                     and all(ext[x][d] == 2 * ext[x + 1][d] for x in range(len(ext) - 1) for d in range(3)))
 
-        if (cluster_tail is None and os.environ.get("AMRB_CLUSTER_TAIL", "1") != "0") or cluster_tail:
+        if ((cluster_tail is None and os.environ.get("AMRB_CLUSTER_TAIL", "1") != "0") or cluster_tail) and self.tail < n:
             t = self.tail
             if 0 < t < n and _cl_chain(t):
                 self.cluster_tail = True
@@ -231,7 +237,7 @@ class MLMG:
         gmax = grid_level_cells if grid_level_cells is not None else int(
             os.environ.get("AMRB_GRID_LEVEL_CELLS", str(128**3 // 2)))
         self.grid_from = self.tail
-        for l in range(self.tail - 1, 0, -1) if self.tail < n else ():
+        for l in range(self.tail - 1, 0, -1) if self.tail < n and self.all_periodic else ():
             lv, nx = self.levels[l], self.levels[l + 1]
             ext = tuple(lv.domain.extents())
             if (len(lv.ba) == 1 and len(nx.ba) == 1 and (lv.replicated or not self.dist)
@@ -269,8 +275,10 @@ class MLMG:
         if fuse_prolong is None:  # AMRB_FUSE_PROLONG=0: separate prolongation (A/B runs)
             fuse_prolong = os.environ.get("AMRB_FUSE_PROLONG", "1") != "0"
         for l, lv in enumerate(self.levels):
+            # (the fused kernel adds the parent to every tile cell, ghosts
+            # included: periodic levels only)
             lv.fuse = (fuse_prolong and l < len(self.levels) - 1 and lv.boxlocal_next and not lv.push
-                       and self.nu2 >= 1)
+                       and self.nu2 >= 1 and self.all_periodic)
         self._ghost = {}  # id(field) -> ghost width known to be current
         self._pending = False  # pushes to peers since the last device barrier
         self._reads = set()  # fields whose ghosts were read since the last barrier
@@ -337,6 +345,23 @@ class MLMG:
         # next fill's barrier (or an NCCL collective), so one barrier per fill
         # suffices for the p2p path.
         fill_boundary(fa, self.transport, lv.domain, self.periodic, ngrow=width, _post_barrier=False)
+        if not self.all_periodic and lv.index > 0 and fa is not lv.rhs:
+            # coarse-level homogeneous Dirichlet: ghost = -alpha_l * mirror
+            # (oracle/mlmg_ref.py reflect_ghosts); the finest level's 'external'
+            # ghosts are set once (set_phi) and never overwritten
+            r = float(1 << lv.index)
+            self._domain_bc(lv, fa, 3, -((r - 1.0) / (r + 1.0)))
+
+    def _domain_bc(self, lv, fa, cond, value):
+        bc = np.zeros((3, 2), dtype=np.int32)
+        for d in range(3):
+            if not self.periodic[d]:
+                bc[d] = cond
+        dom = np.array(list(lv.domain.lo) + list(lv.domain.hi), dtype=np.int32)
+        _b, bp = i32p(bc.reshape(-1))
+        _d, dp = i32p(dom)
+        check(lib().amrb_domain_bc(level_of(fa).handle, field_of(fa).handle, C.c_void_p(fa.storage.data_ptr()),
+                                   fa.ncomp, dp, bp, float(value), stream_ptr()))
 
     def _sweep(self, lv):
         a = lv.phi[lv.cur]
@@ -353,7 +378,7 @@ class MLMG:
             field_of(lv.rhs).handle,
             C.c_void_p(lv.rhs.storage.data_ptr()),
             lv.dhc,
-            None,
+            None if lv.fixed is None else lv.fixed[1],
         )
         # The sweep does not push its ghosts: measured, the per-plane delta loads
         # compete with the kernel's own shared-memory pipe (k_gsrb_sweep5<PUSH>
@@ -590,6 +615,11 @@ class MLMG:
 
     def set_phi(self, phi):
         top = self.levels[0]
+        if not self.all_periodic:
+            # the finest level's 'external' ghosts (apply_domain_boundary), in
+            # both ping-pong buffers: no kernel writes them afterwards
+            for f in top.phi:
+                self._domain_bc(top, f, 1, self.bc.external_value)
         parallel_copy(top.phi[top.cur], phi, self.transport)
         # the captured cycle starts from current ghosts (its last sweep pushed them)
         self._produced(top.phi[top.cur], 0)

@@ -222,3 +222,43 @@ def test_noncubic_pow2_tail_matches_oracle(shape):
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
+
+
+@pytest.mark.parametrize("per,value,n,m", [((False, False, False), 0.0, 64, 32), ((True, False, False), 1.5, 64, 32),
+                                          ((False, True, False), -0.25, 48, 16), ((False, False, False), 0.5, 64, 64)])
+def test_external_boundary_solve_matches_oracle(per, value, n, m):
+    """Non-periodic MLMG: 'external' sides (BoundaryRecord, amr_core.py:73-108)
+    hold `value` in the finest level's ghosts; the coarse correction levels use
+    the level-consistent homogeneous ghosts of oracle/mlmg_ref.py
+    (reflect_ghosts).  Same iterations, history and bit-identical solution."""
+    dom = A.Box((0, 0, 0), (n - 1,) * 3)
+    ba = A.BoxArray([dom]).max_size(m)
+    dm = A.DistributionMapping.single_rank(len(ba))
+    geom = A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, per)
+    conds = tuple("periodic" if p else "external" for p in per)
+    bc = A.BoundaryRecord(conds, conds, value)
+    rng = np.random.default_rng(23)
+    rhs = rng.standard_normal((n, n, n))
+    ref = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), tboxes(ba), bc=(conds, conds, value)).solve(
+        rhs, rtol=1e-10, max_iter=60)
+    phi = A.MultiFab(ba, dm, 1, 1)
+    b = A.MultiFab(ba, dm, 1, 0)
+    b.load_valid_from(dom, rhs)
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), bc=bc)
+    assert mg.tail == len(mg.levels) and not any(lv.fuse for lv in mg.levels)
+    mg.solve(phi, b, rtol=1e-10, max_iter=60)
+    assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
+    assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
+
+
+def test_mlmg_boundary_arguments():
+    dom = A.Box((0, 0, 0), (31, 31, 31))
+    ba = A.BoxArray([dom])
+    dm = A.DistributionMapping.single_rank(1)
+    with pytest.raises(ValueError):  # non-periodic geometry without a record
+        A.MLMG(A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, False), ba, dm)
+    with pytest.raises(ValueError):  # extrap sides are not supported by the solver
+        A.MLMG(A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, False), ba, dm, bc=A.BoundaryRecord.all_extrap(3))
+    with pytest.raises(ValueError):  # record disagrees with the geometry's periodic flags
+        A.MLMG(A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, True), ba, dm,
+               bc=A.BoundaryRecord(("external",) * 3, ("external",) * 3))
