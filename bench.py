@@ -261,7 +261,9 @@ def run_ours(args):
     barrier()
     clk.__exit__(None, None, None)
     t_dev = maxover(e0.elapsed_time(e1) / 1e3)
-    launches = (lib().amrb_launch_count() - launches0) + (mg.graph_replays - replays0) * mg.launches_per_cycle
+    # eager launches (uploads, priming sweep, copies) + the captured iteration's
+    # launches times the iterations the device loop ran
+    launches = (lib().amrb_launch_count() - launches0) + sum(iters) * mg.launches_per_cycle
     # every level's smoother relaxations, counted once for the whole job (replicated
     # bottom levels run redundantly on every rank but are counted once)
     updates_job = mg.cell_updates_per_cycle * sum(iters)

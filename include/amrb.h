@@ -55,6 +55,24 @@ int amrb_version(void);
 /* Kernel launches issued so far by this process (host-side count; launches
  * replayed from a captured CUDA graph are not included). */
 int64_t amrb_launch_count(void);
+/* Device-side solve loop (csrc/graph.cu): a CUDA graph whose WHILE node
+ * repeats a captured body until its control kernel says stop.  Between
+ * amrb_loop_begin and amrb_loop_end every launch on `stream` is captured into
+ * the body; the body must end with amrb_loop_control, which appends *norm to
+ * the pinned host block's history, zeroes *norm, counts the iteration and
+ * continues while !(norm <= rtol * *r0) and iters < max_iter (the oracle's
+ * stopping test, oracle/mlmg_ref.py OracleMLMG.solve).  host_block: pinned
+ * host memory {double rtol; int32 max_iter; int32 iters; double hist[capacity]}
+ * read and written by the device through UVA; set rtol, max_iter and
+ * iters = 0 before amrb_loop_launch, synchronize, then read iters / hist. */
+typedef struct amrb_loop amrb_loop;
+int amrb_loop_begin(void* stream, amrb_loop** out);
+int amrb_loop_control(amrb_loop* loop, double* norm, const double* r0, void* host_block, int capacity,
+                      void* stream);
+int amrb_loop_end(amrb_loop* loop);
+int amrb_loop_launch(amrb_loop* loop, void* stream);
+int amrb_loop_destroy(amrb_loop* loop);
+
 /* Library options: process-wide, set explicitly by the caller (the library
  * reads no environment variables).  Names and defaults:
  *   "pdl"          2  programmatic dependent launch: 0 off, 1 always, 2 eager

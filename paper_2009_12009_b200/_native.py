@@ -37,6 +37,11 @@ _SIGS = {
     "amrb_last_error": (C.c_char_p, []),
     "amrb_version": (C.c_int, []),
     "amrb_launch_count": (i64, []),
+    "amrb_loop_begin": (C.c_int, [vp, P(vp)]),
+    "amrb_loop_control": (C.c_int, [vp, vp, vp, vp, C.c_int, vp]),
+    "amrb_loop_end": (C.c_int, [vp]),
+    "amrb_loop_launch": (C.c_int, [vp, vp]),
+    "amrb_loop_destroy": (C.c_int, [vp]),
     "amrb_set_option": (C.c_int, [C.c_char_p, i64]),
     "amrb_get_option": (C.c_int, [C.c_char_p, P(i64)]),
     "amrb_zero": (C.c_int, [vp, i64, vp]),

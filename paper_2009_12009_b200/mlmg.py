@@ -31,7 +31,7 @@ import os
 import numpy as np
 import torch
 
-from ._native import check, i32p, lib
+from ._native import AMRB_ENOTSUP, check, i32p, lib
 from .boxes import Box, IntVect
 from .comm import Transport, copy_into, device_reduce, fill_boundary, parallel_copy
 from .device import dh_array, field_of, level_of, stream_ptr
@@ -121,7 +121,8 @@ class _Level:
 
 
 def _zero(fa):
-    st = fa.storage
+    """Zero a FabArray's whole storage, or a device tensor (a memset node when captured)."""
+    st = fa if isinstance(fa, torch.Tensor) else fa.storage
     check(lib().amrb_zero(C.c_void_p(st.data_ptr()), st.numel(), stream_ptr()))
 
 
@@ -288,7 +289,12 @@ class MLMG:
         # memory (amrb_store_host): no copy-engine transfer to queue behind the
         # caller's bulk copies on other streams
         self.norm_host = torch.zeros(1, dtype=torch.float64).pin_memory()
-        self.graph = None
+        self.r0_dev = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
+        # pinned block shared with the loop's control kernel (csrc/graph.cu):
+        # rtol, (max_iter, iters), history
+        self.loop_host = torch.zeros(2 + self._HIST, dtype=torch.float64).pin_memory()
+        self.lag = None  # decided by the first _prime()
+        self._loop = None
         self.graph_replays = 0
         self.launches_per_cycle = 0
         self.iterations = 0
@@ -363,7 +369,11 @@ class MLMG:
         check(lib().amrb_domain_bc(level_of(fa).handle, field_of(fa).handle, C.c_void_p(fa.storage.data_ptr()),
                                    fa.ncomp, dp, bp, float(value), stream_ptr()))
 
-    def _sweep(self, lv):
+    def _sweep(self, lv, norm=None):
+        """One fused sweep lv.phi[cur] -> lv.phi[1-cur]; with ``norm`` (a
+        1-element device tensor) the kernel also max-reduces |rhs - L(phi)| of
+        its INPUT into it (NotImplementedError, nothing launched, where the
+        level does not take the streaming kernel)."""
         a = lv.phi[lv.cur]
         b = lv.phi[1 - lv.cur]
         self._need_ghosts(lv, a, 2)
@@ -380,11 +390,13 @@ class MLMG:
             lv.dhc,
             None if lv.fixed is None else lv.fixed[1],
         )
-        # The sweep does not push its ghosts: measured, the per-plane delta loads
-        # compete with the kernel's own shared-memory pipe (k_gsrb_sweep5<PUSH>
-        # 163-175 us vs 112 us for fill + sweep on the C3 fine level), so the
-        # next consumer fills.  amrb_gsrb_sweep_push stays available (tests).
-        check(lib().amrb_gsrb_sweep(*args, stream_ptr()))
+        if norm is None:
+            check(lib().amrb_gsrb_sweep(*args, stream_ptr()))
+        else:
+            rc = lib().amrb_gsrb_sweep_norm(*args, C.c_void_p(norm.data_ptr()), stream_ptr())
+            if rc == AMRB_ENOTSUP:
+                raise NotImplementedError("level does not take the streaming sweep")
+            check(rc)
         self._produced(b, 0)
         lv.cur = 1 - lv.cur
 
@@ -487,7 +499,6 @@ class MLMG:
                 stream_ptr(),
             )
         )
-        self._allmax(self.norm)
 
     def _allmax(self, t):
         if self.dist and self.transport.p2p:
@@ -542,7 +553,10 @@ class MLMG:
         if not up:
             self._produced(nx.rhs, 0)
 
-    def vcycle(self):
+    def vcycle(self, first_done=False):
+        """One V(nu1, nu2) cycle; first_done: the finest level's first
+        pre-smoothing sweep already ran (the previous iteration's fused
+        sweep + residual norm)."""
         L = self.levels
         n = len(L)
         T = self.tail  # first level handled by the coarse-tail kernel (n: none)
@@ -555,7 +569,7 @@ class MLMG:
             if l == n - 1:
                 self._smooth(lv, self.bottom_sweeps)
                 break
-            self._smooth(lv, self.nu1)
+            self._smooth(lv, self.nu1 - (1 if l == 0 and first_done else 0))
             self._resid_restrict(l)
         for l in range(G, T):
             self._level_grid(l, up=False)
@@ -570,11 +584,41 @@ class MLMG:
                 self._prolong(l)
                 self._smooth(L[l], self.nu2)
 
-    def _cycle_and_norm(self):
-        self.vcycle()
-        self._residual_norm()
-        check(lib().amrb_store_host(C.c_void_p(self.norm.data_ptr()), C.c_void_p(self.norm_host.data_ptr()), 1,
-                                    stream_ptr()))
+    # -- one solve iteration -------------------------------------------------------
+    # Lagged norm (self.lag): the residual of a cycle's result is the residual of
+    # the INPUT of the next cycle's first pre-smoothing sweep, which the fused
+    # sweep computes from the phi / rhs it streams anyway (amrb_gsrb_sweep_norm).
+    # So an iteration is "the rest of cycle n + the first sweep of cycle n+1 with
+    # the norm of cycle n's result"; the sweep is out of place, so when the test
+    # says stop, cycle n's solution is intact in the sweep's input buffer.  This
+    # removes the separate residual-norm pass over the finest level (16 N bytes
+    # per cycle).  Without the streaming sweep (or nu1 == 0) the iteration is the
+    # whole cycle followed by the residual-norm kernel.
+    def _body(self):
+        if self.lag:
+            self.vcycle(first_done=True)
+            self._sweep(self.levels[0], norm=self.norm)
+        else:
+            self.vcycle()
+            self._residual_norm()
+        self._allmax(self.norm)
+
+    def _solution_index(self):
+        top = self.levels[0]
+        return 1 - top.cur if self.lag else top.cur
+
+    def _prime(self):
+        """Before the first iteration: the lagged scheme runs the first
+        pre-smoothing sweep of cycle 1 (its norm, of phi0, is discarded).  The
+        first call decides whether the finest level takes the fused sweep +
+        norm kernel at all (self.lag)."""
+        if self.nu1 >= 1 and self.lag is not False:
+            try:
+                self._sweep(self.levels[0], norm=self.norm)
+                self.lag = True
+            except NotImplementedError:
+                self.lag = False
+        _zero(self.norm)
 
     def _host_scalar(self, t):
         """t (1-element device tensor) -> float via the pinned mailbox."""
@@ -583,28 +627,55 @@ class MLMG:
         torch.cuda.current_stream().synchronize()
         return float(self.norm_host[0])
 
-    # -- graph capture -------------------------------------------------------------
+    # -- the device-side solve loop -------------------------------------------------
+    _HIST = 4096  # capacity of the residual history (max_iter is capped to it)
+
     def _capture(self):
-        """Warm up (lazy native tables, programs, scratch) then capture one cycle."""
+        """Warm up (lazy native tables, copy programs, scratch) on zeroed state,
+        then capture one iteration into the body of a WHILE-node graph
+        (csrc/graph.cu): a solve is one graph launch + one synchronisation."""
+        for lv in self.levels:
+            for f in lv.phi + [lv.rhs]:
+                f.storage.zero_()
+                self._produced(f, f.ngrow)
         saved = [lv.cur for lv in self.levels]
-        self._cycle_and_norm()  # eager warm-up on the current data
+        self._prime()
+        self._body()
+        self._body()  # both iterations start from the same state
         torch.cuda.synchronize()
-        for lv, c in zip(self.levels, saved):
-            lv.cur = c
-        g = torch.cuda.CUDAGraph()
+        start = [lv.cur for lv in self.levels]
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
+        loop = C.c_void_p()
         with torch.cuda.stream(s):
-            # relaxed: NCCL's proxy thread keeps making CUDA calls during capture
-            with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
-                self._cap_l0 = int(lib().amrb_launch_count())
-                self._cycle_and_norm()
+            check(lib().amrb_loop_begin(stream_ptr(), C.byref(loop)))
+            try:
+                l0 = int(lib().amrb_launch_count())
+                self._body()
+                check(lib().amrb_loop_control(loop, C.c_void_p(self.norm.data_ptr()),
+                                              C.c_void_p(self.r0_dev.data_ptr()),
+                                              C.c_void_p(self.loop_host.data_ptr()), self._HIST, stream_ptr()))
+                self.launches_per_cycle = int(lib().amrb_launch_count()) - l0  # incl. the control kernel
+            except BaseException:
+                lib().amrb_loop_destroy(loop)
+                raise
+            check(lib().amrb_loop_end(loop))
         torch.cuda.current_stream().wait_stream(s)
-        self.launches_per_cycle = int(lib().amrb_launch_count()) - self._cap_l0
-        self._graph_cur = [lv.cur for lv in self.levels]
+        if [lv.cur for lv in self.levels] != start:
+            lib().amrb_loop_destroy(loop)
+            raise RuntimeError("captured iteration does not return the level buffers to their start state")
+        self._loop = loop
+        self._loop_cur = start
         for lv, c in zip(self.levels, saved):
             lv.cur = c
-        return g
+
+    def __del__(self):
+        loop = getattr(self, "_loop", None)
+        if loop is not None:
+            try:
+                lib().amrb_loop_destroy(loop)
+            except Exception:
+                pass
 
     # -- public API ----------------------------------------------------------------------
     def set_rhs(self, rhs):
@@ -621,47 +692,63 @@ class MLMG:
             for f in top.phi:
                 self._domain_bc(top, f, 1, self.bc.external_value)
         parallel_copy(top.phi[top.cur], phi, self.transport)
-        # the captured cycle starts from current ghosts (its last sweep pushed them)
         self._produced(top.phi[top.cur], 0)
         self._need_ghosts(top, top.phi[top.cur], 2)
 
     def get_phi(self, phi):
         top = self.levels[0]
-        parallel_copy(phi, top.phi[top.cur], self.transport)
+        parallel_copy(phi, top.phi[self._solution_index()], self.transport)
 
     def solve(self, phi, rhs, rtol=1e-10, max_iter=200):
-        """Solve L(phi) = rhs to ||r||_inf <= rtol * ||rhs||_inf; phi is the initial guess."""
+        """Solve L(phi) = rhs to ||r||_inf <= rtol * ||rhs||_inf; phi is the
+        initial guess and receives the solution.  Returns the final ||r||_inf;
+        ``iterations``, ``history`` and ``r0`` are left on the solver."""
+        max_iter = int(max_iter)
+        if max_iter < 0 or max_iter > self._HIST:
+            raise ValueError(f"max_iter must be in [0, {self._HIST}]")
         top = self.levels[0]
-        # the warm-up cycle inside capture runs on scratch state: zero everything first
-        if self.use_graph and self.graph is None:
-            for lv in self.levels:
-                for f in lv.phi + [lv.rhs]:
-                    f.storage.zero_()
-                    self._produced(f, f.ngrow)
-            self.graph = self._capture()
+        if self.use_graph and self._loop is None:
+            self._capture()
         self.set_rhs(rhs)
         self.set_phi(phi)
         r0t = device_reduce(top.rhs, "absmax", 0)
         self._allmax(r0t)
-        r0 = self._host_scalar(r0t)
+        self.r0_dev.copy_(r0t)
         self.history = []
         self.iterations = 0
-        rn = r0
-        while self.iterations < max_iter:
-            if self.graph is not None:
-                self.graph.replay()
-                self.graph_replays += 1
-                for lv, c in zip(self.levels, self._graph_cur):
-                    lv.cur = c
-            else:
-                self._cycle_and_norm()
-            self.iterations += 1
+        if max_iter == 0:
+            self.r0 = self._host_scalar(self.r0_dev)
+            self.get_phi(phi)
+            return self.r0
+        self._prime()
+        if self._loop is not None:
+            for lv, c in zip(self.levels, self._loop_cur):
+                lv.cur = c
+            h = self.loop_host
+            h[0] = float(rtol)
+            hi = h.view(torch.int32)
+            hi[2] = max_iter
+            hi[3] = 0
+            check(lib().amrb_loop_launch(self._loop, stream_ptr()))
+            self.graph_replays += 1
+            check(lib().amrb_store_host(C.c_void_p(self.r0_dev.data_ptr()), C.c_void_p(self.norm_host.data_ptr()),
+                                        1, stream_ptr()))
             torch.cuda.current_stream().synchronize()
-            rn = float(self.norm_host[0])
-            self.history.append(rn)
-            if rn <= rtol * r0:
-                break
-        self.r0 = r0
+            self.r0 = float(self.norm_host[0])
+            self.iterations = int(hi[3])
+            self.history = [float(x) for x in h[2:2 + self.iterations].tolist()]
+            rn = self.history[-1]
+        else:
+            self.r0 = r0 = self._host_scalar(self.r0_dev)
+            rn = r0
+            while self.iterations < max_iter:
+                self._body()
+                self.iterations += 1
+                rn = self._host_scalar(self.norm)
+                _zero(self.norm)
+                self.history.append(rn)
+                if rn <= rtol * r0:
+                    break
         self.get_phi(phi)
         return rn
 
