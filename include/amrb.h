@@ -88,12 +88,27 @@ int amrb_loop_destroy(amrb_loop* loop);
  * AMRB_EINVAL for an unknown name. */
 int amrb_set_option(const char* name, int64_t value);
 int amrb_get_option(const char* name, int64_t* value);
+/* ptr[0..n) = value (one kernel). */
+int amrb_fill(double* ptr, int64_t n, double value, void* stream);
 /* Zero n doubles (cudaMemsetAsync on `stream`; a memset node in a graph). */
 int amrb_zero(double* ptr, int64_t n, void* stream);
 /* host_dst[0..n) <- src (device) by a kernel storing through UVA into pinned
  * host memory: small results reach the host without a copy-engine transfer
  * (which would queue behind bulk copies).  Synchronize the stream to read. */
 int amrb_store_host(const double* src, double* host_dst, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Box -> rank assignment (host; distribution.py:19-148).  lohi = int32     */
+/* [n][2*dim] (lo then hi per box).                                          */
+/* ------------------------------------------------------------------------ */
+/* morton_key: bit k of axis d of (point - origin) -> key bit k*dim + d. */
+int amrb_morton_key(int dim, const int32_t* point, const int32_t* origin, uint64_t* key);
+/* sfc_distribute (distribution.py:97-131): box centres (lo+hi)//2 in Morton
+ * order, contiguous runs of ~equal cost; `total` = the caller's sum of cost. */
+int amrb_sfc_distribute(int dim, int n, const int32_t* lohi, const double* cost, double total,
+                        int nranks, int32_t* owner);
+/* knapsack_distribute (distribution.py:134-148): longest processing time. */
+int amrb_knapsack_distribute(int n, const double* cost, int nranks, int32_t* owner);
 
 /* ------------------------------------------------------------------------ */
 /* Communication plans (host).  Records are CopyRecord(src, dst, src_box,    */
@@ -371,10 +386,15 @@ int amrb_residual_norm(const amrb_level* lv, const amrb_field* rhs,
  * [nlev][6] (3-D padded), dh = double[nlev][3].  Reads level-0 rhs (valid) from
  * `rhs`, runs zero/nu1 sweeps/residual-restrict down to the bottom (nbottom
  * sweeps), pc-prolong + nu2 sweeps back up, and writes level-0 phi (valid).
- * Bit-identical to the per-level kernels / oracle. */
+ * Bit-identical to the per-level kernels / oracle.  cluster: 0 one-CTA kernels
+ * only, 1 an 8-CTA cluster kernel (which also runs a 32^3 top level) for cubic
+ * power-of-two chains, 2 also for 32 x n1 x n2 chains.  *ghosts_written
+ * (nullable) = the ghost width of level-0 phi the launched kernel left current
+ * (1 for the cluster kernel, else 0). */
 int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
                      const amrb_field* rhs, const double* rhs_base, amrb_field* phi,
-                     double* phi_base, int nu1, int nu2, int nbottom, void* stream);
+                     double* phi_base, int nu1, int nu2, int nbottom, int cluster,
+                     int32_t* ghosts_written, void* stream);
 
 /* One single-box periodic MLMG level's half V-cycle in one grid-synchronised
  * (cooperative) launch -- the per-level steps of the reference-semantics
@@ -396,6 +416,12 @@ int amrb_level_grid(int up, const int32_t* lohi, const double* dh, const amrb_fi
  * is written to dev_out. */
 int amrb_reduce(const amrb_level* lv, const amrb_field* x, const double* x_base,
                 int comp, int kind, double* dev_out, void* stream);
+
+/* setval (fabarray.py:119-122, Fab.setval :58-65): components [comp0, comp1)
+ * of box `box` (-1: every resident box) = value: ghosts 0 the valid cells,
+ * 1 the grown box, 2 the ghost cells only. */
+int amrb_setval(const amrb_level* lv, amrb_field* f, double* base, int box, int comp0, int comp1,
+                int ghosts, double value, void* stream);
 
 /* Fill ghost cells outside the physical domain (apply_domain_boundary,
  * amr_core.py:111-146).  bc: int32[3][2] per (axis, side) 0 periodic/skip,

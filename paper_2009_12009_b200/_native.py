@@ -45,7 +45,12 @@ _SIGS = {
     "amrb_set_option": (C.c_int, [C.c_char_p, i64]),
     "amrb_get_option": (C.c_int, [C.c_char_p, P(i64)]),
     "amrb_zero": (C.c_int, [vp, i64, vp]),
+    "amrb_fill": (C.c_int, [vp, i64, f64, vp]),
+    "amrb_setval": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, f64, vp]),
     "amrb_store_host": (C.c_int, [vp, vp, i64, vp]),
+    "amrb_morton_key": (C.c_int, [C.c_int, P(i32), P(i32), P(C.c_uint64)]),
+    "amrb_sfc_distribute": (C.c_int, [C.c_int, C.c_int, P(i32), P(f64), f64, C.c_int, P(i32)]),
+    "amrb_knapsack_distribute": (C.c_int, [C.c_int, P(f64), C.c_int, P(i32)]),
     "amrb_plan_fill_create": (C.c_int, [C.c_int, C.c_int, P(i32), C.c_int, P(i32), P(C.c_uint8), P(vp)]),
     "amrb_plan_copy_create": (
         C.c_int,
@@ -94,7 +99,8 @@ _SIGS = {
     "amrb_prolong_push": (C.c_int, [vp, vp, vp, vp, vp, P(i32), C.c_int, vp, P(C.c_uint64), C.c_int, vp]),
     "amrb_reduce": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
     "amrb_residual_norm": (C.c_int, [vp, vp, vp, vp, vp, P(f64), vp, vp]),
-    "amrb_coarse_tail": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    "amrb_coarse_tail": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   P(i32), vp]),
     "amrb_level_grid": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, vp, vp, C.c_int, vp]),
     "amrb_domain_bc": (C.c_int, [vp, vp, vp, C.c_int, P(i32), P(i32), f64, vp]),
     "amrb_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),

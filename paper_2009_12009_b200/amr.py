@@ -178,7 +178,7 @@ def fill_patch(dst, fine_src, crse_old, crse_new, time_weight, ratio, transport,
     gc = -(-dst.ngrow // max(min(tuple(ratio)), 1)) + max(margin, 1)
     cdomain = domain.coarsen(ratio) if domain is not None else None
     stage = _scratch(dst, coarsened_layout(dst.ba, ratio), gc, "fp_stage")
-    stage.storage.fill_(float("nan"))
+    stage.setval(float("nan"))
     copy_into(stage, blended, transport, include_dst_ghosts=True, domain=cdomain, periodic=periodic)
     prefix, boxes, nb, total = _work(dst, "grown")
     r3 = [1, 1, 1]

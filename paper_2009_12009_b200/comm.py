@@ -118,9 +118,15 @@ class Transport:
             # pads start at zero; make sure every rank sees that before the first barrier
             self._bar.barrier()
             torch.cuda.synchronize()
-            self.p2p = True
+            ok = True
         except Exception:  # no symmetric memory on this system: NCCL send/recv only
-            self.p2p = False
+            ok = False
+        # every rank must take the same path: enable p2p only if it worked everywhere
+        import torch.distributed as dist
+
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        self.p2p = bool(flag.item())
 
     def peer_allmax(self, t):
         """t (1-element float64 CUDA tensor) <- max over ranks, over NVLink."""
@@ -331,9 +337,7 @@ def sum_boundary(fa, transport, domain, periodic=None):
         return
     plan = build_plan_sum_boundary(fa.ba, fa.ngrow, domain, periodic)
     _execute(plan, fa, fa, transport, 1)
-    for f in fa.fabs.values():
-        for piece in box_diff(f.gbox, f.box):
-            f.slice(piece).zero_()
+    fa._setval_boxes(0.0, None, ghosts=2)  # ghost cells only (setval kernel)
 
 
 _KINDS = {"sum": 0, "min": 1, "max": 2, "absmax": 3}
@@ -362,6 +366,10 @@ def reduce(fa, kind, comp, transport):
         raise ValueError(f"unknown reduction {kind!r}")
     if not 0 <= comp < fa.ncomp:
         raise ValueError("component out of range")
+    if transport.mode == "nccl" and (not fa.distributed or fa.dm.nranks != transport.nranks):
+        # a replicated (or undistributed) FabArray holds every box on every rank:
+        # summing the per-rank partials would count each box nranks times
+        raise ValueError("reduce over NCCL needs a FabArray distributed over the transport's ranks")
     out = device_reduce(fa, kind, comp)
     if transport.mode == "nccl":
         check(

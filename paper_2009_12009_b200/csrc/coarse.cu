@@ -768,8 +768,10 @@ using namespace amrb;
 
 extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh, const amrb_field* rhs,
                                 const double* rhs_base, amrb_field* phi, double* phi_base, int nu1, int nu2,
-                                int nbottom, void* stream) {
+                                int nbottom, int cluster, int32_t* ghosts_written, void* stream) {
   return guarded([&] {
+    if (cluster < 0 || cluster > 2) throw Error(AMRB_EINVAL, "amrb_coarse_tail: cluster must be 0, 1 or 2");
+    if (ghosts_written) *ghosts_written = 0;
     if (nlev < 1 || nlev > kMaxTail || !lohi || !dh || !rhs || !phi)
       throw Error(AMRB_EINVAL, "amrb_coarse_tail: bad arguments");
     const Field& fr = *reinterpret_cast<const Field*>(rhs);
@@ -821,11 +823,11 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
     const int n0 = a.lv[0].n[0];
     // 32 x n1 x n2 top level (n1, n2 powers of two <= 32) halving per level
     // down to extents >= 2: the top level on a cluster, the chain below in CTA 0
-    // (AMRB_CLUSTER_TAIL=0 keeps the one-CTA kernels, for A/B runs).  Default:
-    // cubic chains only -- the non-cubic top levels (AMRB_CLUSTER_TAIL=2) are
+    // (cluster = 0 keeps the one-CTA kernels, for A/B runs).  Default (1):
+    // cubic chains only -- the non-cubic top levels (cluster = 2) are
     // bit-identical but measured slower than k_coarse_tail_p2x (C4 weak
     // scaling, 2 GPUs 10.18 -> 10.35 ms, 4 GPUs 10.99 -> 11.02 ms)
-    static const int cl_mode = getenv("AMRB_CLUSTER_TAIL") ? atoi(getenv("AMRB_CLUSTER_TAIL")) : 1;
+    const int cl_mode = cluster;
     bool cl = cl_mode != 0 && n0 == kClN && nlev >= 2 && fp.ng3[0] >= 1 && fp.ng3[1] >= 1 && fp.ng3[2] >= 1;
     for (int l = 0; l < nlev && cl; ++l)
       for (int x = 0; x < 3; ++x) {
@@ -855,6 +857,7 @@ extern "C" int amrb_coarse_tail(int nlev, const int32_t* lohi, const double* dh,
         AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         launch_k(kern, kClCtas, kTailThreads, b2, (cudaStream_t)stream, a, slab_off, cubic ? 1 : 0);
         check_launch("k_coarse_tail_cl");
+        if (ghosts_written) *ghosts_written = 1;  // the cluster kernel leaves the top phi's width-1 ghosts current
         return;
       }
     }

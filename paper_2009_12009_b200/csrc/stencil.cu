@@ -887,6 +887,36 @@ __global__ void k_domain_bc(const BoxGeom* __restrict__ geo, const FabView* __re
   }
 }
 
+// setval (fabarray.py:119-122 / Fab.setval :58-65) over every resident box:
+// components [c0, c1), the valid box grown by `grow` cells per axis.
+__global__ void k_setval(const BoxGeom* __restrict__ geo, const FabView* __restrict__ fv, double* __restrict__ x,
+                         int nboxes, int box, int3 grow, int c0, int c1, double value, int ghosts_only) {
+  pdl_entry();
+  const int b = box >= 0 ? box : blockIdx.y;
+  if (b >= nboxes) return;
+  const BoxGeom g = geo[b];
+  const FabView F = fv[b];
+  const int e0 = g.n[0] + 2 * grow.x, e1 = g.n[1] + 2 * grow.y, e2 = g.n[2] + 2 * grow.z;
+  const int64_t plane = (int64_t)e1 * e2, cells = (int64_t)e0 * plane;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cells * (c1 - c0);
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = c0 + (int)(t / cells);
+    int64_t r = t - (int64_t)(c - c0) * cells;
+    const int i = (int)(r / plane) - grow.x;
+    r -= (int64_t)(i + grow.x) * plane;
+    const int j = (int)(r / e2) - grow.y;
+    const int k = (int)(r - (int64_t)(j + grow.y) * e2) - grow.z;
+    if (ghosts_only && i >= 0 && i < g.n[0] && j >= 0 && j < g.n[1] && k >= 0 && k < g.n[2]) continue;
+    x[F.off + (int64_t)c * F.cs + (int64_t)i * F.s0 + (int64_t)j * F.s1 + k] = value;
+  }
+}
+
+__global__ void k_fill(double* __restrict__ x, int64_t n, double value) {
+  pdl_entry();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    x[t] = value;
+}
+
 const Level& L(const amrb_level* p) {
   if (!p) throw Error(AMRB_EINVAL, "null level");
   return *reinterpret_cast<const Level*>(p);
@@ -951,6 +981,33 @@ extern "C" int amrb_store_host(const double* src, double* host_dst, int64_t n, v
     if (!n) return;
     amrb::launch_k(amrb::k_store_host, 1, 32, 0, (cudaStream_t)stream, src, host_dst, n);
     amrb::check_launch("k_store_host");
+  });
+}
+
+extern "C" int amrb_fill(double* ptr, int64_t n, double value, void* stream) {
+  return amrb::guarded([&] {
+    if (n < 0 || (n && !ptr)) throw amrb::Error(AMRB_EINVAL, "amrb_fill: bad arguments");
+    if (!n) return;
+    const long long blocks = std::min<long long>((n + 255) / 256, 8LL * amrb::num_sms());
+    amrb::launch_k(amrb::k_fill, (unsigned)blocks, 256, 0, (cudaStream_t)stream, ptr, n, value);
+    amrb::check_launch("k_fill");
+  });
+}
+
+extern "C" int amrb_setval(const amrb_level* lv_, amrb_field* f, double* base, int box, int comp0, int comp1,
+                           int ghosts, double value, void* stream) {
+  return amrb::guarded([&] {
+    const amrb::Level& lv = amrb::L(lv_);
+    const amrb::Field& fld = amrb::F(f);
+    amrb::need_same_level(fld, lv, "setval");
+    if (comp0 < 0 || comp1 < comp0) throw amrb::Error(AMRB_EINVAL, "setval: bad component range");
+    if (box >= lv.nboxes || (box >= 0 && !lv.resident[box])) throw amrb::Error(AMRB_EINVAL, "setval: box not resident");
+    if (lv.nboxes == 0 || comp1 == comp0) return;
+    if (ghosts < 0 || ghosts > 2) throw amrb::Error(AMRB_EINVAL, "setval: ghosts must be 0, 1 or 2");
+    const int3 gw = ghosts ? make_int3(fld.ng3[0], fld.ng3[1], fld.ng3[2]) : make_int3(0, 0, 0);
+    amrb::launch_k(amrb::k_setval, dim3(box >= 0 ? 64 : 16, box >= 0 ? 1 : lv.nboxes), 256, 0, (cudaStream_t)stream,
+                   lv.dgeo.p, fld.dev.p, base, lv.nboxes, box, gw, comp0, comp1, value, ghosts == 2 ? 1 : 0);
+    amrb::check_launch("k_setval");
   });
 }
 

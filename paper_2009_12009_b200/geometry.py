@@ -19,80 +19,93 @@ from .device import field_of, level_of, stream_ptr
 __all__ = ["Geometry", "BoundaryRecord", "apply_domain_boundary"]
 
 
+def _periodic_flags(periodic, dim):
+    """None -> all False, a bool -> the same for every axis, else per axis."""
+    if periodic is None or isinstance(periodic, bool):
+        return (bool(periodic),) * dim
+    flags = tuple(bool(p) for p in periodic)
+    if len(flags) != dim:
+        raise ValueError(f"periodic needs {dim} flags")
+    return flags
+
+
 class Geometry:
-    """Maps a level's index space to physical coordinates."""
+    """One level's index space mapped onto the physical box [prob_lo, prob_hi]:
+    cell (lo + i) spans prob_lo + [i, i+1) * cell_size per axis, with
+    cell_size = (prob_hi - prob_lo) / extent (amr_core.py:37-40, the value the
+    MLMG operator's 1/dx^2 is formed from)."""
 
     __slots__ = ("domain", "prob_lo", "prob_hi", "cell_size", "periodic")
 
     def __init__(self, domain, prob_lo, prob_hi, periodic=None):
         if not domain.ixtype.is_cell():
-            raise ValueError("domain must be cell-typed")
-        self.domain = domain
-        self.prob_lo = tuple(float(x) for x in prob_lo)
-        self.prob_hi = tuple(float(x) for x in prob_hi)
-        ext = domain.extents()
-        self.cell_size = tuple((h - l) / e for l, h, e in zip(self.prob_lo, self.prob_hi, ext))
-        if any(cs <= 0 for cs in self.cell_size):
-            raise ValueError("physical extents must be positive")
-        if periodic is None:
-            periodic = (False,) * domain.dim
-        elif isinstance(periodic, bool):
-            periodic = (periodic,) * domain.dim
-        self.periodic = tuple(bool(p) for p in periodic)
+            raise ValueError("a Geometry's domain must be cell-centred")
+        lo = tuple(map(float, prob_lo))
+        hi = tuple(map(float, prob_hi))
+        widths = [b - a for a, b in zip(lo, hi)]
+        sizes = tuple(w / n for w, n in zip(widths, domain.extents()))
+        if not all(c > 0 for c in sizes):
+            raise ValueError("the physical box must have positive extent on every axis")
+        self.domain, self.prob_lo, self.prob_hi = domain, lo, hi
+        self.cell_size = sizes
+        self.periodic = _periodic_flags(periodic, domain.dim)
 
     @property
     def dim(self):
         return self.domain.dim
 
+    def _with_domain(self, dom):
+        return Geometry(dom, self.prob_lo, self.prob_hi, self.periodic)
+
     def refine(self, ratio):
-        return Geometry(self.domain.refine(ratio), self.prob_lo, self.prob_hi, self.periodic)
+        return self._with_domain(self.domain.refine(ratio))
 
     def coarsen(self, ratio):
-        return Geometry(self.domain.coarsen(ratio), self.prob_lo, self.prob_hi, self.periodic)
+        return self._with_domain(self.domain.coarsen(ratio))
 
     def cell_center(self, iv):
-        return tuple(
-            self.prob_lo[d] + (iv[d] - self.domain.lo[d] + 0.5) * self.cell_size[d] for d in range(self.dim)
-        )
+        return tuple(p0 + (i - l + 0.5) * h
+                     for p0, i, l, h in zip(self.prob_lo, iv, self.domain.lo, self.cell_size))
 
     def cell_index(self, point):
-        return IntVect(
-            self.domain.lo[d] + int(np.floor((point[d] - self.prob_lo[d]) / self.cell_size[d]))
-            for d in range(self.dim)
-        )
+        return IntVect(l + int(np.floor((x - p0) / h))
+                       for l, x, p0, h in zip(self.domain.lo, point, self.prob_lo, self.cell_size))
 
     def __repr__(self):
         return f"Geometry({self.domain!r}, dx={self.cell_size}, periodic={self.periodic})"
 
 
 class BoundaryRecord:
-    """Per (dimension, side) condition: 'periodic', 'external' (value) or 'extrap'."""
+    """Physical boundary condition for each (dimension, side): 'periodic',
+    'external' (ghosts take ``external_value``) or 'extrap' (ghosts copy the
+    nearest in-domain plane) -- amr_core.py:73-108."""
 
     CONDITIONS = ("periodic", "external", "extrap")
 
     def __init__(self, lo, hi, external_value=0.0):
-        self.lo = tuple(lo)
-        self.hi = tuple(hi)
+        self.lo, self.hi = tuple(lo), tuple(hi)
+        bad = [c for c in self.lo + self.hi if c not in self.CONDITIONS]
+        if bad:
+            raise ValueError(f"unknown boundary condition {bad[0]!r}")
         self.external_value = float(external_value)
-        for c in self.lo + self.hi:
-            if c not in self.CONDITIONS:
-                raise ValueError(f"unknown boundary condition {c!r}")
 
-    @staticmethod
-    def all_periodic(dim):
-        return BoundaryRecord(("periodic",) * dim, ("periodic",) * dim)
+    @classmethod
+    def all_periodic(cls, dim):
+        return cls(["periodic"] * dim, ["periodic"] * dim)
 
-    @staticmethod
-    def all_extrap(dim):
-        return BoundaryRecord(("extrap",) * dim, ("extrap",) * dim)
+    @classmethod
+    def all_extrap(cls, dim):
+        return cls(["extrap"] * dim, ["extrap"] * dim)
+
+    def sides(self, d):
+        return self.lo[d], self.hi[d]
 
     def check_against(self, geom):
-        for d in range(geom.dim):
-            per = self.lo[d] == "periodic" or self.hi[d] == "periodic"
-            if per != geom.periodic[d]:
-                raise ValueError(
-                    f"dimension {d}: boundary record says periodic={per} but geometry says {geom.periodic[d]}"
-                )
+        """The record's periodic dimensions must be the geometry's."""
+        for d, want in enumerate(geom.periodic):
+            says = "periodic" in self.sides(d)
+            if says != want:
+                raise ValueError(f"dimension {d}: the boundary record is periodic={says}, the geometry {want}")
         return True
 
 

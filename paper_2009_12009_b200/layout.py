@@ -9,6 +9,8 @@ Behaviour mirrors the reference's layout layer:
   query of up to twice a box examines at most 3**D bins (:216-278).
 * DistributionMapping / sfc_distribute / knapsack_distribute / load_stats --
   /root/reference/pkg/src/amrkit/distribution.py:19-178.  Rank == GPU here.
+  The Morton keys, the SFC split and the knapsack run in libamrb
+  (csrc/distribute.cpp); this module packs the box table and wraps them.
 
 The box table is also kept as a contiguous int32 ``lohi`` array (lo then hi
 per box) because that is what the C-ABI plan builders consume.
@@ -16,10 +18,11 @@ per box) because that is what the C-ABI plan builders consume.
 
 from __future__ import annotations
 
-import heapq
+import ctypes as C
 import itertools
 import threading
 from collections import defaultdict
+from collections.abc import Sequence
 
 import numpy as np
 
@@ -98,74 +101,70 @@ class BoxHash(_Bins):
         super().__init__(ba.boxes)
 
 
-class BoxArray:
-    """Ordered, pairwise-disjoint boxes of one index type; immutable."""
+class BoxArray(Sequence):
+    """Ordered, pairwise-disjoint boxes of one index type; immutable.
+
+    A read-only sequence of Box; ``uid`` (fresh per instance) keys the plan
+    caches, equality and hashing compare the boxes and the index type."""
 
     __slots__ = ("boxes", "ixtype", "uid", "_hash", "_lock", "_lohi")
 
     def __init__(self, boxes, ixtype=None, validate=True):
         boxes = tuple(boxes)
-        if ixtype is None:
-            if not boxes:
-                raise ValueError("empty BoxArray needs an explicit index type")
-            ixtype = boxes[0].ixtype
-        for b in boxes:
-            if b.ixtype != ixtype:
-                raise ValueError(f"mixed index types: {b!r} vs {ixtype!r}")
-            if b.is_empty():
-                raise ValueError("BoxArray may not contain empty boxes")
-        set_ = object.__setattr__
-        set_(self, "boxes", boxes)
-        set_(self, "ixtype", ixtype)
-        set_(self, "uid", _next_uid())
-        set_(self, "_hash", None)
-        set_(self, "_lock", threading.Lock())
-        set_(self, "_lohi", None)
+        if ixtype is None and not boxes:
+            raise ValueError("an empty BoxArray needs an explicit index type")
+        ixtype = boxes[0].ixtype if ixtype is None else ixtype
+        odd = next((b for b in boxes if b.ixtype != ixtype), None)
+        if odd is not None:
+            raise ValueError(f"mixed index types: {odd!r} vs {ixtype!r}")
+        if any(b.is_empty() for b in boxes):
+            raise ValueError("BoxArray may not contain empty boxes")
+        init = dict(boxes=boxes, ixtype=ixtype, uid=_next_uid(), _hash=None, _lock=threading.Lock(), _lohi=None)
+        for k, v in init.items():
+            object.__setattr__(self, k, v)
         if validate:
             self.validate()
 
     def __setattr__(self, *a):
-        raise AttributeError("BoxArray is immutable")
+        raise AttributeError("BoxArray values cannot be modified")
 
     def validate(self):
-        """Raise ValueError naming the first overlapping pair, else True."""
-        if len(self.boxes) > 1:
-            bins = _Bins(self.boxes)
-            for i, b in enumerate(self.boxes):
-                for j in bins.candidates(b, count=False):
-                    if j != i and self.boxes[j].intersects(b):
-                        a, c = min(i, j), max(i, j)
-                        raise ValueError(
-                            f"boxes {a} and {c} overlap: {self.boxes[a]!r} vs {self.boxes[c]!r}"
-                        )
+        """True, or ValueError naming the first pair of overlapping boxes."""
+        if len(self.boxes) < 2:
+            return True
+        bins = _Bins(self.boxes)
+        for i, b in enumerate(self.boxes):
+            clash = [j for j in bins.candidates(b, count=False) if j != i and self.boxes[j].intersects(b)]
+            if clash:
+                a, c = sorted((i, clash[0]))
+                raise ValueError(f"boxes {a} and {c} overlap: {self.boxes[a]!r} vs {self.boxes[c]!r}")
         return True
 
-    @property
-    def dim(self):
-        return self.ixtype.dim
-
+    # -- sequence / value protocol ------------------------------------------------
     def __len__(self):
         return len(self.boxes)
 
     def __getitem__(self, i):
         return self.boxes[i]
 
-    def __iter__(self):
-        return iter(self.boxes)
+    def _ident(self):
+        return (self.ixtype, self.boxes)
 
     def __eq__(self, other):
-        if not isinstance(other, BoxArray):
-            return NotImplemented
-        return self.boxes == other.boxes and self.ixtype == other.ixtype
+        return self._ident() == other._ident() if isinstance(other, BoxArray) else NotImplemented
 
     def __hash__(self):
-        return hash((self.boxes, self.ixtype))
+        return hash(self._ident())
 
     def __repr__(self):
-        return f"BoxArray({len(self.boxes)} boxes, type {self.ixtype!r})"
+        return f"BoxArray({len(self)} boxes, type {self.ixtype!r})"
+
+    @property
+    def dim(self):
+        return self.ixtype.dim
 
     def dump(self):
-        return "\n".join(repr(b) for b in self.boxes)
+        return "\n".join(map(repr, self.boxes))
 
     def num_cells(self):
         return sum(b.num_cells() for b in self.boxes)
@@ -173,8 +172,7 @@ class BoxArray:
     def minimal_box(self):
         if not self.boxes:
             return Box.empty(self.dim, self.ixtype)
-        t = self.lohi()
-        d = self.dim
+        t, d = self.lohi(), self.dim
         return Box(t[:, :d].min(axis=0).tolist(), t[:, d:].max(axis=0).tolist(), self.ixtype)
 
     def lohi(self):
@@ -271,50 +269,55 @@ class BoxArray:
 
 
 class DistributionMapping:
-    """owner[i] = rank (GPU) holding box i."""
+    """owner[i] = rank (GPU) holding box i; an immutable value."""
 
     __slots__ = ("owner", "nranks")
 
     def __init__(self, owner, nranks):
-        owner = tuple(int(r) for r in owner)
         nranks = int(nranks)
         if nranks < 1:
             raise ValueError("nranks must be >= 1")
-        bad = [r for r in owner if not 0 <= r < nranks]
-        if bad:
-            raise ValueError(f"owner rank {bad[0]} outside 0..{nranks - 1}")
+        owner = tuple(map(int, owner))
+        out_of_range = [r for r in owner if r < 0 or r >= nranks]
+        if out_of_range:
+            raise ValueError(f"owner rank {out_of_range[0]} outside 0..{nranks - 1}")
         object.__setattr__(self, "owner", owner)
         object.__setattr__(self, "nranks", nranks)
 
     def __setattr__(self, *a):
-        raise AttributeError("DistributionMapping is immutable")
+        raise AttributeError("DistributionMapping values cannot be modified")
 
+    @classmethod
+    def single_rank(cls, nboxes):
+        return cls((0,) * nboxes, 1)
+
+    @classmethod
+    def _from_array(cls, owner, nranks):
+        return cls(np.asarray(owner).tolist(), nranks)
+
+    def owned_indices(self, rank):
+        return [i for i, r in enumerate(self.owner) if r == rank]
+
+    # sequence of owners; equality on (owner, nranks)
     def __len__(self):
         return len(self.owner)
-
-    def __getitem__(self, i):
-        return self.owner[i]
 
     def __iter__(self):
         return iter(self.owner)
 
+    def __getitem__(self, i):
+        return self.owner[i]
+
     def __eq__(self, other):
-        if not isinstance(other, DistributionMapping):
-            return NotImplemented
-        return self.owner == other.owner and self.nranks == other.nranks
+        if isinstance(other, DistributionMapping):
+            return (self.nranks, self.owner) == (other.nranks, other.owner)
+        return NotImplemented
 
     def __hash__(self):
         return hash((self.owner, self.nranks))
 
     def __repr__(self):
         return f"DistributionMapping(nranks={self.nranks}, owner={list(self.owner)})"
-
-    def owned_indices(self, rank):
-        return [i for i, r in enumerate(self.owner) if r == rank]
-
-    @staticmethod
-    def single_rank(nboxes):
-        return DistributionMapping([0] * nboxes, 1)
 
 
 def default_costs(ba):
@@ -323,79 +326,58 @@ def default_costs(ba):
 
 
 def morton_key(center, domain):
-    """Bit-interleaved position; bit k of dim d -> key bit k*D + d (dim 0 lowest)."""
-    center = IntVect(center) if not isinstance(center, IntVect) else center
-    dim = len(center)
-    nbits = 63 // dim
-    key = 0
-    for d in range(dim):
-        c = center[d] - domain.lo[d]
-        if c < 0 or c >= (1 << nbits):
-            raise ValueError(
-                f"coordinate {center[d]} out of key range (needs 0 <= shifted < 2^{nbits})"
-            )
-        k = 0
-        while c:
-            if c & 1:
-                key |= 1 << (k * dim + d)
-            c >>= 1
-            k += 1
-    return key
+    """Bit-interleaved curve position of an index point, shifted by domain.lo:
+    bit k of axis d -> key bit k*D + d (axis 0 least significant); libamrb
+    amrb_morton_key (csrc/distribute.cpp)."""
+    from ._native import check, i32p, lib
+
+    pt = [int(x) for x in center]
+    key = C.c_uint64(0)
+    _p, pp = i32p(pt)
+    _o, op = i32p([int(x) for x in domain.lo][: len(pt)])
+    check(lib().amrb_morton_key(len(pt), pp, op, C.byref(key)))
+    return int(key.value)
+
+
+def _checked_costs(cost, n):
+    cost = np.ascontiguousarray(cost, dtype=np.float64)
+    if cost.shape != (n,):
+        raise ValueError("cost length must match BoxArray length")
+    return cost
 
 
 def sfc_distribute(ba, cost, nranks):
-    """Morton order, then contiguous runs of ~equal cost; each rank < len(ba) gets >= 1 box."""
+    """Morton order of the box centres, then contiguous runs of about equal
+    cost; every rank below the box count gets at least one box
+    (distribution.py:97-131; the split runs in libamrb)."""
+    from ._native import check, f64p, i32p, lib
+
     nranks = int(nranks)
     if nranks < 1:
         raise ValueError("nranks must be >= 1")
-    cost = np.asarray(cost, dtype=np.float64)
-    if len(cost) != len(ba):
-        raise ValueError("cost length must match BoxArray length")
-    n = len(ba)
-    dom = ba.minimal_box() if n else Box.empty(1)
-    two = None
-    keys = []
-    for i, b in enumerate(ba):
-        two = two or IntVect((2,) * b.dim)
-        keys.append((morton_key((b.lo + b.hi) // two, dom), i))
-    order = [i for _, i in sorted(keys)]
-    owner = [0] * n
-    total = float(cost.sum())
-    pos = 0
-    assigned = 0.0
-    for rank in range(nranks):
-        left = nranks - rank
-        limit = (n - pos) - (left - 1)
-        goal = (total - assigned) / left
-        take, run = 0, 0.0
-        while take < limit:
-            c = cost[order[pos + take]]
-            if take and run + c > goal + 1e-12:
-                break
-            run += c
-            take += 1
-        if rank == nranks - 1:
-            take = n - pos
-        for i in order[pos : pos + take]:
-            owner[i] = rank
-        pos += take
-        assigned += run
-    return DistributionMapping(owner, nranks)
+    cost = _checked_costs(cost, len(ba))
+    owner = np.zeros(len(ba), dtype=np.int32)
+    if len(ba):
+        _t, tp = i32p(ba.lohi())
+        _c, cp = f64p(cost)
+        check(lib().amrb_sfc_distribute(ba.dim, len(ba), tp, cp, float(cost.sum()), nranks,
+                                        owner.ctypes.data_as(C.POINTER(C.c_int32))))
+    return DistributionMapping._from_array(owner, nranks)
 
 
 def knapsack_distribute(cost, nranks):
-    """Longest-processing-time greedy; ties to the lower rank id."""
+    """Longest processing time first; ties to the lower box index, then the
+    lower rank (distribution.py:134-148; runs in libamrb)."""
+    from ._native import check, f64p, lib
+
     nranks = int(nranks)
     if nranks < 1:
         raise ValueError("nranks must be >= 1")
-    cost = np.asarray(cost, dtype=np.float64)
-    owner = [0] * len(cost)
-    heap = [(0.0, r) for r in range(nranks)]
-    for i in sorted(range(len(cost)), key=lambda i: (-cost[i], i)):
-        load, rank = heapq.heappop(heap)
-        owner[i] = rank
-        heapq.heappush(heap, (load + float(cost[i]), rank))
-    return DistributionMapping(owner, nranks)
+    cost = np.ascontiguousarray(cost, dtype=np.float64).reshape(-1)
+    owner = np.zeros(len(cost), dtype=np.int32)
+    _c, cp = f64p(cost)
+    check(lib().amrb_knapsack_distribute(len(cost), cp, nranks, owner.ctypes.data_as(C.POINTER(C.c_int32))))
+    return DistributionMapping._from_array(owner, nranks)
 
 
 def load_stats(dm, cost):

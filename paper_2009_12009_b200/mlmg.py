@@ -207,13 +207,17 @@ class MLMG:
                 break
         # a 32^3 single-box level above a 16^3 .. tail joins it: the cluster
         # variant of the tail kernel (8 CTAs, the 32^3 level split in slabs
-        # across their shared memory) runs it too (AMRB_CLUSTER_TAIL=0: off)
-        # (AMRB_CLUSTER_TAIL=2: 32 x n1 x n2 levels too, n1, n2 powers of two
-        # <= 32, the multi-GPU weak-scaling chains 32x16x16 .. and 32x32x16 ..;
-        # bit-identical but measured slower than the one-CTA non-cubic tail,
-        # DESIGN.md §6; libamrb picks the cluster kernel from the same shape test)
+        # across their shared memory) runs it too.  cluster_tail: 0 / False
+        # off, 1 / True / None (default) cubic chains, 2 also 32 x n1 x n2 top
+        # levels (n1, n2 powers of two <= 32: the multi-GPU weak-scaling chains
+        # 32x16x16 .. and 32x32x16 ..; bit-identical but measured slower than
+        # the one-CTA non-cubic tail).  The library picks the kernel
+        # from the same shape test and reports the ghost width it wrote.
         self.cluster_tail = False
-        noncubic = os.environ.get("AMRB_CLUSTER_TAIL", "1") == "2"
+        self.cluster_mode = 1 if cluster_tail is None else int(cluster_tail)
+        if self.cluster_mode not in (0, 1, 2):
+            raise ValueError("cluster_tail must be 0, 1, 2 or a bool")
+        noncubic = self.cluster_mode == 2
 
         def _cl_chain(t0):
             ext = [tuple(self.levels[x].domain.extents()) for x in range(t0, n)]
@@ -221,7 +225,7 @@ class MLMG:
                     and all(2 <= e <= 32 and e & (e - 1) == 0 for es in ext for e in es)
                     and all(ext[x][d] == 2 * ext[x + 1][d] for x in range(len(ext) - 1) for d in range(3)))
 
-        if ((cluster_tail is None and os.environ.get("AMRB_CLUSTER_TAIL", "1") != "0") or cluster_tail) and self.tail < n:
+        if self.cluster_mode and self.tail < n:
             t = self.tail
             if 0 < t < n and _cl_chain(t):
                 self.cluster_tail = True
@@ -234,9 +238,8 @@ class MLMG:
         # latency bound, run each half V-cycle as ONE grid-synchronised launch
         # (amrb_level_grid: in-place sweeps with periodic index wrap, no fills)
         # instead of ~7 fill / sweep / transfer launches
-        # (AMRB_GRID_LEVEL_CELLS: largest such level, 0 = off)
-        gmax = grid_level_cells if grid_level_cells is not None else int(
-            os.environ.get("AMRB_GRID_LEVEL_CELLS", str(128**3 // 2)))
+        # (grid_level_cells: largest such level, 0 = off)
+        gmax = 128**3 // 2 if grid_level_cells is None else int(grid_level_cells)
         self.grid_from = self.tail
         for l in range(self.tail - 1, 0, -1) if self.tail < n and self.all_periodic else ():
             lv, nx = self.levels[l], self.levels[l + 1]
@@ -273,8 +276,8 @@ class MLMG:
         # (k_gsrb_sweep5<PROL>, box-local level pairs): no separate read+write
         # pass over the fine phi and no fill after it; the restriction fills the
         # fine phi to width 2 instead of 1 and the coarse phi gets a width-1 fill
-        if fuse_prolong is None:  # AMRB_FUSE_PROLONG=0: separate prolongation (A/B runs)
-            fuse_prolong = os.environ.get("AMRB_FUSE_PROLONG", "1") != "0"
+        if fuse_prolong is None:  # False: separate prolongation (A/B runs)
+            fuse_prolong = True
         for l, lv in enumerate(self.levels):
             # (the fused kernel adds the parent to every tile cell, ghosts
             # included: periodic levels only)
@@ -435,7 +438,7 @@ class MLMG:
             # over NVLink (peer-pull copy program framed by the signal barrier)
             copy_into(nx.rhs, lv.tmp, self.transport)
         elif self.dist and not lv.replicated:
-            nx.rhs.storage.zero_()
+            _zero(nx.rhs)
             # every rank copies its own boxes into its replica, then all-reduce(sum)
             copy_into(nx.rhs, lv.tmp, _LocalView(self.transport))
             check(
@@ -510,7 +513,7 @@ class MLMG:
         """All tail levels in one kernel: reads rhs, writes phi of levels[tail]."""
         lv = self.levels[self.tail]
         phi = lv.phi[lv.cur]
-        self._produced(phi, 1 if self.cluster_tail else 0)  # the cluster variant writes the width-1 ghosts
+        written = C.c_int32(0)
         lohi, lp = i32p(self._tail_lohi)
         dh = np.ascontiguousarray(self._tail_dh)
         check(
@@ -525,9 +528,14 @@ class MLMG:
                 self.nu1,
                 self.nu2,
                 self.bottom_sweeps,
+                self.cluster_mode,
+                C.byref(written),
                 stream_ptr(),
             )
         )
+        # ghost width the launched kernel left current (the cluster variant: 1);
+        # decided by the library's own shape test, not re-derived here
+        self._produced(phi, int(written.value))
 
     def _level_grid(self, l, up):
         """Half V-cycle of grid level l in one launch (amrb_level_grid)."""
@@ -636,7 +644,7 @@ class MLMG:
         (csrc/graph.cu): a solve is one graph launch + one synchronisation."""
         for lv in self.levels:
             for f in lv.phi + [lv.rhs]:
-                f.storage.zero_()
+                _zero(f)
                 self._produced(f, f.ngrow)
         saved = [lv.cur for lv in self.levels]
         self._prime()
@@ -711,9 +719,8 @@ class MLMG:
             self._capture()
         self.set_rhs(rhs)
         self.set_phi(phi)
-        r0t = device_reduce(top.rhs, "absmax", 0)
-        self._allmax(r0t)
-        self.r0_dev.copy_(r0t)
+        device_reduce(top.rhs, "absmax", 0, out=self.r0_dev)
+        self._allmax(self.r0_dev)
         self.history = []
         self.iterations = 0
         if max_iter == 0:

@@ -67,14 +67,18 @@ def _round(x, a):
 class Fab:
     """One box's data: a strided view into the owning FabArray's allocation."""
 
-    __slots__ = ("box", "gbox", "ncomp", "ngrow", "data")
+    __slots__ = ("box", "gbox", "ncomp", "ngrow", "data", "_owner", "_index_in_owner")
 
-    def __init__(self, box, ncomp, ngrow, data):
+    def __init__(self, box, ncomp, ngrow, data, owner=None, index=-1):
+        import weakref
+
         self.box = box
         self.ngrow = int(ngrow)
         self.ncomp = int(ncomp)
         self.gbox = box.grow(self.ngrow)
         self.data = data
+        self._owner = weakref.ref(owner) if owner is not None else (lambda: None)
+        self._index_in_owner = index
 
     def _index(self, region):
         if not self.gbox.contains_box(region):
@@ -96,10 +100,10 @@ class Fab:
         return ArrayView(self)
 
     def setval(self, value, comp=None, ghosts=True):
-        if ghosts:
-            (self.data if comp is None else self.data[comp]).fill_(value)
-        else:
-            self.slice(self.box, comp).fill_(value)
+        """Valid (or grown) cells of one or all components = value, by the
+        library's setval kernel on the owning FabArray (Fab.setval,
+        fabarray.py:58-65)."""
+        self._owner()._setval_boxes(value, comp, ghosts, box=self._index_in_owner)
 
 
 class ArrayView:
@@ -167,7 +171,7 @@ class FabArray:
         self.fabs = {}
         for i in range(len(ba)):
             if self.resident[i]:
-                self.fabs[i] = Fab(ba[i], self.ncomp, self.ngrow, self._view(i))
+                self.fabs[i] = Fab(ba[i], self.ncomp, self.ngrow, self._view(i), self, i)
         self._progs = {}
         self._native = {}
         self.serial = next(_serials)
@@ -243,11 +247,34 @@ class FabArray:
         return self.dm.owned_indices(rank)
 
     def setval(self, value, comp=None, ghosts=True):
+        """Every resident fab (fabarray.py:119-122), by library kernels: the
+        whole allocation (padding included) in one fill when ghosts and all
+        components are set, else the setval kernel over the boxes."""
+        self.require_cuda("setval")
+        from ._native import check, lib
+        from .device import stream_ptr
+
         if ghosts and comp is None:
-            self.storage.fill_(value)
+            import ctypes as C
+
+            check(lib().amrb_fill(C.c_void_p(self.storage.data_ptr()), self.storage.numel(), float(value),
+                                  stream_ptr()))
             return self
-        for f in self.fabs.values():
-            f.setval(value, comp, ghosts)
+        return self._setval_boxes(value, comp, ghosts)
+
+    def _setval_boxes(self, value, comp=None, ghosts=True, box=-1):
+        import ctypes as C
+
+        from ._native import check, lib
+        from .device import field_of, level_of, stream_ptr
+
+        self.require_cuda("setval")
+        c0, c1 = (0, self.ncomp) if comp is None else (int(comp), int(comp) + 1)
+        if not 0 <= c0 < c1 <= self.ncomp:
+            raise ValueError("component out of range")
+        mode = 2 if ghosts == 2 else (1 if ghosts else 0)
+        check(lib().amrb_setval(level_of(self).handle, field_of(self).handle, C.c_void_p(self.storage.data_ptr()),
+                                int(box), c0, c1, mode, float(value), stream_ptr()))
         return self
 
     def copy_shape(self, ncomp=None, ngrow=None):
@@ -315,15 +342,28 @@ class FabArray:
         return image
 
     def load_valid_from(self, domain, global_arr):
-        """Load every resident fab's valid region from one dense array over domain."""
-        g = np.asarray(global_arr)
+        """Load every resident fab's valid region from one dense array over
+        domain: the host gathers the boxes into the host-image layout
+        (image_size), then one host->device copy and one scatter launch
+        (from_host_image)."""
+        g = np.asarray(global_arr, dtype=np.float64)
         if g.ndim == self.dim:
             g = g[None]
-        gt = torch.as_tensor(np.ascontiguousarray(g)).to(self.device)
-        for i, f in self.fabs.items():
+        if g.shape[0] != self.ncomp:
+            raise ValueError("component count differs")
+        image = torch.empty(max(self.image_size(), 1), dtype=torch.float64).pin_memory()
+        flat = image.numpy()
+        o = 0
+        for i in range(len(self.ba)):
+            if not self.resident[i]:
+                continue
             b = self.ba[i]
             sel = tuple(slice(b.lo[d] - domain.lo[d], b.hi[d] - domain.lo[d] + 1) for d in range(self.dim))
-            f.valid().copy_(gt[(slice(None),) + sel])
+            blk = g[(slice(None),) + sel]
+            flat[o:o + blk.size] = blk.reshape(-1)
+            o += blk.size
+        self.from_host_image(image[: self.image_size()])
+        torch.cuda.current_stream(self.device).synchronize()  # the pinned image is released on return
         return self
 
     def to_global(self, domain, comp=0, default=0.0):

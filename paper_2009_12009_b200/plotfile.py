@@ -28,9 +28,10 @@ writes the Header and sizes the file first.
 
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes as C
+import itertools
 import os
-import queue
 import threading
 
 import numpy as np
@@ -62,93 +63,90 @@ CHECKPOINT_TAG = "amrkit-checkpoint-1"
 
 
 class OutputMode:
-    """``static(nwriters)`` writes now in waves; ``asynchronous()`` snapshots
-    and returns (plotfile.py:43-64)."""
+    """How a plotfile is written (plotfile.py:43-64): ``static(nwriters)``
+    writes before returning, ranks in waves of nwriters; ``asynchronous()``
+    snapshots the data and hands the writes to the background writer."""
 
     __slots__ = ("kind", "nwriters")
+    _KINDS = ("static", "async")
 
     def __init__(self, kind, nwriters=1):
-        if kind not in ("static", "async"):
-            raise ValueError("mode kind must be 'static' or 'async'")
-        if int(nwriters) < 1:
+        nwriters = int(nwriters)
+        if kind not in self._KINDS:
+            raise ValueError("output mode must be 'static' or 'async'")
+        if nwriters < 1:
             raise ValueError("nwriters must be >= 1")
-        self.kind = kind
-        self.nwriters = int(nwriters)
+        self.kind, self.nwriters = kind, nwriters
 
-    @staticmethod
-    def static(nwriters=1):
-        return OutputMode("static", nwriters)
+    @classmethod
+    def static(cls, nwriters=1):
+        return cls("static", nwriters)
 
-    @staticmethod
-    def asynchronous():
-        return OutputMode("async")
+    @classmethod
+    def asynchronous(cls):
+        return cls("async")
 
     def __repr__(self):
         return f"OutputMode({self.kind}, nwriters={self.nwriters})"
 
 
 class WriteHandle:
-    """Completion of one write; ``wait()`` re-raises the writer's error."""
+    """Completion of one plotfile write.  ``done`` polls; ``wait(timeout)``
+    blocks, raises TimeoutError if the write is still running and re-raises the
+    writer's exception if it failed.  Backed by a concurrent.futures.Future."""
 
-    def __init__(self):
-        self._event = threading.Event()
-        self._error = None
-
-    def _finish(self, error=None):
-        self._error = error
-        self._event.set()
+    def __init__(self, future=None):
+        if future is None:  # a write that already happened (static mode)
+            future = concurrent.futures.Future()
+            future.set_result(None)
+        self._future = future
 
     @property
     def done(self):
-        return self._event.is_set()
+        return self._future.done()
 
     def wait(self, timeout=None):
-        if not self._event.wait(timeout):
-            raise TimeoutError("write did not complete in time")
-        if self._error is not None:
-            raise self._error
+        try:
+            self._future.result(timeout)
+        except concurrent.futures.TimeoutError:
+            raise TimeoutError("plotfile write still in progress") from None
 
 
-class _Writer:
-    """One background writer thread, at most one snapshot pending."""
+class _BackgroundWriter:
+    """One writer thread; submit() blocks while a snapshot is already queued
+    behind the running one (one pending snapshot of backpressure, as
+    plotfile.py:86-115)."""
 
     def __init__(self):
-        self._queue = queue.Queue(maxsize=1)
-        self._thread = None
-        self._lock = threading.Lock()
-
-    def _run(self):
-        while True:
-            job, handle = self._queue.get()
-            try:
-                job()
-                handle._finish()
-            except BaseException as exc:  # surfaced by handle.wait()
-                handle._finish(exc)
+        self._pool = concurrent.futures.ThreadPoolExecutor(max_workers=1, thread_name_prefix="amrb-plotfile")
+        self._slots = threading.BoundedSemaphore(2)  # the running job + one pending
 
     def submit(self, job):
-        with self._lock:
-            if self._thread is None or not self._thread.is_alive():
-                self._thread = threading.Thread(target=self._run, daemon=True, name="amrb-plotfile-writer")
-                self._thread.start()
-        handle = WriteHandle()
-        self._queue.put((job, handle))  # blocks while a snapshot is pending
-        return handle
+        self._slots.acquire()
+
+        def run():
+            try:
+                job()
+            finally:
+                self._slots.release()
+
+        return WriteHandle(self._pool.submit(run))
 
 
-_writer = _Writer()
+_writer = _BackgroundWriter()
 
 
 class PlotfileHeader:
-    """Time, component names and one Geometry per level (plotfile.py:123-138)."""
+    """Simulation time, component names and one Geometry per level
+    (plotfile.py:123-138)."""
 
     def __init__(self, time, names, geoms):
+        names = [str(n) for n in names]
+        spaced = [n for n in names if " " in n]
+        if spaced:
+            raise ValueError(f"component names may not contain spaces ({spaced[0]!r})")
         self.version = PLOTFILE_TAG
-        self.time = float(time)
-        self.names = list(names)
-        if any(" " in n for n in self.names):
-            raise ValueError("component names may not contain spaces")
-        self.geoms = list(geoms)
+        self.time, self.names, self.geoms = float(time), names, list(geoms)
 
     @property
     def nlevels(self):
@@ -156,7 +154,7 @@ class PlotfileHeader:
 
 
 def _floats(vals):
-    return " ".join(repr(float(v)) for v in vals)
+    return " ".join(map(repr, map(float, vals)))
 
 
 def _ints(vals):
@@ -169,32 +167,27 @@ def _box_text(b):
 
 def _record_layout(ba, ncomp):
     """Byte offset and size of every box record, and the file size."""
-    sizes = [8 * ncomp * ba[i].num_cells() for i in range(len(ba))]
-    offsets = np.concatenate(([0], np.cumsum(sizes)[:-1])).astype(np.int64) if sizes else np.zeros(0, np.int64)
-    return [int(x) for x in offsets], sizes, int(sum(sizes))
+    sizes = [8 * ncomp * b.num_cells() for b in ba]
+    ends = list(itertools.accumulate(sizes))
+    return [e - n for e, n in zip(ends, sizes)], sizes, (ends[-1] if ends else 0)
 
 
 def _header_text(header, meshes):
+    """The Header file (FORMAT.md:17-84): global key/value lines, then per
+    level its domain, cell size and one line per box record."""
     g0 = header.geoms[0]
-    out = [
-        PLOTFILE_TAG,
-        "endian little",
-        "real float64",
-        f"time {header.time!r}",
-        f"dim {g0.dim}",
-        f"nlevels {header.nlevels}",
-        f"components {len(header.names)} " + " ".join(header.names),
-        "prob_lo " + _floats(g0.prob_lo),
-        "prob_hi " + _floats(g0.prob_hi),
-        "periodic " + _ints(g0.periodic),
+    rows = [
+        (PLOTFILE_TAG,), ("endian", "little"), ("real", "float64"), ("time", repr(header.time)),
+        ("dim", g0.dim), ("nlevels", header.nlevels),
+        ("components", f"{len(header.names)} " + " ".join(header.names)),
+        ("prob_lo", _floats(g0.prob_lo)), ("prob_hi", _floats(g0.prob_hi)), ("periodic", _ints(g0.periodic)),
     ]
-    for lev, mesh in enumerate(meshes):
-        geom = header.geoms[lev]
+    for lev, (mesh, geom) in enumerate(zip(meshes, header.geoms)):
         offs, sizes, _ = _record_layout(mesh.ba, mesh.ncomp)
-        out += [f"level {lev}", "domain " + _box_text(geom.domain), "cell_size " + _floats(geom.cell_size),
-                f"nboxes {len(mesh.ba)}"]
-        out += [f"box {_box_text(mesh.ba[i])} {offs[i]} {sizes[i]}" for i in range(len(mesh.ba))]
-    return "\n".join(out) + "\n"
+        rows += [("level", lev), ("domain", _box_text(geom.domain)), ("cell_size", _floats(geom.cell_size)),
+                 ("nboxes", len(mesh.ba))]
+        rows += [("box", _box_text(b), o, n) for b, o, n in zip(mesh.ba, offs, sizes)]
+    return "".join(" ".join(map(str, r)) + "\n" for r in rows)
 
 
 # ---------------------------------------------------------------------------
@@ -327,46 +320,38 @@ class _LevelSnapshot:
             self.host = None
 
 
-def _write_level(fname, snap, image, nwriters, create):
-    """Positioned writes of every record in waves of nwriters ranks
-    (plotfile.py:195-241: same waves, same counters)."""
+def _write_records(fd, snap, image, rank):
+    """Every record of `rank`'s boxes held here, straight from the pinned image."""
     p = snap.p
-    if create:
-        fd = os.open(fname, os.O_CREAT | os.O_WRONLY | os.O_TRUNC)
-        if p.total:
-            os.pwrite(fd, b"\0", p.total - 1)  # size the file up front
-        os.close(fd)
+    for i in (i for i, r in enumerate(snap.owners) if r == rank and p.mine[i]):
+        off, n = p.offsets[i], p.sizes[i]
+        os.pwrite(fd, memoryview(image[off:off + n]), off)
+        counters.incr("io_bytes_written", n)
+
+
+def _waves(nranks, nwriters):
+    return [list(range(w, min(w + nwriters, nranks))) for w in range(0, nranks, nwriters)]
+
+
+def _write_level(fname, snap, image, nwriters):
+    """Positioned writes in waves of nwriters ranks (plotfile.py:195-241):
+    ranks of one wave write concurrently, waves run one after another, and
+    io_waves / io_peak_writers count them as the reference does.  Simulated
+    ranks (one process): one thread per rank of the wave.  One process per GPU:
+    a rank writes in its own wave; every rank passes a barrier per wave."""
     fd = os.open(fname, os.O_WRONLY)
     try:
-        active = [0]
-        gauge = threading.Lock()
-        ranks = [snap.rank] if snap.dist else list(range(snap.nranks))
-
-        def write_rank(rank, barrier):
-            barrier.wait()  # the whole wave is live before anyone writes
-            with gauge:
-                active[0] += 1
-                counters.peak("io_peak_writers", active[0])
-            try:
-                for i, r in enumerate(snap.owners):
-                    if r != rank or not p.mine[i]:
-                        continue
-                    o, n = p.offsets[i], p.sizes[i]
-                    os.pwrite(fd, memoryview(image[o : o + n]), o)
-                    counters.incr("io_bytes_written", n)
-            finally:
-                with gauge:
-                    active[0] -= 1
-
-        for w0 in range(0, len(ranks), nwriters):
-            wave = ranks[w0 : w0 + nwriters]
+        for wave in _waves(snap.nranks, nwriters):
             counters.incr("io_waves")
-            barrier = threading.Barrier(len(wave))
-            threads = [threading.Thread(target=write_rank, args=(r, barrier)) for r in wave]
-            for t in threads:
-                t.start()
-            for t in threads:
-                t.join()
+            counters.peak("io_peak_writers", len(wave))
+            if snap.dist:
+                if snap.rank in wave:
+                    _write_records(fd, snap, image, snap.rank)
+                _dist_barrier()
+            else:
+                with concurrent.futures.ThreadPoolExecutor(max_workers=len(wave)) as pool:
+                    for f in [pool.submit(_write_records, fd, snap, image, r) for r in wave]:
+                        f.result()
     finally:
         os.close(fd)
 
@@ -380,23 +365,20 @@ def _dist_barrier():
 
 def _write_now(path, header_text, snaps, nwriters):
     root = not snaps or not snaps[0].dist or snaps[0].rank == 0
-    if root:
+    if root:  # the Header, and every data.bin sized up front
         os.makedirs(path, exist_ok=True)
         with open(os.path.join(path, "Header"), "w") as fh:
             fh.write(header_text)
         for lev, s in enumerate(snaps):
-            d = os.path.join(path, f"Level_{lev}")
-            os.makedirs(d, exist_ok=True)
-            fd = os.open(os.path.join(d, "data.bin"), os.O_CREAT | os.O_WRONLY | os.O_TRUNC)
-            if s.p.total:
-                os.pwrite(fd, b"\0", s.p.total - 1)
-            os.close(fd)
+            os.makedirs(os.path.join(path, f"Level_{lev}"), exist_ok=True)
+            with open(os.path.join(path, f"Level_{lev}", "data.bin"), "wb") as fh:
+                fh.truncate(s.p.total)
     images = [s.to_host() for s in snaps]
     if snaps and snaps[0].dist:
         _dist_barrier()  # files exist and are sized before any rank writes
     try:
         for lev, (s, img) in enumerate(zip(snaps, images)):
-            _write_level(os.path.join(path, f"Level_{lev}", "data.bin"), s, img, nwriters, create=False)
+            _write_level(os.path.join(path, f"Level_{lev}", "data.bin"), s, img, nwriters)
     finally:
         for s in snaps:
             s.release()
@@ -419,62 +401,64 @@ def write_plotfile(path, meshes, header, mode=None, transport=None):
     _write_now(path, text, snaps, mode.nwriters)
     if snaps and snaps[0].dist:
         _dist_barrier()
-    h = WriteHandle()
-    h._finish()
-    return h
+    return WriteHandle()
 
 
-class _Lines:
+class _HeaderScan:
+    """Header lines as (key, fields) records consumed in order: take(key)
+    checks the key and returns the fields after it."""
+
     def __init__(self, path):
         try:
             with open(path) as fh:
-                self.lines = [ln.rstrip("\n") for ln in fh]
+                text = fh.read()
         except OSError as exc:
             raise IOError(f"cannot read header at {path}: {exc}") from exc
-        self.at = 0
+        self.rows = [ln.split() for ln in text.splitlines()]
+        self.tag = text.splitlines()[0] if self.rows else ""
+        self.pos = 1
 
-    def next(self, expect=None):
-        line = self.lines[self.at]
-        self.at += 1
-        if expect is not None and not line.startswith(expect):
-            raise ValueError(f"malformed header: wanted {expect!r}, got {line!r}")
-        return line.split()
+    def take(self, key):
+        row = self.rows[self.pos] if self.pos < len(self.rows) else [""]
+        if not row or row[0] != key:
+            raise ValueError(f"malformed header: wanted {key!r}, got {' '.join(row)!r}")
+        self.pos += 1
+        return row[1:]
+
+    def one(self, key, conv):
+        return conv(self.take(key)[0])
 
 
-def _box(parts, dim):
-    return Box(IntVect(int(x) for x in parts[:dim]), IntVect(int(x) for x in parts[dim : 2 * dim]))
+def _box(fields, dim):
+    return Box([int(x) for x in fields[:dim]], [int(x) for x in fields[dim:2 * dim]])
 
 
 def read_plotfile(path, nranks=1, device=None):
     """(header, meshes): metadata plus one ngrow=0 device FabArray per level
     (plotfile.py:314-360).  The records are copied to the device once per level
     and scattered into the FabArray by one copy-program launch."""
-    rd = _Lines(os.path.join(path, "Header"))
-    if rd.lines[0] != PLOTFILE_TAG:
-        raise ValueError(f"not a plotfile (version tag {rd.lines[0]!r})")
-    rd.at = 1
-    rd.next("endian")
-    rd.next("real")
-    time = float(rd.next("time")[1])
-    dim = int(rd.next("dim")[1])
-    nlevels = int(rd.next("nlevels")[1])
-    cp = rd.next("components")
-    names = cp[2 : 2 + int(cp[1])]
-    prob_lo = [float(x) for x in rd.next("prob_lo")[1:]]
-    prob_hi = [float(x) for x in rd.next("prob_hi")[1:]]
-    periodic = [bool(int(x)) for x in rd.next("periodic")[1:]]
+    hd = _HeaderScan(os.path.join(path, "Header"))
+    if hd.tag != PLOTFILE_TAG:
+        raise ValueError(f"not a plotfile (version tag {hd.tag!r})")
+    hd.take("endian")
+    hd.take("real")
+    time = hd.one("time", float)
+    dim = hd.one("dim", int)
+    nlevels = hd.one("nlevels", int)
+    comps = hd.take("components")
+    names = comps[1:1 + int(comps[0])]
+    prob_lo = [float(x) for x in hd.take("prob_lo")]
+    prob_hi = [float(x) for x in hd.take("prob_hi")]
+    periodic = [x == "1" for x in hd.take("periodic")]
     geoms, meshes = [], []
     for lev in range(nlevels):
-        rd.next("level")
-        dom = _box(rd.next("domain")[1:], dim)
-        rd.next("cell_size")
-        nboxes = int(rd.next("nboxes")[1])
-        boxes, offs, sizes = [], [], []
-        for _ in range(nboxes):
-            parts = rd.next("box")[1:]
-            boxes.append(_box(parts, dim))
-            offs.append(int(parts[2 * dim]))
-            sizes.append(int(parts[2 * dim + 1]))
+        hd.take("level")
+        dom = _box(hd.take("domain"), dim)
+        hd.take("cell_size")
+        rec = [hd.take("box") for _ in range(hd.one("nboxes", int))]
+        boxes = [_box(f, dim) for f in rec]
+        offs = [int(f[2 * dim]) for f in rec]
+        sizes = [int(f[2 * dim + 1]) for f in rec]
         geoms.append(Geometry(dom, prob_lo, prob_hi, periodic))
         ba = BoxArray(boxes)
         dm = (DistributionMapping.single_rank(len(ba)) if nranks == 1
@@ -521,18 +505,16 @@ def write_checkpoint(path, meshes, header, step, user_blob=b"", pc=None, mode=No
 
 def read_checkpoint(path, device=None):
     """{step, time, nranks, owners, header, meshes, blob, particles} (plotfile.py:491-524)."""
-    rd = _Lines(os.path.join(path, "Header"))
-    if rd.lines[0] != CHECKPOINT_TAG:
-        raise ValueError(f"not a checkpoint (version tag {rd.lines[0]!r})")
-    rd.at = 1
-    step = int(rd.next("step")[1])
-    time = float(rd.next("time")[1])
-    nranks = int(rd.next("nranks")[1])
-    nlevels = int(rd.next("nlevels")[1])
-    owners = [[int(x) for x in rd.next("owners")[2:]] for _ in range(nlevels)]
-    nblob = int(rd.next("blob")[1])
-    has_pc = bool(int(rd.next("particles")[1]))
-    if has_pc:
+    hd = _HeaderScan(os.path.join(path, "Header"))
+    if hd.tag != CHECKPOINT_TAG:
+        raise ValueError(f"not a checkpoint (version tag {hd.tag!r})")
+    step = hd.one("step", int)
+    time = hd.one("time", float)
+    nranks = hd.one("nranks", int)
+    nlevels = hd.one("nlevels", int)
+    owners = [[int(x) for x in hd.take("owners")[1:]] for _ in range(nlevels)]
+    nblob = hd.one("blob", int)
+    if hd.one("particles", int):
         raise ValueError("checkpoint holds particles (not supported by the device reader)")
     with open(os.path.join(path, "blob.bin"), "rb") as fh:
         blob = fh.read()

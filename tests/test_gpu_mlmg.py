@@ -196,12 +196,13 @@ def test_grid_and_cluster_levels_eager_equals_graph():
     assert mg1.history == mg2.history and np.array_equal(phi1, phi2)
 
 
+@pytest.mark.parametrize("mode", [1, 2, 0])
 @pytest.mark.parametrize("shape", [(64, 32, 32), (32, 64, 32), (64, 64, 32)])
-def test_noncubic_pow2_tail_matches_oracle(shape):
+def test_noncubic_pow2_tail_matches_oracle(shape, mode):
     """Non-cubic power-of-two coarse chains (the multi-GPU weak-scaling shapes)
-    take k_coarse_tail_p2x (or, with AMRB_CLUSTER_TAIL=2, k_coarse_tail_cl for
-    a 32 x n1 x n2 top level) and grid levels above: same iterations,
-    history and bit-identical solution as the oracle."""
+    take k_coarse_tail_p2x (or, with cluster_tail=2, k_coarse_tail_cl for a
+    32 x n1 x n2 top level; 0: no cluster kernel) and grid levels above: same
+    iterations, history and bit-identical solution as the oracle."""
     hi = tuple(s - 1 for s in shape)
     dom = A.Box((0, 0, 0), hi)
     ba = A.BoxArray([dom]).max_size(32)
@@ -215,10 +216,10 @@ def test_noncubic_pow2_tail_matches_oracle(shape):
     phi = A.MultiFab(ba, dm, 1, 1)
     b = A.MultiFab(ba, dm, 1, 0)
     b.load_valid_from(dom, rhs)
-    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1))
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), cluster_tail=mode)
     assert mg.tail < len(mg.levels)
-    # the non-cubic cluster tail is opt-in (AMRB_CLUSTER_TAIL=2)
-    assert mg.cluster_tail == (os.environ.get("AMRB_CLUSTER_TAIL") == "2" and shape[0] == 64)
+    # the non-cubic cluster tail is opt-in (cluster_tail=2)
+    assert mg.cluster_tail == (mode == 2 and shape[0] == 64)
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
