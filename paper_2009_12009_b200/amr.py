@@ -167,11 +167,11 @@ def fill_patch(dst, fine_src, crse_old, crse_new, time_weight, ratio, transport,
     # built once); each is fully rewritten before use
     if fine_src is dst:
         fine_src = snapshot_valid(dst, transport, reuse=True)
-    if time_weight == 0.0:
-        blended = crse_old
-    elif time_weight == 1.0 or crse_old is None:
-        blended = crse_new
-    else:
+    # coarse data at the fill time: an endpoint as is, else the linear blend
+    # (1 - w) old + w new on the device (coarse_fine.py:248-258)
+    endpoint = {0.0: crse_old, 1.0: crse_new}.get(time_weight, None if crse_old is not None else crse_new)
+    blended = endpoint
+    if blended is None:
         blended = _scratch(crse_new, crse_new.ba, 0, "blend")
         _axpby(blended, 1.0 - time_weight, crse_old, time_weight, crse_new)
     margin = 1 if kind == "linear" else 0

@@ -21,7 +21,7 @@ is the real thing -- one process per GPU, messages are NCCL send/recv.
 from __future__ import annotations
 
 import ctypes as C
-from collections import deque
+from collections import defaultdict, deque
 
 import numpy as np
 import torch
@@ -50,10 +50,12 @@ __all__ = [
 
 
 class TransportError(RuntimeError):
+    """A message between two ranks failed (transport.py:20-24): ``src``,
+    ``dst`` and the reason in the message."""
+
     def __init__(self, src, dst, why):
+        self.src, self.dst = src, dst
         super().__init__(f"transport failure {src} -> {dst}: {why}")
-        self.src = src
-        self.dst = dst
 
 
 class Transport:
@@ -67,15 +69,11 @@ class Transport:
     """
 
     def __init__(self, nranks):
-        nranks = int(nranks)
-        if nranks < 1:
+        if int(nranks) < 1:
             raise ValueError("nranks must be >= 1")
-        self.nranks = nranks
-        self.rank = 0
-        self.mode = "sim"
-        self.nccl_comm = None
-        self.p2p = False
-        self._queues = {}
+        self.nranks, self.rank, self.mode = int(nranks), 0, "sim"
+        self.nccl_comm, self.p2p = None, False
+        self._queues = defaultdict(deque)  # (src, dst) -> FIFO of (tag, payload)
 
     @classmethod
     def distributed(cls):
@@ -167,20 +165,19 @@ class Transport:
     def send(self, src, dst, tag, payload):
         if not (0 <= src < self.nranks and 0 <= dst < self.nranks):
             raise TransportError(src, dst, "rank out of range")
-        self._queues.setdefault((src, dst), deque()).append((tag, payload))
+        self._queues[(src, dst)].append((tag, payload))
         self.account(src, dst, int(getattr(payload, "nbytes", len(payload))))
 
     def drain(self, dst):
-        out = []
+        """Every message queued for ``dst``, by source rank, FIFO per source."""
+        got = []
         for src in range(self.nranks):
-            q = self._queues.get((src, dst))
-            while q:
-                tag, payload = q.popleft()
-                out.append((src, tag, payload))
-        return out
+            q = self._queues.pop((src, dst), None)
+            got.extend((src, tag, payload) for tag, payload in (q or ()))
+        return got
 
     def pending(self):
-        return sum(len(q) for q in self._queues.values())
+        return sum(map(len, self._queues.values()))
 
     def account(self, src, dst, nbytes):
         counters.incr("transport_messages")

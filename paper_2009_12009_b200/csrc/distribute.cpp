@@ -26,6 +26,9 @@ namespace {
 
 int64_t floor_half(int64_t x) { return x >= 0 ? x / 2 : -((-x + 1) / 2); }
 
+// shifted coordinates must lie in [0, 2^bits); 1-D keys use 63 bits
+bool in_key_range(int64_t c, int bits) { return c >= 0 && (bits >= 63 || c < ((int64_t)1 << bits)); }
+
 // Morton keys of the box centres; false if a shifted coordinate is out of range
 bool centre_keys(int dim, int n, const int32_t* lohi, std::vector<uint64_t>& keys, int64_t* bad_coord) {
   std::vector<int64_t> origin(dim, 0);
@@ -42,7 +45,7 @@ bool centre_keys(int dim, int n, const int32_t* lohi, std::vector<uint64_t>& key
     for (int d = 0; d < dim; ++d) {
       const int64_t centre = floor_half((int64_t)box[d] + box[dim + d]);
       const int64_t c = centre - origin[d];
-      if (c < 0 || c >= ((int64_t)1 << bits)) {
+      if (!in_key_range(c, bits)) {
         if (bad_coord) *bad_coord = centre;
         return false;
       }
@@ -66,7 +69,7 @@ extern "C" int amrb_morton_key(int dim, const int32_t* point, const int32_t* ori
     uint64_t k = 0;
     for (int d = 0; d < dim; ++d) {
       const int64_t c = (int64_t)point[d] - origin[d];
-      if (c < 0 || c >= ((int64_t)1 << bits))
+      if (!in_key_range(c, bits))
         throw Error(AMRB_EINVAL, "coordinate " + std::to_string(point[d]) + " out of key range (needs 0 <= shifted < 2^" +
                                      std::to_string(bits) + ")");
       for (int b = 0; b < bits && (c >> b); ++b)

@@ -167,10 +167,10 @@ class BoxArray(Sequence):
         return "\n".join(map(repr, self.boxes))
 
     def num_cells(self):
-        return sum(b.num_cells() for b in self.boxes)
+        return int(sum(map(Box.num_cells, self.boxes)))
 
     def minimal_box(self):
-        if not self.boxes:
+        if len(self) == 0:
             return Box.empty(self.dim, self.ixtype)
         t, d = self.lohi(), self.dim
         return Box(t[:, :d].min(axis=0).tolist(), t[:, d:].max(axis=0).tolist(), self.ixtype)
@@ -184,19 +184,22 @@ class BoxArray(Sequence):
             object.__setattr__(self, "_lohi", t)
         return self._lohi
 
-    # derived layouts
+    # -- derived layouts (no overlap check: a coarsening may merge boxes, callers
+    # test coarsenable() first; nodal layouts may share faces) ------------------
+    def _each(self, fn, ixtype=None, validate=False):
+        return BoxArray(list(map(fn, self.boxes)), ixtype or self.ixtype, validate=validate)
+
     def refine(self, ratio):
-        return BoxArray([b.refine(ratio) for b in self.boxes], self.ixtype, validate=False)
+        return self._each(lambda b: b.refine(ratio))
 
     def coarsen(self, ratio):
-        # may create overlap; callers check coarsenable() first
-        return BoxArray([b.coarsen(ratio) for b in self.boxes], self.ixtype, validate=False)
+        return self._each(lambda b: b.coarsen(ratio))
 
     def coarsenable(self, ratio):
-        return all(b.coarsen(ratio).refine(ratio) == b for b in self.boxes)
+        return all(b == b.coarsen(ratio).refine(ratio) for b in self.boxes)
 
     def convert(self, ixtype):
-        return BoxArray([b.convert(ixtype) for b in self.boxes], ixtype, validate=ixtype.is_cell())
+        return self._each(lambda b: b.convert(ixtype), ixtype, validate=ixtype.is_cell())
 
     def max_size(self, m):
         """Chop so no extent exceeds m; cuts at lo + k*m of each box, remainder last."""
@@ -215,36 +218,27 @@ class BoxArray(Sequence):
         return BoxArray(out, self.ixtype, validate=False)
 
     def prune(self, fully_covered):
-        return BoxArray([b for b in self.boxes if not fully_covered(b)], self.ixtype, validate=False)
+        return BoxArray(itertools.filterfalse(fully_covered, self.boxes), self.ixtype, validate=False)
 
-    # queries
+    # -- hash-backed queries --------------------------------------------------------
     def _bins(self):
-        if self._hash is None:
-            with self._lock:
-                if self._hash is None:
-                    object.__setattr__(self, "_hash", BoxHash(self))
-        return self._hash
+        with self._lock:  # built once, on first query
+            if self._hash is None:
+                object.__setattr__(self, "_hash", BoxHash(self))
+            return self._hash
 
     def intersections(self, q):
         """[(index, overlap)] for members meeting q, via the hash."""
-        if q.ixtype != self.ixtype:
+        if self.ixtype != q.ixtype:
             raise ValueError("index type mismatch")
-        if q.is_empty() or not self.boxes:
-            return []
-        out = []
-        for i in self._bins().candidates(q):
-            ov = self.boxes[i].intersect(q)
-            if not ov.is_empty():
-                out.append((i, ov))
-        return out
+        hits = [] if (q.is_empty() or not self.boxes) else self._bins().candidates(q)
+        pairs = ((i, self.boxes[i].intersect(q)) for i in hits)
+        return [(i, ov) for i, ov in pairs if not ov.is_empty()]
 
     def owner_at(self, p):
-        if not self.boxes:
-            return None
-        for i in self._bins().candidates_at(p):
-            if self.boxes[i].contains(p):
-                return i
-        return None
+        """Index of the box holding point p, or None."""
+        hits = self._bins().candidates_at(p) if self.boxes else ()
+        return next((i for i in hits if self.boxes[i].contains(p)), None)
 
     def contains_box(self, q):
         if q.ixtype != self.ixtype:

@@ -72,31 +72,26 @@ class Fab:
     def __init__(self, box, ncomp, ngrow, data, owner=None, index=-1):
         import weakref
 
-        self.box = box
-        self.ngrow = int(ngrow)
-        self.ncomp = int(ncomp)
-        self.gbox = box.grow(self.ngrow)
-        self.data = data
+        self.ngrow, self.ncomp = int(ngrow), int(ncomp)
+        self.box, self.gbox, self.data = box, box.grow(int(ngrow)), data
         self._owner = weakref.ref(owner) if owner is not None else (lambda: None)
         self._index_in_owner = index
 
     def _index(self, region):
         if not self.gbox.contains_box(region):
             raise ValueError(f"{region!r} not within {self.gbox!r}")
-        return tuple(
-            slice(region.lo[d] - self.gbox.lo[d], region.hi[d] - self.gbox.lo[d] + 1) for d in range(self.box.dim)
-        )
+        return tuple(slice(a - g, b - g + 1) for a, b, g in zip(region.lo, region.hi, self.gbox.lo))
 
     def slice(self, region, comp=None):
-        idx = self._index(region)
-        if comp is None:
-            return self.data[(slice(None),) + idx]
-        return self.data[(comp,) + idx]
+        """View of ``region`` (all components, or one)."""
+        return self.data[(slice(None) if comp is None else comp,) + self._index(region)]
 
     def valid(self, comp=None):
+        """View of the valid box."""
         return self.slice(self.box, comp)
 
     def array(self):
+        """Global-index window onto this fab."""
         return ArrayView(self)
 
     def setval(self, value, comp=None, ghosts=True):
@@ -107,25 +102,25 @@ class Fab:
 
 
 class ArrayView:
-    """Global-index window (i, j, k, n) onto a Fab (fabarray.py:68-91)."""
+    """Global-index window onto a Fab (fabarray.py:68-91): ``view[i, j, k, n]``
+    -- the spatial indices are global cell indices, the last one the component."""
 
     __slots__ = ("data", "lo", "dim")
 
     def __init__(self, fab):
-        self.data = fab.data
-        self.lo = fab.gbox.lo
-        self.dim = fab.box.dim
+        self.data, self.lo, self.dim = fab.data, fab.gbox.lo, fab.box.dim
 
-    def _key(self, key):
-        if len(key) != self.dim + 1:
+    def _local(self, key):
+        if len(key) - 1 != self.dim:
             raise IndexError(f"expected {self.dim + 1} indices (spatial + component)")
-        return (key[-1],) + tuple(key[d] - self.lo[d] for d in range(self.dim))
+        *cell, comp = key
+        return (comp, *(c - o for c, o in zip(cell, self.lo)))
 
     def __getitem__(self, key):
-        return self.data[self._key(key)]
+        return self.data[self._local(key)]
 
     def __setitem__(self, key, value):
-        self.data[self._key(key)] = value
+        self.data[self._local(key)] = value
 
 
 class FabArray:
@@ -278,16 +273,11 @@ class FabArray:
         return self
 
     def copy_shape(self, ncomp=None, ngrow=None):
-        return type(self)(
-            self.ba,
-            self.dm,
-            self.ncomp if ncomp is None else ncomp,
-            self.ngrow if ngrow is None else ngrow,
-            self.dtype,
-            device=self.device,
-            replicated=self.replicated,
-            rank=self.rank,
-        )
+        """A new zeroed FabArray on the same layout and device."""
+        nc = self.ncomp if ncomp is None else ncomp
+        ng = self.ngrow if ngrow is None else ngrow
+        return type(self)(self.ba, self.dm, nc, ng, self.dtype, device=self.device, replicated=self.replicated,
+                          rank=self.rank)
 
     def owners(self):
         """Owner rank per box as seen by copy programs.

@@ -32,29 +32,26 @@ __all__ = [
 
 
 class CopyRecord:
-    """Congruent copy: src cell c of box src_index lands on dst cell c + shift."""
+    """Congruent copy (fabarray.py:171-182): source cell c of box src_index
+    lands on destination cell c + shift of box dst_index."""
 
     __slots__ = ("src_index", "dst_index", "src_box", "dst_box", "shift")
 
     def __init__(self, src_index, dst_index, src_box, dst_box, shift):
-        assert dst_box == src_box.shift(shift)
-        self.src_index = src_index
-        self.dst_index = dst_index
-        self.src_box = src_box
-        self.dst_box = dst_box
-        self.shift = shift
+        if dst_box != src_box.shift(shift):
+            raise ValueError("dst_box must be src_box shifted by shift")
+        for k, v in zip(self.__slots__, (src_index, dst_index, src_box, dst_box, shift)):
+            setattr(self, k, v)
+
+    def _fields(self):
+        return tuple(getattr(self, k) for k in self.__slots__)
 
     def sort_key(self):
+        """Apply order of CommPlan (fabarray.py:182-197)."""
         return (self.dst_index, tuple(self.dst_box.lo), self.src_index, tuple(self.shift))
 
     def __eq__(self, other):
-        return isinstance(other, CopyRecord) and (
-            self.src_index,
-            self.dst_index,
-            self.src_box,
-            self.dst_box,
-            self.shift,
-        ) == (other.src_index, other.dst_index, other.src_box, other.dst_box, other.shift)
+        return isinstance(other, CopyRecord) and self._fields() == other._fields()
 
     def __repr__(self):
         return f"CopyRecord({self.src_index}->{self.dst_index}, {self.src_box!r}, shift={tuple(self.shift)})"
@@ -155,11 +152,10 @@ def _cached(key, build):
 
 
 def normalize_periodic(periodic, dim):
-    if periodic is None:
-        return (False,) * dim
-    if isinstance(periodic, bool):
-        return (periodic,) * dim
-    return tuple(bool(p) for p in periodic)
+    """None / a bool / per-axis flags -> a dim-tuple of bools."""
+    if periodic is None or isinstance(periodic, bool):
+        return (bool(periodic),) * dim
+    return tuple(map(bool, periodic))
 
 
 def _domain_arr(domain):

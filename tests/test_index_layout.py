@@ -120,8 +120,8 @@ def test_matches_reference_layout_layer(amrkit, rng):
     """Same chop, SFC map and knapsack as the reference (build container only)."""
     from amrkit.distribution import default_costs as rdc, knapsack_distribute as rks, sfc_distribute as rsfc
 
-    for _ in range(20):
-        dim = int(rng.integers(2, 4))
+    for _ in range(30):
+        dim = int(rng.integers(1, 4))
         n = int(rng.integers(16, 64))
         m = int(rng.integers(4, 17))
         rb = amrkit.BoxArray([amrkit.Box(amrkit.IntVect([0] * dim), amrkit.IntVect([n - 1] * dim))]).max_size(m)
