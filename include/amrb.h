@@ -240,11 +240,18 @@ int amrb_gsrb_color(const amrb_level* lv, amrb_field* phi, double* phi_base,
  * ghosts of `a` filled to width 2 and of `rhs` to width 1; the red update of
  * the first ghost ring is recomputed locally, so no second exchange is needed.
  * fixed_lohi (nullable) = int32[6] global lo, hi: cells outside it in any axis
- * are never relaxed (non-periodic physical boundaries). */
+ * are never relaxed (non-periodic physical boundaries).
+ * push (nullable): a DEVICE table of int64 addresses, 27 per box (ghosts.py):
+ * every output cell within 2 of a box face is also stored through it into
+ * the ghost cells FillBoundary(b, 2) would copy it to -- on this GPU or, via
+ * NVLink-mapped symmetric memory, a peer -- so b's width-2 ghosts are current
+ * when the kernel ends (a peer's: after a device barrier).  With push the
+ * call is AMRB_ENOTSUP (nothing launched) unless the level takes the
+ * k_gsrb_stream path. */
 int amrb_gsrb_sweep(const amrb_level* lv, const amrb_field* a, const double* a_base,
                     amrb_field* b, double* b_base, const amrb_field* rhs,
                     const double* rhs_base, const double dh[3],
-                    const int32_t* fixed_lohi, void* stream);
+                    const int32_t* fixed_lohi, const uint64_t* push, void* stream);
 
 /* amrb_gsrb_sweep that also reduces the residual of its INPUT:
  * *norm = max(*norm, max over valid cells of |rhs - L(a)|), stored as the
@@ -255,7 +262,8 @@ int amrb_gsrb_sweep(const amrb_level* lv, const amrb_field* a, const double* a_b
 int amrb_gsrb_sweep_norm(const amrb_level* lv, const amrb_field* a, const double* a_base,
                          amrb_field* b, double* b_base, const amrb_field* rhs,
                          const double* rhs_base, const double dh[3],
-                         const int32_t* fixed_lohi, uint64_t* norm, void* stream);
+                         const int32_t* fixed_lohi, uint64_t* norm, const uint64_t* push,
+                         void* stream);
 
 /* Prolongation fused into the first post-smoothing sweep of the V-cycle up-leg:
  * b = GSRB(a + P(c)), P = piecewise-constant interpolation of the coarse
@@ -269,33 +277,9 @@ int amrb_gsrb_sweep_prolong(const amrb_level* lv, const amrb_field* a, const dou
                             amrb_field* b, double* b_base, const amrb_field* rhs,
                             const double* rhs_base, const double dh[3],
                             const amrb_level* clv, const amrb_field* c, const double* c_base,
-                            void* stream);
+                            const uint64_t* push, void* stream);
 
-/* Ghost push: FillBoundary (fabarray.py:364-374) fused into the kernel that
- * produces a field.  A push table holds the fill plan's records whose source
- * box this rank owns (rec11 = amrb_plan_records rows; fabtab = the GLOBAL fab
- * table of the destination field: every box's layout inside its owner's
- * allocation; owner = rank per box).  A producer given the table and the
- * per-rank base pointers of the field (peer_bases[r] = rank r's allocation,
- * NVLink-mapped symmetric memory for r != my_rank) stores every valid cell it
- * writes also into each ghost cell the plan copies it to, so the ghosts are
- * filled to `width` when the kernel ends (multi-GPU: after a device barrier).
- * AMRB_ENOTSUP when a box is thinner than 2*width or the records are not the
- * face/edge/corner slabs of a box (callers then fill with a copy program). */
-typedef struct amrb_push amrb_push;
-int amrb_push_create(const amrb_level* lv, int nrec, const int32_t* rec11,
-                     const int64_t* fabtab, int nboxes, const int32_t* owner,
-                     int my_rank, int nranks, int width, amrb_push** out);
-int amrb_push_destroy(amrb_push* p);
 
-/* amrb_gsrb_sweep that also fills b's ghosts (push table built for b's
- * layout, width <= b's ngrow).  AMRB_ENOTSUP when the level does not take the
- * k_gsrb_sweep5 path (nothing launched). */
-int amrb_gsrb_sweep_push(const amrb_level* lv, const amrb_field* a, const double* a_base,
-                         amrb_field* b, double* b_base, const amrb_field* rhs,
-                         const double* rhs_base, const double dh[3],
-                         const int32_t* fixed_lohi, const amrb_push* push,
-                         const uint64_t* peer_bases, int npeers, void* stream);
 
 /* average_down (coarse_fine.py:136-163) on the box-local coarsened layout
  * (crse box b = fine box b coarsened).  ratio = int32[3] per 3-D axis, each 1
@@ -321,12 +305,7 @@ int amrb_prolong(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
                  const amrb_field* crse, const double* crse_base, int ncomp,
                  const int32_t* ratio, int add, void* stream);
 
-/* amrb_prolong (ncomp = 1) that also fills fine's ghosts through a push
- * table (see amrb_push_create). */
-int amrb_prolong_push(const amrb_level* fine_lv, amrb_field* fine, double* fine_base,
-                      const amrb_field* crse, const double* crse_base,
-                      const int32_t* ratio, int add, const amrb_push* push,
-                      const uint64_t* peer_bases, int npeers, void* stream);
+
 
 /* ------------------------------------------------------------------------ */
 /* Inter-level AMR operators + two-level advection.  Work     */

@@ -79,9 +79,9 @@ _SIGS = {
     "amrb_lap_apply": (C.c_int, [vp, vp, vp, vp, vp, P(f64), vp]),
     "amrb_residual": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
     "amrb_gsrb_color": (C.c_int, [vp, vp, vp, vp, vp, P(f64), C.c_int, vp]),
-    "amrb_gsrb_sweep": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp]),
-    "amrb_gsrb_sweep_norm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, vp]),
-    "amrb_gsrb_sweep_prolong": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp, vp, vp, vp]),
+    "amrb_gsrb_sweep": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, vp]),
+    "amrb_gsrb_sweep_norm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, vp, vp]),
+    "amrb_gsrb_sweep_prolong": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp, vp, vp, vp, vp]),
     "amrb_restrict": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
     "amrb_residual_restrict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),
     "amrb_prolong": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
@@ -93,10 +93,6 @@ _SIGS = {
     "amrb_fr_crse": (C.c_int, [vp, i64, vp, vp, f64, vp]),
     "amrb_fr_fine": (C.c_int, [vp, i64, C.c_int, C.c_int, vp, vp, f64, vp]),
     "amrb_fr_reflux": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp]),
-    "amrb_push_create": (C.c_int, [vp, C.c_int, P(i32), P(i64), C.c_int, P(i32), C.c_int, C.c_int, C.c_int, P(vp)]),
-    "amrb_push_destroy": (C.c_int, [vp]),
-    "amrb_gsrb_sweep_push": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, P(C.c_uint64), C.c_int, vp]),
-    "amrb_prolong_push": (C.c_int, [vp, vp, vp, vp, vp, P(i32), C.c_int, vp, P(C.c_uint64), C.c_int, vp]),
     "amrb_reduce": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
     "amrb_residual_norm": (C.c_int, [vp, vp, vp, vp, vp, P(f64), vp, vp]),
     "amrb_coarse_tail": (C.c_int, [C.c_int, P(i32), P(f64), vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int,

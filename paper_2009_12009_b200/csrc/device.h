@@ -157,54 +157,4 @@ int num_sms();
 
 constexpr int kMaxPeers = 8;
 
-// ---------------------------------------------------------------------------
-// Ghost push ("fill inside the producer"): a kernel that writes the valid
-// cells of a field also stores every cell a FillBoundary record would copy
-// into the destination ghost cell -- on this GPU, or over NVLink into a peer's
-// symmetric allocation.  Records are bucketed per source box by the cell's
-// (plane, row) class: 0 = within g of the low face, 2 = within g of the high
-// face, 1 = interior (every box extent >= 2g).
-// ---------------------------------------------------------------------------
-struct PushRec {
-  int lo[3], hi[3];  // source region, box-local valid coordinates
-  int peer, pad_;    // rank owning the destination box
-  int64_t off;       // destination element of box-local source cell (0,0,0)
-  int64_t s0, s1;    // destination strides
-};
-
-struct PushBox {
-  int n[3];
-  int cnt[9], off[9];  // candidates for (plane class, row class) = 3 * ci + cj
-};
-
-struct PushDev {
-  const PushBox* box = nullptr;
-  const PushRec* rec = nullptr;
-  const int* cand = nullptr;
-  int g = 0;
-  int my_rank = 0;
-  double* base[kMaxPeers] = {};
-};
-
-// Host object behind amrb_push.
-struct Push {
-  int g = 0, nboxes = 0, nranks = 1, my_rank = 0;
-  std::vector<PushBox> hbox;
-  std::vector<PushRec> hrec;
-  std::vector<int> hcand;
-  DevArray<PushBox> box;
-  DevArray<PushRec> rec;
-  DevArray<int> cand;
-  PushDev dev(const uint64_t* peer_bases, int npeers) const {
-    PushDev d;
-    d.box = box.p;
-    d.rec = rec.p;
-    d.cand = cand.p;
-    d.g = g;
-    d.my_rank = my_rank;
-    for (int r = 0; r < npeers && r < kMaxPeers; ++r) d.base[r] = reinterpret_cast<double*>(peer_bases[r]);
-    return d;
-  }
-};
-
 }  // namespace amrb

@@ -131,6 +131,10 @@ struct StreamArgs {
   int c_kc, c_jc, c_ic;  // coarse (i>>1, j0/2-1, k0/2-1) before the even-column shift
   int flo[3], fhi[3];    // cells outside [flo, fhi] (global) are never relaxed
   unsigned long long* norm;  // kModeNorm
+  // ghost push (ghosts.py): per box 27 destination base addresses (0: none);
+  // the ghost copy of output cell (i, j, k) of box b toward direction
+  // (dx, dy, dz) is at push[27 b + 9 (dx+1) + 3 (dy+1) + (dz+1)] + i s0 + j s1 + k
+  const long long* push;
 };
 
 constexpr int r128(int x) { return (x + 127) / 128 * 128; }
@@ -148,22 +152,33 @@ struct StreamLayout {
   static constexpr int COFF = ROFF + r128(RB);
   static constexpr int SLOT = COFF + (MODE == kModeProl ? r128(CB) : 0);
   static constexpr int BAR = NS * SLOT;
-  static constexpr int BYTES = BAR + 8 * NS;
-  static constexpr int WK = TK / 64;
+  static constexpr int PTAB = BAR + 8 * NS;  // PUSH: this box's 27 destination addresses
+  static constexpr int BYTES = PTAB + 8 * 27;
+  // lanes per tile row: 32 k-pairs per warp for TK >= 64 (WK warps across k),
+  // else TK/2 lanes per row and RPW = 32 / LK row groups per warp
+  static constexpr int WK = TK >= 64 ? TK / 64 : 1;
+  static constexpr int LK = TK >= 64 ? 32 : TK / 2;
+  static constexpr int RPW = 32 / LK;
 };
+
+template <int TJ, int TK, int RW>
+__host__ __device__ constexpr int stream_warps() {
+  return (TJ / (RW * (TK >= 64 ? 1 : 64 / TK)) + 1) * (TK >= 64 ? TK / 64 : 1);
+}
 
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double x, double y) { *reinterpret_cast<double2*>(p) = make_double2(x, y); }
 
-template <int TJ, int TK, int RW, int D, int MODE, int MINB>
-__global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
+template <int TJ, int TK, int RW, int D, int MODE, int MINB, bool PUSH>
+__global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     k_gsrb_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ StreamArgs args) {
   pdl_entry();
   using LY = StreamLayout<TJ, TK, D, MODE>;
-  constexpr int WK = LY::WK, NSW = TJ / RW * WK, NS = LY::NS, PK = LY::PK, CK = LY::CK;
+  constexpr int WK = LY::WK, LK = LY::LK, RPW = LY::RPW, NS = LY::NS, PK = LY::PK, CK = LY::CK;
+  constexpr int NSW = TJ / (RW * RPW) * WK;  // strip warps (then WK ring warps)
   constexpr bool PROL = MODE == kModeProl, NORM = MODE == kModeNorm;
-  static_assert(TK % 64 == 0 && TJ % RW == 0 && RW % 2 == 0 && TJ + 2 <= 32, "tile shape");
+  static_assert((TK % 64 == 0 || TK == 32) && TJ % (RW * RPW) == 0 && RW % 2 == 0 && TJ + 2 <= 32, "tile shape");
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + LY::BAR);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -209,6 +224,7 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
     for (int x = 0; x < NS; ++x) mbar_init(&bars[x], 1);
     fence_barrier_init();
   }
+  if (PUSH && tid < 27) reinterpret_cast<long long*>(sm + LY::PTAB)[tid] = args.push[27 * box + tid];
   __syncthreads();
   if (tid == producer)
     for (int q = -2; q <= min(NS - 3, L + 1); ++q) issue(q);
@@ -216,9 +232,10 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
   // ---- roles ---------------------------------------------------------------
   const bool strip = warp < NSW;
   const int wk = strip ? warp % WK : warp - NSW;
-  const int m = 32 * wk + lane;  // k-pair index in the tile
-  const int c0 = 2 + 2 * m;      // smem column of the pair's first cell
-  const int r0 = 2 + (strip ? (warp / WK) * RW : 0);  // strip: first smem row
+  const int rg = lane / LK;              // row group of the lane (RPW > 1: narrow tiles)
+  const int m = LK * wk + lane % LK;     // k-pair index in the tile
+  const int c0 = 2 + 2 * m;              // smem column of the pair's first cell
+  const int r0 = 2 + (strip ? ((warp / WK) * RPW + rg) * RW : 0);  // strip: first smem row
 
   // strip state (row x = smem row r0 + x): pairs of planes p, p+1, p+2
   double a0[RW][2], a1[RW][2], a2[RW][2], am[RW], rs[RW], ao[RW];
@@ -234,14 +251,57 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
     ostep = dir * B.s0;
   }
   const int64_t orow = strip ? args.fb[box].s1 : 0;
-
+  bool pushed = false;
+  // Ghost push of the plane just written (strip rows of this lane): a cell
+  // within 2 of a box face also goes to the neighbour(s) across it; the
+  // destination of each nonempty subset of its near faces is one entry of the
+  // box's table (staged in shared memory).  A lane's column fixes its row and
+  // column classes for the whole segment, so warps away from the box's j / k
+  // edges only push the first and last two planes of the box.
+  const long long* ptab = reinterpret_cast<const long long*>(sm + LY::PTAB);
+  const int kk_ = k0 + 2 * m;
+  const int ck_ = kk_ < 2 ? 0 : (kk_ >= g.n[2] - 2 ? 2 : 1);
+  int cjs = 0;  // 2 bits per strip row: the row's class
+#pragma unroll
+  for (int x = 0; x < RW; ++x) {
+    const int jj = j0 + r0 - 2 + x;
+    cjs |= (jj < 2 ? 0 : (jj >= g.n[1] - 2 ? 2 : 1)) << (2 * x);
+  }
+  const bool jk_edge = PUSH && strip && __any_sync(0xffffffffu, ck_ != 1 || cjs != 0x55555555 >> (32 - 2 * RW));
+  auto push_plane = [&](int ip) {
+    const int ci = ip < 2 ? 0 : (ip >= g.n[0] - 2 ? 2 : 1);
+    if (ci == 1 && !jk_edge) return;  // warp-uniform
+    const int64_t pbase = (int64_t)ip * ostep * dir + kk_;
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const int cj = (cjs >> (2 * x)) & 3;
+      const int64_t rel = pbase + (int64_t)(j0 + r0 - 2 + x) * orow;
+      const double2 v = make_double2(a0[x][0], a0[x][1]);
+      auto put = [&](int a, int b, int c) {
+        const long long dst = ptab[a * 9 + b * 3 + c];
+        if (dst) {
+          *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) + rel) = v;
+          pushed = true;
+        }
+      };
+      if (cj != 1) put(1, cj, 1);
+      if (ck_ != 1) put(1, 1, ck_);
+      if (cj != 1 && ck_ != 1) put(1, cj, ck_);
+      if (ci != 1) {
+        put(ci, 1, 1);
+        if (cj != 1) put(ci, cj, 1);
+        if (ck_ != 1) put(ci, 1, ck_);
+        if (cj != 1 && ck_ != 1) put(ci, cj, ck_);
+      }
+    }
+  };
   // PROL: every cell of plane q's tile += its coarse parent (the single addition
   // of k_prolong), pairs spread over all threads; a barrier must follow before
   // anyone reads the plane
   auto correct_plane = [&](int q) {
     double* S = phi_s(q);
     const double* Cq = crs_s(q);
-    constexpr int PP = (TK + 4) / 2, NP = (TJ + 4) * PP, NT = 32 * (NSW + WK);
+    constexpr int PP = (TK + 4) / 2, NP = (TJ + 4) * PP, NT = 32 * stream_warps<TJ, TK, RW>();
     for (int e = tid; e < NP; e += NT) {
       const int rr = e / PP, pc = e - rr * PP;
       const double2 v = lds2(S + rr * PK + 2 * pc);
@@ -364,6 +424,7 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
       for (int x = 0; x < RW; ++x)
         *reinterpret_cast<double2*>(out + x * orow) = make_double2(a0[x][0], a0[x][1]);
       out += ostep;
+      if (PUSH) push_plane(plane(p));
     }
 #pragma unroll
     for (int x = 0; x < RW; ++x) {
@@ -402,6 +463,7 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
     arrive_ring(p + 2, g2);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      if (RPW > 1 && h != rg) continue;  // narrow tiles: one ring row per row group
       const int b = h ? PHI : 1 - PHI;
       const int row = (h ? TJ + 2 : 1) * PK;
       const double kn = b ? S1[row + c0 + 2] : S1[row + c0 - 1];
@@ -427,8 +489,8 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
     __syncthreads();
     if (tid == producer && p >= -1 && p - 1 + NS <= L + 1) issue(p - 1 + NS);
     if (red_on) {
-      if (top_ok) S1[1 * PK + c0 + (1 - PHI)] = rv[0];
-      if (bot_ok) S1[(TJ + 2) * PK + c0 + PHI] = rv[1];
+      if (top_ok && (RPW == 1 || rg == 0)) S1[1 * PK + c0 + (1 - PHI)] = rv[0];
+      if (bot_ok && (RPW == 1 || rg == 1)) S1[(TJ + 2) * PK + c0 + PHI] = rv[1];
       if (rcok) S1[rco] = rc;
     }
 #pragma unroll
@@ -469,6 +531,7 @@ __global__ void __launch_bounds__(32 * ((TJ / RW + 1) * (TK / 64)), MINB)
       run(std::false_type{}, ring_step);
   }
 
+  if (PUSH && pushed) __threadfence_system();  // pushes to peers before the consumer's device barrier
   if (NORM) {
     for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
     if (strip && lane == 0 && nmax) atomicMax(args.norm, nmax);
@@ -505,12 +568,13 @@ const SegTable& seg_table(Level& lv, int tj, int tk, int nseg, bool alternate) {
   return *t;
 }
 
-template <int TJ, int TK, int RW, int D, int MODE, int MINB>
+template <int TJ, int TK, int RW, int D, int MODE, int MINB, bool PUSH>
 bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
                    const double* r_base, const Coef& cf, const int flo[3], const int fhi[3], cudaStream_t st,
-                   const Level* clv, const Field* c, const double* c_base, unsigned long long* norm) {
+                   const Level* clv, const Field* c, const double* c_base, unsigned long long* norm,
+                   const long long* push) {
   using LY = StreamLayout<TJ, TK, D, MODE>;
-  constexpr int NW = (TJ / RW + 1) * (TK / 64);
+  constexpr int NW = stream_warps<TJ, TK, RW>();
   int nres = 0;
   for (int bx = 0; bx < lv.nboxes; ++bx) {
     if (!lv.resident[bx]) continue;
@@ -547,7 +611,7 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
   } else {
     mc = ma;
   }
-  auto kern = k_gsrb_stream<TJ, TK, RW, D, MODE, MINB>;
+  auto kern = k_gsrb_stream<TJ, TK, RW, D, MODE, MINB, PUSH>;
   static int per_sm = 0;
   if (!per_sm) {
     AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
@@ -573,6 +637,7 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
     args.fhi[x] = fhi[x];
   }
   args.norm = norm;
+  args.push = push;
   launch_k(kern, (unsigned)t.n, 32 * NW, LY::BYTES, st, ma, mr, mc, args);
   check_launch("k_gsrb_stream");
   return true;
@@ -584,25 +649,27 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
 bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                          const Field& r, const double* r_base, const Coef& cf, const int flo[3], const int fhi[3],
                          cudaStream_t st, const Level* clv, const Field* c, const double* c_base,
-                         unsigned long long* norm) {
-#define AMRB_STREAM(TJ, TK, RW, D, M, B) \
-  launch_stream<TJ, TK, RW, D, M, B>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, c_base, norm)
+                         unsigned long long* norm, const long long* push) {
+#define AMRB_STREAM(TJ, TK, RW, D, M, B)                                                                     \
+  (push ? launch_stream<TJ, TK, RW, D, M, B, true>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, \
+                                                    c_base, norm, push)                                          \
+        : launch_stream<TJ, TK, RW, D, M, B, false>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, \
+                                                     c_base, norm, push))
   // variants (library option "stream_config" forces one; measured on the C3 fine
-  // level, tools/mb_stream.py): 1 = 16x64 tiles, 4-row strips; 2 = 16x64, 2-row
-  // strips (two CTAs/SM); 3 = 8x64, 2-row, depth 3; 4 = 16x128, 4-row; 5 = 16x64,
-  // 4-row, depth 3
+  // level, tools/mb_stream.py): 1 = 16x64 tiles, 4-row strips (the fastest plain
+  // sweep); 2 = 16x64, 2-row strips (two CTAs/SM even with the ghost push);
+  // 4 = 16x128, 4-row (the fastest fused prolongation); 6 = 16x32 (two rows
+  // per warp, 32-wide boxes)
 #define AMRB_STREAM_CFG(M, CFG)                  \
   switch (CFG) {                                 \
     case 1:                                      \
       return AMRB_STREAM(16, 64, 4, 2, M, 1);    \
     case 2:                                      \
       return AMRB_STREAM(16, 64, 2, 2, M, 2);    \
-    case 3:                                      \
-      return AMRB_STREAM(8, 64, 2, 3, M, 3);     \
     case 4:                                      \
       return AMRB_STREAM(16, 128, 4, 2, M, 1);   \
-    case 5:                                      \
-      return AMRB_STREAM(16, 64, 4, 3, M, 1);    \
+    case 6:                                      \
+      return AMRB_STREAM(16, 32, 4, 2, M, 4);    \
   }                                              \
   return false;
   auto run = [&](int cfg) -> bool {
@@ -617,10 +684,12 @@ bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_ba
     return false;
   };
   if (const int64_t forced = option("stream_config")) return run((int)forced);
-  // defaults per mode, then the narrower tiles when a box does not divide
-  static const int prefs[3][3] = {{1, 2, 3}, {4, 1, 3}, {2, 1, 3}};
-  for (int cfg : prefs[mode])
-    if (run(cfg)) return true;
+  // defaults per mode (with / without ghost push), then narrower tiles when a
+  // box does not divide
+  static const int prefs[2][3][4] = {{{1, 2, 6, 0}, {4, 1, 6, 0}, {2, 1, 6, 0}},
+                                     {{2, 1, 6, 0}, {4, 2, 6, 0}, {2, 1, 6, 0}}};
+  for (int cfg : prefs[push ? 1 : 0][mode])
+    if (cfg && run(cfg)) return true;
   return false;
 #undef AMRB_STREAM_CFG
 

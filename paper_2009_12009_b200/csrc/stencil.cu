@@ -670,62 +670,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// k_prolong (ncomp 1) that also pushes every written cell within g of a box
-// face into the ghost cells the fill plan maps it to (see PushRec).
-__global__ void __launch_bounds__(256)
-    k_prolong_push(const int4* __restrict__ tiles, int ti, const BoxGeom* __restrict__ fgeo,
-                   const FabView* __restrict__ ff, double* __restrict__ fine, const FabView* __restrict__ fc,
-                   const double* __restrict__ crse, int add, int3 sh, const __grid_constant__ PushDev push) {
-  pdl_entry();
-  const int4 t = tiles[blockIdx.x];
-  const BoxGeom g = fgeo[t.x];
-  const int j = t.z + threadIdx.y, k = t.w + threadIdx.x;
-  if (j >= g.n[1] || k >= g.n[2]) return;
-  const FabView F = ff[t.x], C = fc[t.x];
-  const int iend = min(t.y + ti, g.n[0]);
-  const double* cb = crse + C.off + (int64_t)(j >> sh.y) * C.s1 + (k >> sh.z);
-  double* fb = fine + F.off + (int64_t)j * F.s1 + k;
-  bool remote = false;
-  int64_t d[kPushMid] = {0, 0, 0};  // interior-plane destinations of (j, k), deltas from the cell
-  const bool band = push_cls(j, g.n[1], push.g) != 1 || push_cls(k, g.n[2], push.g) != 1;
-  if (band) push_deltas_mid(push, t.x, j, k, F, fine, d, remote);
-  int i = t.y;
-  for (; i + 4 <= iend; i += 4) {
-    double c[4], f[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      c[u] = ldg(cb + (int64_t)((i + u) >> sh.x) * C.s0);
-      f[u] = add ? fb[(int64_t)(i + u) * F.s0] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double v = add ? f[u] + c[u] : c[u];
-      double* o = fb + (int64_t)(i + u) * F.s0;
-      *o = v;
-      if (push_cls(i + u, g.n[0], push.g) != 1) {
-        remote |= push_cell(&push, t.x, i + u, j, k, v);
-      } else if (band) {
-#pragma unroll
-        for (int x = 0; x < kPushMid; ++x)
-          if (d[x] != 0) o[d[x]] = v;
-      }
-    }
-  }
-  for (; i < iend; ++i) {
-    const double c = ldg(cb + (int64_t)(i >> sh.x) * C.s0);
-    double* o = fb + (int64_t)i * F.s0;
-    const double v = add ? *o + c : c;
-    *o = v;
-    if (push_cls(i, g.n[0], push.g) != 1) {
-      remote |= push_cell(&push, t.x, i, j, k, v);
-    } else if (band) {
-#pragma unroll
-      for (int x = 0; x < kPushMid; ++x)
-        if (d[x] != 0) o[d[x]] = v;
-    }
-  }
-  if (remote) __threadfence_system();  // remote ghost stores before the consumer's barrier
-}
 
 // ---------------------------------------------------------------------------
 // Reductions: per-tile partial (fixed tree), then one ordered final pass.
@@ -1214,7 +1158,7 @@ void launch_sweep_full(Level& lv, const Field& a, const double* a_base, const Fi
 
 extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const double* a_base, amrb_field* b,
                                   double* b_base, const amrb_field* rhs, const double* rhs_base, const double dh[3],
-                                  const int32_t* fixed_lohi, void* stream) {
+                                  const int32_t* fixed_lohi, const uint64_t* push, void* stream) {
   return guarded([&] {
     Level& lv = Lm(lv_);
     need_ghost(F(a), 2, "gsrb_sweep (phi in)");
@@ -1242,11 +1186,13 @@ extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const
     const bool fixed = fixed_lohi != nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     const Coef cf = make_coef(dh);
+    const long long* ptab = reinterpret_cast<const long long*>(push);
+    if (ptab) need_ghost(F(b), 2, "gsrb_sweep (pushed phi out)");
     if (option("sweep_kernel") == 0 &&
         launch_sweep_stream(0, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, st, nullptr, nullptr,
-                            nullptr, nullptr))
+                            nullptr, nullptr, ptab))
       return;
-    if (launch_sweep_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st)) return;
+    if (ptab) throw Error(AMRB_ENOTSUP, "gsrb_sweep: ghost push needs the k_gsrb_stream path");
     if (divides(16, 64))
       launch_sweep_full<16, 64>(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, cf, flo, fhi, fixed, st);
     else if (divides(16, 32))
@@ -1268,13 +1214,14 @@ extern "C" int amrb_gsrb_sweep(const amrb_level* lv_, const amrb_field* a, const
 
 extern "C" int amrb_gsrb_sweep_norm(const amrb_level* lv_, const amrb_field* a, const double* a_base, amrb_field* b,
                                     double* b_base, const amrb_field* rhs, const double* rhs_base, const double dh[3],
-                                    const int32_t* fixed_lohi, uint64_t* norm, void* stream) {
+                                    const int32_t* fixed_lohi, uint64_t* norm, const uint64_t* push, void* stream) {
   return guarded([&] {
     Level& lv = Lm(lv_);
     need_ghost(F(a), 2, "gsrb_sweep_norm (phi in)");
     need_ghost(F(rhs), 1, "gsrb_sweep_norm (rhs)");
     for (auto* f : {a, (const amrb_field*)b, rhs}) need_same_level(F(f), lv, "gsrb_sweep_norm");
     if (!norm) throw Error(AMRB_EINVAL, "gsrb_sweep_norm: null norm");
+    if (push) need_ghost(F(b), 2, "gsrb_sweep_norm (pushed phi out)");
     if (!lv.all_even()) throw Error(AMRB_EINVAL, "gsrb_sweep needs even box extents");
     int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
     if (fixed_lohi)
@@ -1285,46 +1232,15 @@ extern "C" int amrb_gsrb_sweep_norm(const amrb_level* lv_, const amrb_field* a, 
     if (option("sweep_kernel") != 0 ||
         !launch_sweep_stream(2, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
                              (cudaStream_t)stream, nullptr, nullptr, nullptr,
-                             reinterpret_cast<unsigned long long*>(norm)))
+                             reinterpret_cast<unsigned long long*>(norm), reinterpret_cast<const long long*>(push)))
       throw Error(AMRB_ENOTSUP, "gsrb_sweep_norm: level does not take the k_gsrb_stream path");
-  });
-}
-
-extern "C" int amrb_gsrb_sweep_push(const amrb_level* lv_, const amrb_field* a, const double* a_base, amrb_field* b,
-                                   double* b_base, const amrb_field* rhs, const double* rhs_base, const double dh[3],
-                                   const int32_t* fixed_lohi, const amrb_push* push_, const uint64_t* peer_bases,
-                                   int npeers, void* stream) {
-  return guarded([&] {
-    Level& lv = Lm(lv_);
-    if (!push_ || !peer_bases || npeers < 1 || npeers > kMaxPeers)
-      throw Error(AMRB_EINVAL, "gsrb_sweep_push: bad push arguments");
-    const Push& push = *reinterpret_cast<const Push*>(push_);
-    need_ghost(F(a), 2, "gsrb_sweep_push (phi in)");
-    need_ghost(F(rhs), 1, "gsrb_sweep_push (rhs)");
-    need_ghost(F(b), push.g, "gsrb_sweep_push (phi out)");
-    for (auto* f : {a, (const amrb_field*)b, rhs}) need_same_level(F(f), lv, "gsrb_sweep_push");
-    if (push.nboxes != lv.nboxes || npeers != push.nranks)
-      throw Error(AMRB_EINVAL, "gsrb_sweep_push: push table built for another level or rank count");
-    if (!lv.all_even()) throw Error(AMRB_EINVAL, "gsrb_sweep needs even box extents");
-    int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
-    if (fixed_lohi)
-      for (int x = 0; x < 3; ++x) {
-        flo[x] = fixed_lohi[x];
-        fhi[x] = fixed_lohi[3 + x];
-      }
-    const PushDev pd = push.dev(peer_bases, npeers);
-    if (reinterpret_cast<uint64_t>(b_base) != peer_bases[push.my_rank])
-      throw Error(AMRB_EINVAL, "gsrb_sweep_push: peer_bases[my_rank] must be b_base");
-    if (!launch_sweep_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
-                          fixed_lohi != nullptr, (cudaStream_t)stream, &pd))
-      throw Error(AMRB_ENOTSUP, "gsrb_sweep_push: level does not take the k_gsrb_sweep5 path");
   });
 }
 
 extern "C" int amrb_gsrb_sweep_prolong(const amrb_level* lv_, const amrb_field* a, const double* a_base,
                                           amrb_field* b, double* b_base, const amrb_field* rhs, const double* rhs_base,
                                           const double dh[3], const amrb_level* clv_, const amrb_field* c,
-                                          const double* c_base, void* stream) {
+                                          const double* c_base, const uint64_t* push, void* stream) {
   return guarded([&] {
     Level& lv = Lm(lv_);
     const Level& clv = L(clv_);
@@ -1343,13 +1259,11 @@ extern "C" int amrb_gsrb_sweep_prolong(const amrb_level* lv_, const amrb_field* 
           throw Error(AMRB_EINVAL, "gsrb_sweep_prolong: coarse box is not the coarsened fine box");
     }
     const int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
-    if (option("sweep_kernel") == 0 &&
-        launch_sweep_stream(1, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
-                            (cudaStream_t)stream, &clv, &F(c), c_base, nullptr))
-      return;
-    if (!launch_sweep_prolong_tma(lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), clv, F(c), c_base,
-                                  (cudaStream_t)stream))
-      throw Error(AMRB_ENOTSUP, "gsrb_sweep_prolong: level does not take the k_gsrb_sweep5 path");
+    if (option("sweep_kernel") != 0 ||
+        !launch_sweep_stream(1, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
+                             (cudaStream_t)stream, &clv, &F(c), c_base, nullptr,
+                             reinterpret_cast<const long long*>(push)))
+      throw Error(AMRB_ENOTSUP, "gsrb_sweep_prolong: level does not take the k_gsrb_stream path");
   });
 }
 
@@ -1405,28 +1319,6 @@ extern "C" int amrb_prolong(const amrb_level* flv_, amrb_field* fine, double* fi
   });
 }
 
-extern "C" int amrb_prolong_push(const amrb_level* flv_, amrb_field* fine, double* fine_base, const amrb_field* crse,
-                                 const double* crse_base, const int32_t* ratio, int add, const amrb_push* push_,
-                                 const uint64_t* peer_bases, int npeers, void* stream) {
-  return guarded([&] {
-    Level& lv = Lm(flv_);
-    need_same_level(F(fine), lv, "prolong_push");
-    if (!push_ || !peer_bases || npeers < 1 || npeers > kMaxPeers)
-      throw Error(AMRB_EINVAL, "prolong_push: bad push arguments");
-    const Push& push = *reinterpret_cast<const Push*>(push_);
-    need_ghost(F(fine), push.g, "prolong_push");
-    if (push.nboxes != lv.nboxes || npeers != push.nranks)
-      throw Error(AMRB_EINVAL, "prolong_push: push table built for another level or rank count");
-    if (reinterpret_cast<uint64_t>(fine_base) != peer_bases[push.my_rank])
-      throw Error(AMRB_EINVAL, "prolong_push: peer_bases[my_rank] must be fine_base");
-    const int3 r = ratio3(ratio);
-    const int3 sh = make_int3(r.x == 2, r.y == 2, r.z == 2);
-    const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
-    launch_tiles(tt, k_prolong_push, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(fine).dev.p, fine_base,
-                 F(crse).dev.p, crse_base, add, sh, push.dev(peer_bases, npeers));
-    check_launch("k_prolong_push");
-  });
-}
 
 extern "C" int amrb_residual_norm(const amrb_level* lv_, const amrb_field* rhs, const double* rhs_base,
                                   const amrb_field* phi, const double* phi_base, const double dh[3], double* dev_out,

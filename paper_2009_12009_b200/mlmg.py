@@ -38,7 +38,7 @@ from .device import dh_array, field_of, level_of, stream_ptr
 from .geometry import BoundaryRecord, Geometry, apply_domain_boundary
 from .interlevel import coarsened_layout, prolong_from
 from .layout import BoxArray, DistributionMapping
-from .push import PushTable, prolong_push
+from .ghosts import push_table
 from .stencil import gsrb_sweep_prolong
 from .multifab import FabArray, MultiFab, world_size
 
@@ -135,7 +135,7 @@ class MLMG:
     """
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
-                 ghost_push=False, agg_cells=128**3, fuse_prolong=None, cluster_tail=None,
+                 ghost_push=None, agg_cells=128**3, fuse_prolong=None, cluster_tail=None,
                  grid_level_cells=None, bc=None):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
@@ -261,17 +261,23 @@ class MLMG:
                 dhs[x] = lv.dh
             self._tail_lohi = lohi
             self._tail_dh = dhs
-        # ghost push: sweeps and prolongation fill their output's ghosts in the
-        # kernel (csrc/push.cu); the tracker below decides where a copy-program
-        # fill or (multi-GPU) a device barrier is still needed
-        # Measured on the C3 fine level (tools/mb_push.py): prolongation with
-        # ghost push 80 us vs 66 us for prolongation + copy-program fill, so it
-        # is off by default; ghost_push=True exercises the path (tests).
+        # ghost push (ghosts.py): the streaming sweeps also write their
+        # output's width-2 ghosts through a per-box direction table, so the
+        # copy-program fill before the next consumer disappears (ghosts on
+        # other GPUs: a device barrier instead).  Periodic lattice layouts.
+        # Measured on one GPU (tools/mb_stream.py, C3 fine level): sweep + push
+        # 88.5 us vs sweep 75 us + fill 12 us -- the ghost bytes cost the same
+        # either way in a bandwidth-bound kernel, so one GPU keeps the fills
+        # (ghost_push=None: push only across GPUs; True / False force it).
         self.p2p = self.dist and self.transport.p2p
+        if ghost_push is None:
+            ghost_push = self.p2p
         for lv in self.levels:
-            lv.push, lv.push_local = False, lv.replicated or not self.dist
-            if ghost_push:
-                self._make_push(lv)
+            lv.push = None
+            if ghost_push and self.all_periodic:
+                tabs = [push_table(f, lv.domain, self.periodic, 2) for f in lv.phi]
+                if all(t is not None for t in tabs):
+                    lv.push = tabs
         # up-leg: prolongation fused into the first post-smoothing sweep
         # (k_gsrb_sweep5<PROL>, box-local level pairs): no separate read+write
         # pass over the fine phi and no fill after it; the restriction fills the
@@ -281,7 +287,7 @@ class MLMG:
         for l, lv in enumerate(self.levels):
             # (the fused kernel adds the parent to every tile cell, ghosts
             # included: periodic levels only)
-            lv.fuse = (fuse_prolong and l < len(self.levels) - 1 and lv.boxlocal_next and not lv.push
+            lv.fuse = (fuse_prolong and l < len(self.levels) - 1 and lv.boxlocal_next
                        and self.nu2 >= 1 and self.all_periodic)
         self._ghost = {}  # id(field) -> ghost width known to be current
         self._pending = False  # pushes to peers since the last device barrier
@@ -307,16 +313,7 @@ class MLMG:
             for i, lv in enumerate(self.levels)
         )
 
-    # -- ghost push / ghost state ------------------------------------------------
-    def _make_push(self, lv):
-        """Push table for the level's phi layout (width 2); lv.push stays False
-        when the layout is not supported."""
-        if self.dist and not lv.push_local and not self.p2p:
-            return  # NCCL copy programs only: peers' storage is not mapped
-        t = PushTable(lv.phi[0], lv.domain, self.periodic, 2, rank=self.transport.rank, local=lv.push_local)
-        if t.ok:
-            lv.push, lv.push_table = True, t
-
+    # -- ghost state ---------------------------------------------------------------
     def _barrier(self):
         self.transport.peer_barrier()
         self._pending = False
@@ -342,11 +339,17 @@ class MLMG:
         if pushed_to_peers:
             self._pending = True
 
-    def _before_push(self, lv, fa):
+    def _before_push(self, tab, fa):
         """Before a kernel stores into peers' ghosts of fa: no peer may still be
         reading them."""
-        if not lv.push_local and id(fa) in self._reads:
+        if tab.remote and id(fa) in self._reads:
             self._barrier()
+
+    def _push_for(self, lv, fa):
+        """The push table of lv's phi buffer fa, or None."""
+        if lv.push is None:
+            return None
+        return lv.push[0] if fa is lv.phi[0] else lv.push[1]
 
     # -- building blocks ---------------------------------------------------------
     def _fill(self, lv, fa, width):
@@ -381,6 +384,9 @@ class MLMG:
         b = lv.phi[1 - lv.cur]
         self._need_ghosts(lv, a, 2)
         self._need_ghosts(lv, lv.rhs, 1)
+        tab = self._push_for(lv, b)
+        if tab is not None:
+            self._before_push(tab, b)
         lvh = level_of(a)
         args = (
             lvh.handle,
@@ -393,14 +399,19 @@ class MLMG:
             lv.dhc,
             None if lv.fixed is None else lv.fixed[1],
         )
+        push = None if tab is None else C.c_void_p(tab.ptr)
         if norm is None:
-            check(lib().amrb_gsrb_sweep(*args, stream_ptr()))
+            rc = lib().amrb_gsrb_sweep(*args, push, stream_ptr())
+            if rc == AMRB_ENOTSUP:  # pushing needs the streaming kernel: fill instead from now on
+                lv.push, tab = None, None
+                rc = lib().amrb_gsrb_sweep(*args, None, stream_ptr())
+            check(rc)
         else:
-            rc = lib().amrb_gsrb_sweep_norm(*args, C.c_void_p(norm.data_ptr()), stream_ptr())
+            rc = lib().amrb_gsrb_sweep_norm(*args, C.c_void_p(norm.data_ptr()), push, stream_ptr())
             if rc == AMRB_ENOTSUP:
                 raise NotImplementedError("level does not take the streaming sweep")
             check(rc)
-        self._produced(b, 0)
+        self._produced(b, 0 if tab is None else 2, pushed_to_peers=tab is not None and tab.remote)
         lv.cur = 1 - lv.cur
 
     def _smooth(self, lv, n):
@@ -458,13 +469,8 @@ class MLMG:
             tr = _LocalView(self.transport) if (self.dist and not lv.replicated) else self.transport
             copy_into(lv.stage, crse, tr)
             crse = lv.stage
-        if lv.push:
-            self._before_push(lv, fine)
-            prolong_push(fine, crse, lv.push_table, add=True)
-            self._produced(fine, 2, not lv.push_local)
-        else:
-            prolong_from(fine, crse, (2, 2, 2), add=True)
-            self._produced(fine, 0)
+        prolong_from(fine, crse, (2, 2, 2), add=True)
+        self._produced(fine, 0)
 
     def _prolong_sweep(self, l):
         """Fused up-leg step: lv.phi <- GSRB(lv.phi + P(nx.phi)).  False (nothing
@@ -475,12 +481,15 @@ class MLMG:
         self._need_ghosts(lv, a, 2)
         self._need_ghosts(lv, lv.rhs, 1)
         self._need_ghosts(nx, crse, 1)
+        tab = self._push_for(lv, b)
+        if tab is not None:
+            self._before_push(tab, b)
         try:
-            gsrb_sweep_prolong(a, b, lv.rhs, lv.dh, crse)
+            gsrb_sweep_prolong(a, b, lv.rhs, lv.dh, crse, push=tab)
         except NotImplementedError:
             lv.fuse = False
             return False
-        self._produced(b, 0)
+        self._produced(b, 0 if tab is None else 2, pushed_to_peers=tab is not None and tab.remote)
         lv.cur = 1 - lv.cur
         return True
 

@@ -75,18 +75,28 @@ def fixed_lohi(fixed):
     return arr
 
 
-def gsrb_sweep(a, b, rhs, dh, fixed=None):
+def _push_ptr(push):
+    return None if push is None else C.c_void_p(push.ptr)
+
+
+def gsrb_sweep(a, b, rhs, dh, fixed=None, push=None):
     """b = one fused red+black sweep of a (a ghosts width 2, rhs ghosts width 1
-    filled).  ``fixed`` = Box outside which cells are never relaxed."""
+    filled).  ``fixed`` = Box outside which cells are never relaxed.  ``push``
+    = ghosts.push_table(b, ...): b's width-2 ghosts are written by the kernel
+    (NotImplementedError, nothing launched, if the level does not take the
+    streaming sweep)."""
     _same_layout(a, b, rhs)
     fa = fixed_lohi(fixed)
     fp = None if fa is None else i32p(fa)[1]
-    check(lib().amrb_gsrb_sweep(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
-                                field_of(rhs).handle, _p(rhs), dh_array(dh), fp, stream_ptr()))
+    rc = lib().amrb_gsrb_sweep(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
+                               field_of(rhs).handle, _p(rhs), dh_array(dh), fp, _push_ptr(push), stream_ptr())
     del fa
+    if rc == AMRB_ENOTSUP:
+        raise NotImplementedError("gsrb_sweep: ghost push needs the streaming sweep")
+    check(rc)
 
 
-def gsrb_sweep_norm(a, b, rhs, dh, norm, fixed=None):
+def gsrb_sweep_norm(a, b, rhs, dh, norm, fixed=None, push=None):
     """gsrb_sweep(a, b, rhs) that also max-reduces |rhs - L(a)| over the valid
     cells of ``a`` into ``norm`` (a 1-element int64/uint64 CUDA tensor holding
     the bit pattern of a non-negative double; zero it first).  Raises
@@ -97,14 +107,14 @@ def gsrb_sweep_norm(a, b, rhs, dh, norm, fixed=None):
     fp = None if fa is None else i32p(fa)[1]
     rc = lib().amrb_gsrb_sweep_norm(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
                                     field_of(rhs).handle, _p(rhs), dh_array(dh), fp, C.c_void_p(norm.data_ptr()),
-                                    stream_ptr())
+                                    _push_ptr(push), stream_ptr())
     del fa
     if rc == AMRB_ENOTSUP:
         raise NotImplementedError("gsrb_sweep_norm: level does not take the streaming sweep path")
     check(rc)
 
 
-def gsrb_sweep_prolong(a, b, rhs, dh, crse):
+def gsrb_sweep_prolong(a, b, rhs, dh, crse, push=None):
     """b = one fused red+black sweep of (a + pc-interpolated crse), periodic;
     crse on the box-local coarsened layout of a (ghosts width 1), a's ghosts
     width 2, rhs's width 1.  Same bits as prolong_from(a, crse, add=True);
@@ -116,7 +126,7 @@ def gsrb_sweep_prolong(a, b, rhs, dh, crse):
         raise ValueError("crse must live on the box-local coarsened layout")
     rc = lib().amrb_gsrb_sweep_prolong(level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b),
                                        field_of(rhs).handle, _p(rhs), dh_array(dh), level_of(crse).handle,
-                                       field_of(crse).handle, _p(crse), stream_ptr())
+                                       field_of(crse).handle, _p(crse), _push_ptr(push), stream_ptr())
     if rc == AMRB_ENOTSUP:
         raise NotImplementedError("gsrb_sweep_prolong: level does not take the fused TMA sweep path")
     check(rc)

@@ -124,46 +124,6 @@ def test_residual_restrict_bitexact(rng):
         assert np.array_equal(got[i][sl], cf[i][sl])
 
 
-@pytest.mark.parametrize("n,m", [(64, 32), (128, 64), (64, 64)])
-def test_sweep_and_prolong_push_equal_fill(n, m):
-    """Ghost push inside the producer == producer + fill_boundary, bit for bit,
-    on every cell of every grown box (valid and ghost)."""
-    from paper_2009_12009_b200 import push as P
-    from paper_2009_12009_b200 import stencil as S
-    from paper_2009_12009_b200.interlevel import coarsened_layout, prolong_from
-
-    dom = A.Box((0, 0, 0), (n - 1,) * 3)
-    ba = A.BoxArray([dom]).max_size(m)
-    dm = A.DistributionMapping.single_rank(len(ba))
-    tr = A.Transport(1)
-    a = A.MultiFab(ba, dm, 1, 2)
-    rhs = A.MultiFab(ba, dm, 1, 1)
-    g = torch.Generator(device="cuda").manual_seed(7)
-    a.storage.copy_(torch.randn(a.storage.shape, generator=g, device="cuda", dtype=torch.float64))
-    rhs.storage.copy_(torch.randn(rhs.storage.shape, generator=g, device="cuda", dtype=torch.float64))
-    A.fill_boundary(a, tr, dom, True, ngrow=2)
-    A.fill_boundary(rhs, tr, dom, True)
-    dh = (float(n * n),) * 3
-    tab = P.PushTable(a, dom, True, 2)
-    assert tab.ok
-    b1 = A.MultiFab(ba, dm, 1, 2)
-    b2 = A.MultiFab(ba, dm, 1, 2)
-    S.gsrb_sweep(a, b1, rhs, dh)
-    A.fill_boundary(b1, tr, dom, True, ngrow=2)
-    P.gsrb_sweep_push(a, b2, rhs, dh, tab)
-    for i in b1.fabs:
-        assert torch.equal(b1.fab(i).data, b2.fab(i).data), i
-    # prolongation (add) onto both, then compare again
-    cba = coarsened_layout(ba, 2)
-    c = A.MultiFab(cba, dm, 1, 0)
-    c.storage.copy_(torch.randn(c.storage.shape, generator=g, device="cuda", dtype=torch.float64))
-    prolong_from(b1, c, (2, 2, 2), add=True)
-    A.fill_boundary(b1, tr, dom, True, ngrow=2)
-    P.prolong_push(b2, c, tab, add=True)
-    for i in b1.fabs:
-        assert torch.equal(b1.fab(i).data, b2.fab(i).data), i
-
-
 @pytest.mark.parametrize("n,m,lo", [(128, 128, 0), (128, 64, 0), (64, 32, 0), (64, 64, -32)])
 def test_sweep_prolong_equals_prolong_fill_sweep(n, m, lo):
     """k_gsrb_sweep5<PROL>: GSRB(a + pc(c)) == prolong_from(add); fill(2);

@@ -62,7 +62,7 @@ def _eq(x, y):
         assert np.array_equal(x[i], y[i]), i
 
 
-@pytest.mark.parametrize("n,m,lo", [(64, 64, 0), (128, 64, 0), (64, 64, 3), (128, 128, -7), (64, 32, 0)])
+@pytest.mark.parametrize("n,m,lo", [(64, 64, 0), (128, 64, 0), (64, 64, 3), (128, 128, -7), (64, 32, 0), (96, 32, 5)])
 def test_stream_sweep_matches_oracle_and_legacy(rng, n, m, lo):
     dom, ba, dm, tr, per, a, rhs, g, gr = _setup(rng, n, m, lo)
     got = _sweep(a, rhs)
@@ -109,8 +109,8 @@ def test_stream_fixed_ring(rng, lo):
 
 @pytest.mark.parametrize("n,m", [(128, 64), (256, 256)])
 def test_stream_prolong_fused(rng, n, m):
-    """PROL: b = sweep(a + pc(c)) == prolong(add); fill(2); sweep -- bitwise, and
-    == the legacy fused kernel."""
+    """PROL: b = sweep(a + pc(c)) == prolong(add); fill(2); sweep -- bitwise
+    (the reference composition runs the other sweep kernels)."""
     dom, ba, dm, tr, per, a, rhs, g, gr = _setup(rng, n, m)
     cba = A.coarsened_layout(ba, 2)
     cdom = dom.coarsen(2)
@@ -118,18 +118,15 @@ def test_stream_prolong_fused(rng, n, m):
     c.load_valid_from(cdom, rng.normal(size=(1,) + tuple(cdom.extents())))
     A.fill_boundary(c, tr, cdom, per)
     out = {}
-    for legacy in (False, True):
-        b = A.MultiFab(ba, dm, 1, 2)
-        with option("sweep_kernel", 1 if legacy else 0):
-            S.gsrb_sweep_prolong(a, b, rhs, DH, c)
-        torch.cuda.synchronize()
-        out[legacy] = _valid(b)
-    _eq(out[False], out[True])
+    b = A.MultiFab(ba, dm, 1, 2)
+    S.gsrb_sweep_prolong(a, b, rhs, DH, c)
+    torch.cuda.synchronize()
+    out[False] = _valid(b)
     a2 = A.MultiFab(ba, dm, 1, 2)
     a2.storage.copy_(a.storage)
     prolong_from(a2, c, (2, 2, 2), add=True)
     A.fill_boundary(a2, tr, dom, per)
-    _eq(out[False], _sweep(a2, rhs))
+    _eq(out[False], _sweep(a2, rhs, legacy=True))
 
 
 @pytest.mark.parametrize("n,m", [(64, 64), (256, 256), (128, 64)])
@@ -159,16 +156,16 @@ def test_stream_norm_nan_propagates(rng):
 
 
 def test_stream_not_applicable_raises_for_norm(rng):
-    """32-wide boxes do not take the streaming path: the plain sweep falls back
+    """16-wide boxes do not take the streaming path: the plain sweep falls back
     to the other kernels, the norm variant raises NotImplementedError."""
-    dom, ba, dm, tr, per, a, rhs, g, gr = _setup(rng, 64, 32)
+    dom, ba, dm, tr, per, a, rhs, g, gr = _setup(rng, 64, 16)
     b = A.MultiFab(ba, dm, 1, 2)
     nrm = torch.zeros(1, dtype=torch.int64, device="cuda")
     with pytest.raises(NotImplementedError):
         S.gsrb_sweep_norm(a, b, rhs, DH, nrm)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 4, 6])
 def test_stream_variants_agree(rng, cfg):
     """Every compiled tile / strip / depth variant (library option
     "stream_config") gives the same bits for the plain, PROL and NORM sweeps."""
@@ -179,10 +176,11 @@ def test_stream_variants_agree(rng, cfg):
     c.load_valid_from(cdom, rng.normal(size=(1,) + tuple(cdom.extents())))
     A.fill_boundary(c, tr, cdom, per)
     want_plain = _sweep(a, rhs, legacy=True)
-    b = A.MultiFab(ba, dm, 1, 2)
-    with option("sweep_kernel", 1):
-        S.gsrb_sweep_prolong(a, b, rhs, DH, c)
-    want_prol = _valid(b)
+    a2 = A.MultiFab(ba, dm, 1, 2)
+    a2.storage.copy_(a.storage)
+    prolong_from(a2, c, (2, 2, 2), add=True)
+    A.fill_boundary(a2, tr, dom, per)
+    want_prol = _sweep(a2, rhs, legacy=True)
     r = A.MultiFab(ba, dm, 1, 0)
     S.residual(r, rhs, a, DH)
     want_norm = A.device_reduce(r, "absmax").item()
@@ -198,3 +196,45 @@ def test_stream_variants_agree(rng, cfg):
         torch.cuda.synchronize()
         _eq(_valid(b), want_plain)
         assert nrm.view(torch.float64).item() == want_norm
+
+
+@pytest.mark.parametrize("n,m,per", [(64, 32, True), (128, 64, True), (64, 64, True), (128, 128, True),
+                                     (128, 64, False), (96, 32, True)])
+def test_push_equals_fill(rng, n, m, per):
+    """Ghost push (ghosts.push_table): the sweep, its NORM variant and the
+    fused prolongation sweep leave every cell of every grown box -- valid and
+    ghost -- exactly as the same kernel followed by fill_boundary(width 2)."""
+    from paper_2009_12009_b200.ghosts import push_table
+
+    dom, ba, dm, tr, p3, a, rhs, g, gr = _setup(rng, n, m, periodic=per)
+    fixed = None if per else dom
+    cba = A.coarsened_layout(ba, 2)
+    cdom = dom.coarsen(2)
+    c = A.MultiFab(cba, dm, 1, 1)
+    c.load_valid_from(cdom, rng.normal(size=(1,) + tuple(cdom.extents())))
+    A.fill_boundary(c, tr, cdom, p3)
+    runs = [("sweep", lambda b, t: S.gsrb_sweep(a, b, rhs, DH, fixed=fixed, push=t)),
+            ("norm", lambda b, t: S.gsrb_sweep_norm(a, b, rhs, DH, torch.zeros(1, dtype=torch.int64, device="cuda"),
+                                                    fixed=fixed, push=t))]
+    if per:
+        runs.append(("prolong", lambda b, t: S.gsrb_sweep_prolong(a, b, rhs, DH, c, push=t)))
+    for name, fn in runs:
+        b1 = A.MultiFab(ba, dm, 1, 2)
+        b2 = A.MultiFab(ba, dm, 1, 2)
+        fn(b1, None)
+        A.fill_boundary(b1, tr, dom, p3, ngrow=2)
+        tab = push_table(b2, dom, p3, 2)
+        assert tab is not None and not tab.remote
+        fn(b2, tab)
+        torch.cuda.synchronize()
+        for i in b1.fabs:
+            assert torch.equal(b1.fab(i).data, b2.fab(i).data), (name, i)
+
+
+def test_push_table_rejects_irregular_layout():
+    from paper_2009_12009_b200.ghosts import push_table
+
+    ba = A.BoxArray([A.Box((0, 0, 0), (63, 63, 31)), A.Box((0, 0, 32), (31, 63, 63)), A.Box((32, 0, 32), (63, 63, 63))])
+    dm = A.DistributionMapping.single_rank(len(ba))
+    f = A.MultiFab(ba, dm, 1, 2)
+    assert push_table(f, A.Box((0, 0, 0), (63, 63, 63)), True, 2) is None

@@ -20,7 +20,7 @@ from paper_2009_12009_b200 import stencil as S  # noqa: E402
 from paper_2009_12009_b200._native import option  # noqa: E402
 
 PEAK = 6552.0
-CONFIGS = [int(x) for x in os.environ.get("MB_CONFIGS", "0,1,2,3,4").split(",")]
+CONFIGS = [int(x) for x in os.environ.get("MB_CONFIGS", "0,1,2,4").split(",")]
 
 
 def timeit(fn, reps):
@@ -72,12 +72,15 @@ def case(shape, m, reps, rows):
     cba = A.coarsened_layout(ba, 2)
     c = A.MultiFab(cba, dm, 1, 1)
     A.fill_boundary(c, tr, dom.coarsen(2), True)
-    ops = [("sweep", 1, 0, lambda: S.gsrb_sweep(a, b, rhs, dh)),
-           ("sweep_prolong", 1, 0, lambda: S.gsrb_sweep_prolong(a, b, rhs, dh, c))]
+    from paper_2009_12009_b200.ghosts import push_table
+
+    tab = push_table(b, dom, True, 2)
+    ops = [("sweep", 1, 0, lambda: S.gsrb_sweep(a, b, rhs, dh))]
     for cfg in CONFIGS:
         ops += [("sweep", 0, cfg, lambda: S.gsrb_sweep(a, b, rhs, dh)),
-                ("sweep_norm", 0, cfg, lambda: S.gsrb_sweep_norm(a, b, rhs, dh, nrm)),
-                ("sweep_prolong", 0, cfg, lambda: S.gsrb_sweep_prolong(a, b, rhs, dh, c))]
+                ("sweep+push", 0, cfg, lambda: S.gsrb_sweep(a, b, rhs, dh, push=tab)),
+                ("sweep_norm+push", 0, cfg, lambda: S.gsrb_sweep_norm(a, b, rhs, dh, nrm, push=tab)),
+                ("sweep_prolong+push", 0, cfg, lambda: S.gsrb_sweep_prolong(a, b, rhs, dh, c, push=tab))]
     for name, kern, cfg, fn in ops:
         try:
             with option("sweep_kernel", kern), option("stream_config", cfg):
@@ -97,7 +100,10 @@ def main():
     args = ap.parse_args()
     torch.cuda.set_device(0)
     rows = []
-    for shape, m in (((256, 256, 256), 256), ((128, 128, 128), 128), ((256, 256, 256), 64), ((512, 512, 512), 512)):
+    cases = os.environ.get("MB_CASES", "256/256,128/128,256/64,512/512,512/32")
+    for c in cases.split(","):
+        n, m = (int(x) for x in c.split("/"))
+        shape = (n, n, n)
         case(shape, m, args.reps, rows)
 
 
