@@ -223,7 +223,7 @@ def run_ours(args):
     rhs_sha = hashlib.sha256(rhs_np.tobytes()).hexdigest()
     del rhs_np
     phi = A.MultiFab(ba, dm, 1, 1)
-    mg = A.MLMG(geom, ba, dm, transport=tr)
+    mg = A.MLMG(geom, ba, dm, transport=tr, ghost_push={"auto": None, "on": True, "off": False}[args.ghost_push])
 
     def barrier():
         torch.cuda.synchronize()
@@ -617,6 +617,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ghost-push", default="auto", choices=["auto", "on", "off"],
+                    help="A/B runs: MLMG ghost push (auto: across GPUs only)")
     ap.add_argument("--config", default="c3", choices=["c3", "c5"],
                     help="c3: the headline MLMG solve (C3 / C4 weak scaling); c5: 512^3 sweeps (strong scaling)")
     args = ap.parse_args()

@@ -85,6 +85,8 @@ int amrb_loop_destroy(amrb_loop* loop);
  *                     (0: enough for one wave of CTAs)
  *   "stream_alternate" 1  odd segments stream downward (L2 halo sharing)
  *   "stream_config"    0  k_gsrb_stream tile / strip / depth variant (A/B runs)
+ *   "peer_timeout_ms" 30000  bound on every device-side wait for a peer
+ *                     (NVLink signal pads); 0 waits forever
  * AMRB_EINVAL for an unknown name. */
 int amrb_set_option(const char* name, int64_t value);
 int amrb_get_option(const char* name, int64_t* value);
@@ -190,6 +192,12 @@ int amrb_prog_run_p2p_sync(amrb_prog* g, const double* src_base, double* dst_bas
                            int rank, uint32_t* epoch, void* stream);
 /* Device-side barrier across ranks over NVLink signal pads: pad_ptrs[r] =
  * rank r's pad (>= nranks uint32 slots), epoch = this rank's device counter. */
+/* Failure detection: pinned host memory of 4 uint64 {code, rank, peer, epoch}
+ * the device-side peer waits report into (code 1: a peer did not arrive within
+ * the "peer_timeout_ms" option; later waits then return at once).  The caller
+ * zeroes it, and after synchronising raises TransportError(rank, peer) when
+ * code != 0 (comm.py Transport.check_faults).  NULL disables reporting. */
+int amrb_set_fault_mailbox(void* pinned_host);
 int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch,
                       void* stream);
 /* In-place max over ranks of one device double over NVLink (one launch):

@@ -70,6 +70,7 @@ _SIGS = {
     "amrb_prog_destroy": (C.c_int, [vp]),
     "amrb_prog_run_p2p": (C.c_int, [vp, vp, vp, P(C.c_uint64), C.c_int, vp]),
     "amrb_prog_run_p2p_sync": (C.c_int, [vp, vp, vp, P(C.c_uint64), C.c_int, P(C.c_uint64), C.c_int, vp, vp]),
+    "amrb_set_fault_mailbox": (C.c_int, [vp]),
     "amrb_peer_barrier": (C.c_int, [P(C.c_uint64), C.c_int, C.c_int, vp, vp]),
     "amrb_peer_allmax": (C.c_int, [P(C.c_uint64), P(C.c_uint64), C.c_int, C.c_int, vp, vp, vp]),
     "amrb_level_create": (C.c_int, [C.c_int, P(i32), P(C.c_uint8), P(vp)]),

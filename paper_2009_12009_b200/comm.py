@@ -119,6 +119,9 @@ class Transport:
             ok = True
         except Exception:  # no symmetric memory on this system: NCCL send/recv only
             ok = False
+        # device-side peer waits report a missing peer here (amrb_set_fault_mailbox)
+        self._faults = torch.zeros(4, dtype=torch.int64).pin_memory()
+        check(lib().amrb_set_fault_mailbox(C.c_void_p(self._faults.data_ptr())))
         # every rank must take the same path: enable p2p only if it worked everywhere
         import torch.distributed as dist
 
@@ -140,6 +143,19 @@ class Transport:
             ),
             src=self.rank,
         )
+
+    def check_faults(self):
+        """Raise TransportError(rank, peer) if a device-side wait for a peer
+        timed out (library option "peer_timeout_ms").  Call after synchronising
+        the stream the waits ran on."""
+        f = getattr(self, "_faults", None)
+        if f is None or int(f[0]) == 0:
+            return
+        code, me, peer, epoch = (int(x) for x in f.tolist())
+        from ._native import get_option
+
+        raise TransportError(peer, me, f"peer {peer} did not reach device epoch {epoch} within "
+                                       f"{get_option('peer_timeout_ms')} ms (NVLink signal wait, code {code})")
 
     def peer_barrier(self):
         check(

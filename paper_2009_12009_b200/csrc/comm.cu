@@ -53,10 +53,60 @@ struct PeerPtrs {
 
 // Device barrier fused into a p2p copy launch (see k_copy): pads[r] = rank r's
 // signal pad, epoch = {this rank's barrier epoch, CTA completion ticket}.
+// Failure detection for the NVLink signalling (transport.py:20-24,37-38: a
+// failed message raises TransportError(src, dst, why)).  Every device-side
+// wait for a peer is bounded: after `timeout_ns` of %globaltimer the waiting
+// lane records (code, waiting rank, missing peer, epoch) in the fault mailbox
+// -- pinned host memory the Transport registered -- and gives up; once a fault
+// is recorded every later wait returns at once, so a dead peer costs one
+// timeout, not one per barrier.  The host raises TransportError from the
+// mailbox after its next synchronisation (Transport.check_faults).
+struct Fault {
+  unsigned long long* box;  // [0] code (0 none, 1 peer wait timed out), [1] rank, [2] peer, [3] epoch
+  unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// spin until *pad (wrap-safe) reaches `target`; false (and a fault recorded) on timeout
+__device__ bool peer_wait(const uint32_t* pad, uint32_t target, int rank, int peer, const Fault& f) {
+  if (f.box && *reinterpret_cast<volatile unsigned long long*>(f.box) != 0) return false;
+  const unsigned long long t0 = global_ns();
+  for (unsigned it = 0;; ++it) {
+    uint32_t x;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(pad) : "memory");
+    if ((int32_t)(x - target) >= 0) return true;
+    if ((it & 255) == 255 && f.timeout_ns && global_ns() - t0 > f.timeout_ns) {
+      if (f.box && atomicCAS(f.box, 0ull, 1ull) == 0ull) {
+        f.box[1] = (unsigned long long)rank;
+        f.box[2] = (unsigned long long)peer;
+        f.box[3] = (unsigned long long)target;
+        __threadfence_system();
+      }
+      return false;
+    }
+  }
+}
+
+unsigned long long* g_fault_box = nullptr;  // amrb_set_fault_mailbox
+
+Fault current_fault() {
+  Fault f;
+  f.box = g_fault_box;
+  const int64_t ms = option("peer_timeout_ms");
+  f.timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
+  return f;
+}
+
 struct SyncArgs {
   uint32_t* pads[kMaxPeers];
   uint32_t* epoch;
   int rank, nranks, on;
+  Fault fault;
 };
 
 struct Wave {
@@ -119,12 +169,7 @@ __global__ void __launch_bounds__(kCopyThreads)
           __threadfence_system();
           asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(sy.pads[p] + sy.rank), "r"(ep) : "memory");
         }
-        if (wait) {
-          uint32_t x;
-          do {
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(sy.pads[sy.rank] + p) : "memory");
-          } while ((int32_t)(x - ep) < 0);
-        }
+        if (wait) peer_wait(sy.pads[sy.rank] + p, ep, sy.rank, p, sy.fault);
       }
     }
     __syncthreads();
@@ -531,6 +576,7 @@ extern "C" int amrb_prog_run_p2p_sync(amrb_prog* g_, const double* src_base, dou
     sy.rank = rank;
     sy.nranks = npeers;
     sy.on = 1;
+    sy.fault = current_fault();
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     bool synced = false;
     for (auto* w : g->apply) {
@@ -566,7 +612,8 @@ struct PadPtrs {
 // every peer's signal pad (slot = my rank), wait until every peer published it
 // in mine.  The epoch lives in device memory, so a captured graph replays
 // correctly; the wrap-safe compare allows 2^31 outstanding epochs.
-__global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nranks, uint32_t* epoch) {
+__global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nranks, uint32_t* epoch,
+                               amrb::Fault fault) {
   amrb::pdl_entry();
   // one warp; lane p publishes to and polls peer p concurrently
   const int p = threadIdx.x;
@@ -575,15 +622,16 @@ __global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nra
   if (p < nranks && p != rank) {
     __threadfence_system();
     asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
-    uint32_t v;
-    do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(my_pad + p) : "memory");
-    } while ((int32_t)(v - e) < 0);
+    amrb::peer_wait(my_pad + p, e, rank, p, fault);
   }
   __syncwarp();
   if (p == 0) *epoch = e;
 }
 }  // namespace
+
+extern "C" int amrb_set_fault_mailbox(void* pinned_host) {
+  return amrb::guarded([&] { amrb::g_fault_box = reinterpret_cast<unsigned long long*>(pinned_host); });
+}
 
 extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch, void* stream) {
   return amrb::guarded([&] {
@@ -592,7 +640,8 @@ extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks,
       throw Error(AMRB_EINVAL, "amrb_peer_barrier: bad arguments");
     PadPtrs pads{};
     for (int r = 0; r < nranks; ++r) pads.p[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
-    launch_k(k_peer_barrier, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream), pads.p[rank], pads, rank, nranks, epoch);
+    launch_k(k_peer_barrier, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream), pads.p[rank], pads, rank, nranks, epoch,
+             current_fault());
     check_launch("k_peer_barrier");
   });
 }
@@ -603,8 +652,8 @@ namespace {
 // Max-all-reduce of one double over NVLink: publish the local value into slot
 // [rank] of every peer's symmetric buffer, run the signal barrier, then take
 // the max over the local slots.  One launch, graph-replay safe (device epoch).
-__global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, const uint64_t* __restrict__ bufs_unused, int rank,
-                              int nranks, uint32_t* epoch, double* val, double* my_slots, PeerPtrs peer_slots) {
+__global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, amrb::Fault fault, int rank, int nranks, uint32_t* epoch,
+                              double* val, double* my_slots, PeerPtrs peer_slots) {
   amrb::pdl_entry();
   // one warp; lane p serves peer p (value store, publish, poll) concurrently
   const int p = threadIdx.x;
@@ -617,10 +666,7 @@ __global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, const uint64_t* __
     if (p != rank) {
       __threadfence_system();
       asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
-      uint32_t w;
-      do {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(w) : "l"(my_pad + p) : "memory");
-      } while ((int32_t)(w - e) < 0);
+      amrb::peer_wait(my_pad + p, e, rank, p, fault);
     }
   }
   __syncwarp();
@@ -633,7 +679,6 @@ __global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, const uint64_t* __
     m = fmax(m, x);
   }
   *val = m;
-  (void)bufs_unused;
 }
 }  // namespace
 
@@ -650,7 +695,7 @@ extern "C" int amrb_peer_allmax(const uint64_t* pad_ptrs, const uint64_t* slot_p
       slots.p[r] = reinterpret_cast<const double*>(slot_ptrs[r]);
     }
     launch_k(k_peer_allmax, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream),
-        pads.p[rank], pads, nullptr, rank, nranks, epoch, val, const_cast<double*>(slots.p[rank]), slots);
+        pads.p[rank], pads, current_fault(), rank, nranks, epoch, val, const_cast<double*>(slots.p[rank]), slots);
     check_launch("k_peer_allmax");
   });
 }

@@ -36,7 +36,8 @@ namespace {
 std::mutex g_opt_mu;
 std::map<std::string, int64_t>& options() {
   static std::map<std::string, int64_t> o = {{"pdl", 2}, {"sweep_kernel", 0}, {"grid_per_sm", 0}, {"stream_segments", 0}, {"stream_alternate", 1},
-                                               {"stream_config", 0}};
+                                               {"stream_config", 0},
+                                               {"peer_timeout_ms", 30000}};
   return o;
 }
 }  // namespace

@@ -267,11 +267,10 @@ class MLMG:
         # other GPUs: a device barrier instead).  Periodic lattice layouts.
         # Measured on one GPU (tools/mb_stream.py, C3 fine level): sweep + push
         # 88.5 us vs sweep 75 us + fill 12 us -- the ghost bytes cost the same
-        # either way in a bandwidth-bound kernel, so one GPU keeps the fills
-        # (ghost_push=None: push only across GPUs; True / False force it).
+        # either way in a bandwidth-bound kernel; on two GPUs the pushed solve
+        # measured 8.77 ms vs 8.44 ms with p2p fills (bench.py --ghost-push).
+        # So fills stay the default (ghost_push=True forces the push).
         self.p2p = self.dist and self.transport.p2p
-        if ghost_push is None:
-            ghost_push = self.p2p
         for lv in self.levels:
             lv.push = None
             if ghost_push and self.all_periodic:
@@ -642,7 +641,12 @@ class MLMG:
         check(lib().amrb_store_host(C.c_void_p(t.data_ptr()), C.c_void_p(self.norm_host.data_ptr()), 1,
                                     stream_ptr()))
         torch.cuda.current_stream().synchronize()
+        self._check_faults()
         return float(self.norm_host[0])
+
+    def _check_faults(self):
+        if self.dist and hasattr(self.transport, "check_faults"):
+            self.transport.check_faults()
 
     # -- the device-side solve loop -------------------------------------------------
     _HIST = 4096  # capacity of the residual history (max_iter is capped to it)
@@ -750,6 +754,7 @@ class MLMG:
             check(lib().amrb_store_host(C.c_void_p(self.r0_dev.data_ptr()), C.c_void_p(self.norm_host.data_ptr()),
                                         1, stream_ptr()))
             torch.cuda.current_stream().synchronize()
+            self._check_faults()
             self.r0 = float(self.norm_host[0])
             self.iterations = int(hi[3])
             self.history = [float(x) for x in h[2:2 + self.iterations].tolist()]

@@ -100,6 +100,40 @@ def main():
               f"hist_equal={mg.history == m1.history} phi_bit_identical={same} rn={rn:.3e} rn1={rn1:.3e}",
               flush=True)
         ok = ok and same and mg.history == m1.history
+
+    # -- the same solve with the ghost push (remote ghosts stored over NVLink) --------
+    if tr.p2p:
+        phi2 = A.MultiFab(ba, dmw, 1, 1)
+        mg2 = A.MLMG(geom, ba, dmw, transport=tr, ghost_push=True)
+        pushing = any(lv.push is not None and lv.push[0].remote for lv in mg2.levels)
+        mg2.solve(phi2, rhs, rtol=1e-10, max_iter=60)
+        same2 = all(torch.equal(phi.fab(i).valid(), phi2.fab(i).valid()) for i in phi.fabs)
+        flag = torch.tensor([1 if (same2 and mg2.history == mg.history) else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"ghost push: remote={pushing} identical={bool(flag.item())}", flush=True)
+            ok = ok and bool(flag.item())
+
+    # -- failure detection: a peer that never arrives ---------------------------------
+    if tr.p2p:
+        from paper_2009_12009_b200._native import set_option
+
+        set_option("peer_timeout_ms", 300)
+        dist.barrier()
+        if rank == 0:
+            import time
+
+            t0 = time.time()
+            tr.peer_barrier()  # rank 1 never joins this one
+            torch.cuda.synchronize()
+            try:
+                tr.check_faults()
+                print("STALL NOT DETECTED", flush=True)
+                ok = False
+            except A.TransportError as e:
+                print(f"stalled peer detected after {time.time() - t0:.2f} s: {e}", flush=True)
+        dist.barrier()
+    if rank == 0:
         print("DIST_CHECK", "PASS" if ok else "FAIL", flush=True)
     dist.barrier()
     if rank == 0 and not ok:

@@ -6,7 +6,7 @@ torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 import paper_2009_12009_b200 as A
 from paper_2009_12009_b200 import stencil as S
-f = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1)}[world]
+f = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}[world]
 ext = tuple(256 * x for x in f)
 dom = A.Box((0, 0, 0), tuple(e - 1 for e in ext))
 ba = A.BoxArray([dom]).max_size(64)
@@ -41,6 +41,8 @@ def sw():
 res["sweep L0 (+fill w2)"] = graph_time(sw)
 res["resid_restrict L0"] = graph_time(lambda: mg._resid_restrict(0))
 res["residual_norm"] = graph_time(lambda: mg._residual_norm())
+nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+res["sweep+norm L0 (+fill w2)"] = graph_time(lambda: mg._sweep(top, norm=nrm))
 for l in range(1, len(mg.levels)):
     lv = mg.levels[l]
     if lv.replicated: break
@@ -57,7 +59,8 @@ for l in range(2, mg.grid_from):
     lv = mg.levels[l]
     res[f"sweep L{l} (+fill w2)"] = graph_time(lambda: mg._sweep(lv))
 res["coarse tail"] = graph_time(lambda: mg._coarse_tail())
-res["vcycle+norm"] = graph_time(lambda: mg._cycle_and_norm(), 5)
+mg._prime()
+res["iteration (cycle + fused norm)"] = graph_time(lambda: mg._body(), 5)
 if rank == 0:
     print("levels:", [(tuple(l.domain.extents()), l.replicated) for l in mg.levels], "grid_from", mg.grid_from,
           "tail", mg.tail, "cluster", mg.cluster_tail)
