@@ -73,6 +73,11 @@ int amrb_loop_end(amrb_loop* loop);
 int amrb_loop_launch(amrb_loop* loop, void* stream);
 int amrb_loop_destroy(amrb_loop* loop);
 
+/* Checked builds (make CHECKED=1 -> libamrb_checked.so): number of failed
+ * device-side invariant checks since the last reset and the source line of
+ * the first; *failures = -1 in the normal build. */
+int amrb_debug_checks(int64_t* failures, int64_t* line, int reset);
+
 /* Library options: process-wide, set explicitly by the caller (the library
  * reads no environment variables).  Names and defaults:
  *   "pdl"          2  programmatic dependent launch: 0 off, 1 always, 2 eager

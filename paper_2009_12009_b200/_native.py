@@ -16,7 +16,10 @@ import numpy as np
 __all__ = ["lib", "check", "LIB_PATH", "AmrbError", "ptr", "i32p", "i64p", "u8p", "f64p", "get_option", "set_option",
            "option"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libamrb.so")
+# AMRB_LIBRARY=checked selects the checked build (device invariant checks,
+# make -C csrc CHECKED=1) for test runs; the default is the production library
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                        "libamrb_checked.so" if os.environ.get("AMRB_LIBRARY") == "checked" else "libamrb.so")
 
 AMRB_OK, AMRB_EINVAL, AMRB_ECUDA, AMRB_ENCCL, AMRB_ENOMEM, AMRB_ENOTSUP = 0, -1, -2, -3, -4, -5
 FABTAB_W = 8
@@ -42,6 +45,7 @@ _SIGS = {
     "amrb_loop_end": (C.c_int, [vp]),
     "amrb_loop_launch": (C.c_int, [vp, vp]),
     "amrb_loop_destroy": (C.c_int, [vp]),
+    "amrb_debug_checks": (C.c_int, [P(i64), P(i64), C.c_int]),
     "amrb_set_option": (C.c_int, [C.c_char_p, i64]),
     "amrb_get_option": (C.c_int, [C.c_char_p, P(i64)]),
     "amrb_zero": (C.c_int, [vp, i64, vp]),
@@ -206,3 +210,11 @@ class option:
 
     def __exit__(self, *exc):
         set_option(self.name, self.old)
+
+
+def debug_checks(reset=True):
+    """(failures, first failing source line) of the checked build's device
+    invariant checks; failures = -1 in the production build."""
+    f, ln = i64(0), i64(0)
+    check(lib().amrb_debug_checks(C.byref(f), C.byref(ln), 1 if reset else 0))
+    return int(f.value), int(ln.value)

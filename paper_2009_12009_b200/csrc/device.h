@@ -69,6 +69,22 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Checked builds (make CHECKED=1 -> _lib/libamrb_checked.so): device-side
+// invariant checks in the concurrency-heavy kernels.  A failed check counts
+// into a device word and records its line (amrb_debug_checks reads them);
+// compute-sanitizer is closed on this GPU pool, so these are the sanitizer.
+#ifndef AMRB_CHECKED
+#define AMRB_CHECKED 0
+#endif
+// `box` = unsigned int[2] in device memory: {failures, first failing line}
+#define AMRB_DCHECK_AT(box, cond)                                   \
+  do {                                                              \
+    if (AMRB_CHECKED && !(cond) && (box)) {                         \
+      if (atomicAdd((box), 1u) == 0u) (box)[1] = (unsigned)__LINE__; \
+    }                                                               \
+  } while (0)
+unsigned int* debug_check_words();  // device words of the checked build (gsrb_stream.cu)
+
 // Valid box of one grid, 3-D padded, global index space.
 struct BoxGeom {
   int lo[3];

@@ -124,6 +124,8 @@ struct StreamArgs {
   const BoxGeom* geo;
   const FabView* fb;  // output views
   double* b;
+  int64_t b_elems;  // size of the output allocation (checked builds)
+  unsigned int* dcheck;  // checked builds: {failures, line}
   const int* slot;  // per box: block index in the tensor maps
   Coef cf;
   int a_kc, a_jc, a_ic;  // tensor coordinate of phi cell (i, j0-2, k0-2) = (i + a_ic, j0 + a_jc, k0 + a_kc)
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     k_gsrb_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ StreamArgs args) {
   pdl_entry();
+#define AMRB_DCHECK(cond) AMRB_DCHECK_AT(args.dcheck, cond)
   using LY = StreamLayout<TJ, TK, D, MODE>;
   constexpr int WK = LY::WK, LK = LY::LK, RPW = LY::RPW, NS = LY::NS, PK = LY::PK, CK = LY::CK;
   constexpr int NSW = TJ / (RW * RPW) * WK;  // strip warps (then WK ring warps)
@@ -190,6 +193,8 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
   const int L = i1 - i0;
   const int istart = dir > 0 ? i0 : i1 - 1;  // box-local plane of stream position 0
   const BoxGeom g = args.geo[box];
+  AMRB_DCHECK(0 <= i0 && i0 < i1 && i1 <= g.n[0] && (dir == 1 || dir == -1));
+  AMRB_DCHECK(0 <= j0 && j0 + TJ <= g.n[1] && 0 <= k0 && k0 + TK <= g.n[2]);
   const int bslot = args.slot[box];
   const int gj0 = g.lo[1] + j0, gk0 = g.lo[2] + k0;
   const int cshift = ((k0 >> 1) + args.c_kc) & 1;
@@ -199,8 +204,12 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
   auto phi_s = [&](int q) { return reinterpret_cast<double*>(slot_base(q)); };
   auto rhs_s = [&](int q) { return reinterpret_cast<const double*>(slot_base(q + 1) + LY::ROFF); };  // rides with phi q+1
   auto crs_s = [&](int q) { return reinterpret_cast<const double*>(slot_base(q) + LY::COFF); };
-  auto wait_pos = [&](int q) { mbar_wait(&bars[(q + 2) % NS], (unsigned)(((q + 2) / NS) & 1)); };
+  auto wait_pos = [&](int q) {
+    AMRB_DCHECK(q >= -2 && q <= L + 1);
+    mbar_wait(&bars[(q + 2) % NS], (unsigned)(((q + 2) / NS) & 1));
+  };
   auto issue = [&](int q) {  // phi position q, rhs position q-1 (from q = 0), coarse parent plane
+    AMRB_DCHECK(q >= -2 && q <= L + 1);
     uint64_t* bar = &bars[(q + 2) % NS];
     const bool wr = q >= 0;
     mbar_expect_tx(bar, LY::PB + (wr ? LY::RB : 0) + (PROL ? LY::CB : 0));
@@ -249,6 +258,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     const FabView B = args.fb[box];
     out = args.b + B.off + (int64_t)istart * B.s0 + (int64_t)(j0 + r0 - 2) * B.s1 + (k0 + 2 * m);
     ostep = dir * B.s0;
+    AMRB_DCHECK(r0 >= 2 && r0 + RW <= TJ + 2 && c0 >= 2 && c0 + 1 <= TK + 1);
   }
   const int64_t orow = strip ? args.fb[box].s1 : 0;
   bool pushed = false;
@@ -421,8 +431,11 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
         a0[x][b] = relax(c, rs[x], lapi(c, am[x], xp, ym, yp, zm, zp), cf.rgamma);
       }
 #pragma unroll
-      for (int x = 0; x < RW; ++x)
+      for (int x = 0; x < RW; ++x) {
+        AMRB_DCHECK(out + x * orow >= args.b && out + x * orow + 2 <= args.b + args.b_elems &&
+                    ((reinterpret_cast<uintptr_t>(out + x * orow) & 15) == 0));
         *reinterpret_cast<double2*>(out + x * orow) = make_double2(a0[x][0], a0[x][1]);
+      }
       out += ostep;
       if (PUSH) push_plane(plane(p));
     }
@@ -481,6 +494,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       const int cc = side ? TK + 2 : 1;
       const int rr = 1 + 2 * idx + (side ? 1 - PHI : PHI);
       rco = rr * PK + cc;
+      AMRB_DCHECK(rr >= 1 && rr <= TJ + 2 && rco - PK >= 0 && rco + PK < LY::PJ * PK);
       const double c = S1[rco];
       rc = relax(c, R1[rco - PK], lapi(c, S0[rco], S2[rco], S1[rco - PK], S1[rco + PK], S1[rco - 1], S1[rco + 1]),
                  cf.rgamma);
@@ -531,6 +545,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       run(std::false_type{}, ring_step);
   }
 
+#undef AMRB_DCHECK
   if (PUSH && pushed) __threadfence_system();  // pushes to peers before the consumer's device barrier
   if (NORM) {
     for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
@@ -630,7 +645,19 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
   args.geo = lv.dgeo.p;
   args.fb = b.dev.p;
   args.b = b_base;
+  {
+    int64_t hi = 0;  // one past the last element any resident box of b touches
+    for (int bx = 0; bx < lv.nboxes; ++bx)
+      if (lv.resident[bx]) {
+        const FabView& v = b.host[bx];
+        const BoxGeom& gg = lv.geo[bx];
+        hi = std::max<int64_t>(hi, v.off + (int64_t)(gg.n[0] + b.ng3[0]) * v.s0 + (int64_t)(gg.n[1] + b.ng3[1]) * v.s1 +
+                                       gg.n[2] + b.ng3[2] + 1);
+      }
+    args.b_elems = hi;
+  }
   args.slot = lv.dslot.p;
+  args.dcheck = AMRB_CHECKED ? debug_check_words() : nullptr;
   args.cf = cf;
   for (int x = 0; x < 3; ++x) {
     args.flo[x] = flo[x];
@@ -644,6 +671,16 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
 }
 
 }  // namespace
+
+unsigned int* debug_check_words() {
+  static unsigned int* words = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    AMRB_CUDA(cudaMalloc(&words, 2 * sizeof(unsigned int)));
+    AMRB_CUDA(cudaMemset(words, 0, 2 * sizeof(unsigned int)));
+  });
+  return words;
+}
 
 // mode 0: plain, 1: PROL (clv/c/c_base), 2: NORM (norm)
 bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
@@ -698,3 +735,14 @@ bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_ba
 }
 
 }  // namespace amrb
+
+extern "C" int amrb_debug_checks(int64_t* failures, int64_t* line, int reset) {
+  return amrb::guarded([&] {
+    if (!failures || !line) throw amrb::Error(AMRB_EINVAL, "amrb_debug_checks: null argument");
+    unsigned int w[2] = {0, 0};
+    if (AMRB_CHECKED) AMRB_CUDA(cudaMemcpy(w, amrb::debug_check_words(), sizeof w, cudaMemcpyDeviceToHost));
+    *failures = AMRB_CHECKED ? (int64_t)w[0] : -1;
+    *line = (int64_t)w[1];
+    if (AMRB_CHECKED && reset) AMRB_CUDA(cudaMemset(amrb::debug_check_words(), 0, sizeof w));
+  });
+}

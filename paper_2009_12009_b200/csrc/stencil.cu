@@ -25,6 +25,7 @@ namespace amrb {
 namespace {
 thread_local std::string g_last_error;
 }
+
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 namespace {
