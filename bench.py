@@ -384,6 +384,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample()
+    others = None
+    if world == 1 and not args.no_other_configs:
+        others = {"c1": c1_micro(), "c5": c5_micro()}
 
     if rank == 0:
         line = {
@@ -422,9 +425,128 @@ def run_ours(args):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if others is not None:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier(device_ids=[local])
+
+
+def _graph_us(fn, reps=10):
+    """us per call of fn, `reps` calls captured in one CUDA graph (warm)."""
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / reps)
+    return float(np.median(ts))
+
+
+def c1_micro():
+    """Config C1: periodic 64^3 in 8 boxes of 32^3, one ghost
+    layer; FillBoundary + 7-point Laplacian on the device (graph-timed), and the
+    same step in the numpy oracle on the host (the reference's fill_boundary
+    measured 2.35 ms)."""
+    import torch
+
+    import paper_2009_12009_b200 as A
+    from oracle import mesh_ref as M
+    from oracle import mlmg_ref as R
+    from paper_2009_12009_b200 import stencil as S
+
+    n, m = 64, 32
+    dom = A.Box((0, 0, 0), (n - 1,) * 3)
+    ba = A.BoxArray([dom]).max_size(m)
+    dm = A.DistributionMapping.single_rank(len(ba))
+    tr = A.Transport(1)
+    g = np.random.default_rng(0).standard_normal((1, n, n, n))
+    phi = A.MultiFab(ba, dm, 1, 1)
+    phi.setval(-7777.0)
+    phi.load_valid_from(dom, g)
+    out = A.MultiFab(ba, dm, 1, 0)
+    dh = (float(n * n),) * 3
+    fill_us = _graph_us(lambda: A.fill_boundary(phi, tr, dom, True))
+    lap_us = _graph_us(lambda: S.laplacian(out, phi, dh))
+    step_us = _graph_us(lambda: (A.fill_boundary(phi, tr, dom, True), S.laplacian(out, phi, dh)))
+    boxes = [(tuple(b.lo), tuple(b.hi)) for b in ba]
+    d = ((0, 0, 0), (n - 1,) * 3)
+    fabs = M.make_fabs(boxes, 1, 1, -7777.0)
+    M.load_global(boxes, fabs, 1, d, g)
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        M.fill_boundary(boxes, fabs, 1, d, (True,) * 3)
+        for i in fabs:
+            R.laplacian(fabs[i][0], dh)
+    cpu_ms = 1e3 * (time.perf_counter() - t0) / reps
+    return {"workload": "C1 periodic 64^3, 8 boxes of 32^3, 1 ghost: FillBoundary + Laplacian",
+            "fill_us": round(fill_us, 2), "laplacian_us": round(lap_us, 2), "step_us": round(step_us, 2),
+            "cpu_oracle_step_ms": round(cpu_ms, 3), "cpu_oracle": "numpy restatement, 1 thread",
+            "timing": "CUDA graph of 10 steps, warm"}
+
+
+def c5_micro(ghost_push="auto"):
+    """Config C5 microtimings (1 GPU): 512^3 in 4,096 boxes of 32^3 -- the
+    copy-program FillBoundary at width 1 and 2, the streaming sweep alone and
+    with its ghost push, and the bench's C5 step (10 sweeps + Laplacian)."""
+    import torch
+
+    import paper_2009_12009_b200 as A
+    from paper_2009_12009_b200 import stencil as S
+    from paper_2009_12009_b200.ghosts import push_table
+
+    n, m = 512, 32
+    dom = A.Box((0, 0, 0), (n - 1,) * 3)
+    ba = A.BoxArray([dom]).max_size(m)
+    dm = A.DistributionMapping.single_rank(len(ba))
+    tr = A.Transport(1)
+    a, b = A.MultiFab(ba, dm, 1, 2), A.MultiFab(ba, dm, 1, 2)
+    rhs, lap = A.MultiFab(ba, dm, 1, 1), A.MultiFab(ba, dm, 1, 0)
+    rng = np.random.default_rng(4)
+    a.load_valid_from(dom, rng.standard_normal((n, n, n)))
+    rhs.load_valid_from(dom, rng.standard_normal((n, n, n)))
+    A.fill_boundary(rhs, tr, dom, True)
+    A.fill_boundary(a, tr, dom, True)
+    dh = (float(n * n),) * 3
+    tab = push_table(b, dom, True, 2)
+    tab_a = push_table(a, dom, True, 2)
+    res = {"workload": "C5 512^3, 4096 boxes of 32^3, periodic (1 GPU)",
+           "fill_w1_us": round(_graph_us(lambda: A.fill_boundary(a, tr, dom, True, ngrow=1)), 1),
+           "fill_w2_us": round(_graph_us(lambda: A.fill_boundary(a, tr, dom, True, ngrow=2)), 1),
+           "sweep_us": round(_graph_us(lambda: S.gsrb_sweep(a, b, rhs, dh)), 1),
+           "sweep_with_ghost_push_us": round(_graph_us(lambda: S.gsrb_sweep(a, b, rhs, dh, push=tab)), 1)}
+    fields = [a, b]
+    tabs = {id(a): tab_a, id(b): tab}
+
+    def step():
+        for _ in range(10):
+            S.gsrb_sweep(fields[0], fields[1], rhs, dh, push=tabs[id(fields[1])])
+            fields.reverse()
+        S.laplacian(lap, fields[0], dh)
+
+    res["step_ms"] = round(_graph_us(step, reps=2) / 1e3, 3)
+    res["step"] = "10 x fused sweep (FillBoundary pushed by the sweep) + Laplacian, graph"
+    res["cell_updates_per_s"] = 10 * n ** 3 / (res["step_ms"] * 1e-3)
+    del a, b, rhs, lap
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_c5(args):
@@ -454,23 +576,38 @@ def run_c5(args):
     b = A.MultiFab(ba, dm, 1, 2, symmetric=sym)
     rhs = A.MultiFab(ba, dm, 1, 1, symmetric=sym)
     lap = A.MultiFab(ba, dm, 1, 0)
-    gen = torch.Generator(device="cuda")
-    for i, f in rhs.fabs.items():
-        gen.manual_seed(1000003 * 4 + i)
-        f.valid().copy_(torch.randn(tuple(f.valid().shape), generator=gen, device="cuda", dtype=torch.float64))
-        gen.manual_seed(2000003 * 4 + i)
-        a.fab(i).valid().copy_(torch.randn(tuple(f.valid().shape), generator=gen, device="cuda", dtype=torch.float64))
+    # phi then rhs, standard normals from np.random.default_rng(4)
+    rng = np.random.default_rng(4)
+    a.load_valid_from(dom, rng.standard_normal((n, n, n)))
+    rhs.load_valid_from(dom, rng.standard_normal((n, n, n)))
     A.fill_boundary(rhs, tr, dom, True)
     dh = (float(n * n),) * 3
     fields = [a, b]
+    # FillBoundary fused into the sweep (ghosts.push_table): each sweep also
+    # writes its output's width-2 ghosts -- on other GPUs through NVLink, then a
+    # device barrier -- instead of a copy-program fill before the next sweep
+    # (tools/mb_stream.py, C5 layout: sweep + push 1019 us vs fill + sweep
+    # ~1.3 ms); the width-1 fill before the Laplacian is covered as well
+    from paper_2009_12009_b200.ghosts import push_table
+
+    tabs = {id(f): push_table(f, dom, True, 2) for f in (a, b)}
+    use_push = args.ghost_push != "off" and all(t is not None for t in tabs.values())
 
     def step():
         for _ in range(10):
-            A.fill_boundary(fields[0], tr, dom, True, ngrow=2)
-            S.gsrb_sweep(fields[0], fields[1], rhs, dh)
+            if use_push:
+                S.gsrb_sweep(fields[0], fields[1], rhs, dh, push=tabs[id(fields[1])])
+                if world > 1:
+                    tr.peer_barrier()  # peers' pushes into our ghosts have landed
+            else:
+                A.fill_boundary(fields[0], tr, dom, True, ngrow=2)
+                S.gsrb_sweep(fields[0], fields[1], rhs, dh)
             fields.reverse()
-        A.fill_boundary(fields[0], tr, dom, True, ngrow=1)
+        if not use_push:
+            A.fill_boundary(fields[0], tr, dom, True, ngrow=1)
         S.laplacian(lap, fields[0], dh)
+
+    A.fill_boundary(a, tr, dom, True, ngrow=2)  # the first sweep's input
 
     def barrier():
         torch.cuda.synchronize()
@@ -525,6 +662,8 @@ def run_c5(args):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         a.from_host_image(host_in)
+        if use_push:  # the uploaded phi's ghosts (the graph's sweeps keep them current after this)
+            A.fill_boundary(a, tr, dom, True, ngrow=2)
         fields[:] = [a, b]
         g.replay()
         a.to_host_image(host_out)
@@ -558,6 +697,8 @@ def run_c5(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C5 512^3, 4096 boxes of 32^3, periodic: 10 x (fill w2 + fused GSRB sweep) + "
                                    "fill w1 + Laplacian per step (one CUDA graph)", "domain": [n] * 3, "box": m,
+                       "fill": ("fused into the sweep (ghost push" + (", NVLink + device barrier" if world > 1 else "")
+                                + ")") if use_push else "copy-program FillBoundary",
                        "boxes": len(ba), "global_batch": 1, "seq_len": ncells,
                        "parallelism": f"dp{world} (boxes by Morton SFC, same problem on every GPU count)",
                        "l2": "working set 5+ GB exceeds the 126 MB L2"},
@@ -617,6 +758,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the C1 / C5 microtimings of the C3 line")
     ap.add_argument("--ghost-push", default="auto", choices=["auto", "on", "off"],
                     help="A/B runs: MLMG ghost push (auto: across GPUs only)")
     ap.add_argument("--config", default="c3", choices=["c3", "c5"],

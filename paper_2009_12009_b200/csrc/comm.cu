@@ -126,15 +126,25 @@ struct Wave {
 constexpr int kSmall = kChunk / 4;
 constexpr int kPackMax = 256;
 
-__device__ __forceinline__ void rec_cell(const DevRec& r, int64_t loc, int64_t cells, int64_t& so, int64_t& dofs) {
-  const int c = (int)(loc / cells);
-  int t = (int)(loc - (int64_t)c * cells);
-  const int k = t % r.e2;
-  t /= r.e2;
-  const int j = t % r.e1;
-  const int i = t / r.e1;
-  so = r.src + c * r.scs + i * r.ss0 + j * r.ss1 + k;
-  dofs = r.dst + c * r.dcs + i * r.ds0 + j * r.ds1 + k;
+// (comp, i, j, k) of flat index loc of a record, as source / destination
+// element offsets.  A record holds < 2^31 cells per component, so after the
+// component split the index arithmetic is unsigned 32-bit (the 64-bit
+// division runs only for multi-component records).
+__device__ __forceinline__ void rec_cell(const DevRec& r, int64_t loc, int64_t cells, int ncomp, int64_t& so,
+                                         int64_t& dofs) {
+  int c = 0;
+  unsigned t = (unsigned)loc;
+  if (ncomp > 1) {
+    c = (int)(loc / cells);
+    t = (unsigned)(loc - (int64_t)c * cells);
+  }
+  const unsigned e2 = (unsigned)r.e2, e1 = (unsigned)r.e1;
+  const unsigned row = t / e2;
+  const unsigned k = t - row * e2;
+  const unsigned i = row / e1;
+  const unsigned j = row - i * e1;
+  so = r.src + c * r.scs + (int64_t)i * r.ss0 + (int64_t)j * r.ss1 + k;
+  dofs = r.dst + c * r.dcs + (int64_t)i * r.ds0 + (int64_t)j * r.ds1 + k;
 }
 
 // With sy.on (p2p fills) the launch also is the cross-rank barrier that used to
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(kCopyThreads)
       dofs[u] = -1;
       if (loc < end) {
         int64_t so, dof;
-        rec_cell(r, loc, cells, so, dof);
+        rec_cell(r, loc, cells, ncomp, so, dof);
         dofs[u] = dof;
         v[u] = s[so];
       }
@@ -220,7 +230,7 @@ __global__ void __launch_bounds__(kCopyThreads)
         const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
         const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
         int64_t so, dof;
-        rec_cell(r, loc - beg[lo], cells, so, dof);
+        rec_cell(r, loc - beg[lo], cells, ncomp, so, dof);
         dofs[u] = dof;
         v[u] = s[so];
       }
