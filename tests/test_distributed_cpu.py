@@ -1,5 +1,5 @@
-"""Host-side logic of the one-process-per-GPU path, exercised with 2 gloo ranks
-on CPU: every rank derives the same plans and the same per-rank layouts, the
+"""Host-side logic of the one-process-per-GPU path, exercised with 2, 4 and 8
+gloo ranks on CPU: every rank derives the same plans and the same per-rank layouts, the
 per-pair message sizes a sender computes equal what the receiver expects,
 re-boxing per rank is consistent, and each rank's resident set is its owned
 boxes.  (Device work is covered by tests/dist_check.py on GPUs.)"""
@@ -22,13 +22,20 @@ def _free_port():
 
 
 def _worker(rank, world, port, out):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2009_12009_b200 as A
     from paper_2009_12009_b200.mlmg import mg_hierarchy, rebox_per_rank
 
-    dom = A.Box((0, 0, 0), (63, 31, 31))
+    # the weak-scaling shapes of C4 (bench.py _domain_for), scaled down
+    ext = {2: (64, 32, 32), 4: (64, 64, 32), 8: (64, 64, 64)}[world]
+    dom = A.Box((0, 0, 0), tuple(e - 1 for e in ext))
     ba = A.BoxArray([dom]).max_size(16)
     dm = A.sfc_distribute(ba, A.default_costs(ba), world)
     plan = A.build_plan_fill_boundary(ba, 2, dom, True)
@@ -56,10 +63,24 @@ def _worker(rank, world, port, out):
     rba, rdm = rebox_per_rank(ba, dm)
     ok &= len(rba) == world and sorted(rdm.owner) == list(range(world))
     ok &= sum(b.num_cells() for b in rba) == dom.num_cells()
+    # every rank box is one SFC octant / slab of the domain
+    split = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}[world]
+    ok &= all(tuple(b.extents()) == tuple(e // f for e, f in zip(ext, split)) for b in rba)
     levels = [(tuple(d.lo), tuple(d.hi), k) for d, _, k in mg_hierarchy(dom, rba, nranks=world)]
     alllv = [None] * world
     dist.all_gather_object(alllv, levels)
     ok &= all(x == alllv[0] for x in alllv)
+    # the same resolutions as the oracle's hierarchy on the user's layout
+    from oracle import mlmg_ref as R
+
+    want = [d for d, _, _ in R.mg_levels(((0, 0, 0), tuple(e - 1 for e in ext)),
+                                          [(tuple(b.lo), tuple(b.hi)) for b in ba])]
+    ok &= [(lo, hi) for lo, hi, _ in levels] == want
+    # the rebox fill plan's remote pairs are the SFC neighbours: a message per ordered pair
+    rplan = A.build_plan_fill_boundary(rba, 2, dom, True).table()
+    pairs = {(rdm[int(r[0])], rdm[int(r[1])]) for r in rplan if rdm[int(r[0])] != rdm[int(r[1])]}
+    expect = {2: 2, 4: 12, 8: 56}[world]
+    ok &= len(pairs) == expect
     # distributed FabArray on CPU storage: resident set = owned boxes (layout only)
     fa = A.FabArray(ba, dm, 1, 1, device="cpu")
     ok &= fa.distributed and set(fa.fabs) == set(dm.owned_indices(rank))
@@ -70,8 +91,8 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_two_rank_host_logic():
-    world = 2
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multi_rank_host_logic(world):
     port = _free_port()
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
@@ -82,4 +103,4 @@ def test_two_rank_host_logic():
     for p in procs:
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
-    assert dict(out) == {0: True, 1: True}
+    assert dict(out) == {r: True for r in range(world)}
