@@ -305,28 +305,24 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       }
     }
   };
-  // PROL: every cell of plane q's tile += its coarse parent (the single addition
-  // of k_prolong), pairs spread over all threads; a barrier must follow before
-  // anyone reads the plane
-  auto correct_plane = [&](int q) {
-    double* S = phi_s(q);
-    const double* Cq = crs_s(q);
-    constexpr int PP = (TK + 4) / 2, NP = (TJ + 4) * PP, NT = 32 * stream_warps<TJ, TK, RW>();
-    for (int e = tid; e < NP; e += NT) {
-      const int rr = e / PP, pc = e - rr * PP;
-      const double2 v = lds2(S + rr * PK + 2 * pc);
-      const double cp = Cq[(rr >> 1) * CK + pc + cshift];
-      sts2(S + rr * PK + 2 * pc, v.x + cp, v.y + cp);
-    }
+  // PROL: a plane tile holds the fine values BEFORE the prolongation; every
+  // read of a not-yet-relaxed value adds its coarse parent on the fly (the
+  // single addition of k_prolong, so the bits equal prolong-then-sweep).
+  // Relaxed values written back to shared memory already include it.
+  auto parent = [&](int q, int off) {  // smem offset off = r * PK + c of plane position q
+    const int r = off / PK, c = off - r * PK;
+    return crs_s(q)[(r >> 1) * CK + (c >> 1) + cshift];
   };
+  auto old = [&](const double* S, int q, int off) { return PROL ? S[off] + parent(q, off) : S[off]; };
   // arrival of plane position q: own pairs to registers
   auto arrive_strip = [&](int q, double (&dst)[RW][2]) {
     const double* S = phi_s(q);
 #pragma unroll
     for (int x = 0; x < RW; ++x) {
       const double2 v = lds2(S + (r0 + x) * PK + c0);
-      dst[x][0] = v.x;
-      dst[x][1] = v.y;
+      const double cp = PROL ? parent(q, (r0 + x) * PK + c0) : 0.0;  // one parent per pair
+      dst[x][0] = PROL ? v.x + cp : v.x;
+      dst[x][1] = PROL ? v.y + cp : v.y;
     }
   };
   auto arrive_ring = [&](int q, double (&dst)[2][2]) {
@@ -334,19 +330,15 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const double2 v = lds2(S + (h ? TJ + 2 : 1) * PK + c0);
-      dst[h][0] = v.x;
-      dst[h][1] = v.y;
+      const double cp = PROL ? parent(q, (h ? TJ + 2 : 1) * PK + c0) : 0.0;
+      dst[h][0] = PROL ? v.x + cp : v.x;
+      dst[h][1] = PROL ? v.y + cp : v.y;
     }
   };
 
   // prologue: positions -2, -1
   wait_pos(-2);
   wait_pos(-1);
-  if (PROL) {
-    correct_plane(-2);
-    correct_plane(-1);
-    __syncthreads();
-  }
   if (strip) {
     arrive_strip(-2, a0);
     arrive_strip(-1, a1);
@@ -375,10 +367,6 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     const double* R1 = rhs_s(p + 1);
     const bool red_on = (p + 1 >= 0 && p + 1 < L) || plane_ok(p + 1);
     double nr[RW], rsn[RW];
-    if (PROL) {
-      correct_plane(p + 2);
-      __syncthreads();
-    }
     arrive_strip(p + 2, a2);
     // ---- phase A: red(p+1) in column (r, c0 + b); NORM: residual of plane p+1
 #pragma unroll
@@ -386,9 +374,9 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       const int b = (PHI + x) & 1;  // compile-time after unrolling
       const int row = (r0 + x) * PK;
       const double c = a1[x][b];
-      const double ym = x > 0 ? a1[x > 0 ? x - 1 : 0][b] : S1[row - PK + c0 + b];
-      const double yp = x < RW - 1 ? a1[x < RW - 1 ? x + 1 : 0][b] : S1[row + PK + c0 + b];
-      const double kn = b ? S1[row + c0 + 2] : S1[row + c0 - 1];  // the neighbour pair's cell
+      const double ym = x > 0 ? a1[x > 0 ? x - 1 : 0][b] : old(S1, p + 1, row - PK + c0 + b);
+      const double yp = x < RW - 1 ? a1[x < RW - 1 ? x + 1 : 0][b] : old(S1, p + 1, row + PK + c0 + b);
+      const double kn = old(S1, p + 1, b ? row + c0 + 2 : row + c0 - 1);  // the neighbour pair's cell
       const double zm = b ? a1[x][0] : kn;
       const double zp = b ? kn : a1[x][1];
       const double2 rr = lds2(R1 + row - PK + c0);
@@ -451,7 +439,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       a1[x][1] = a2[x][1];
       rs[x] = rsn[x];
     }
-    if (PROL || p + 1 + NS <= L + 1) fence_proxy_async();  // our shared stores before a later TMA into the slot
+    if (p + 1 + NS <= L + 1) fence_proxy_async();  // our shared stores before a later TMA into the slot
   };
 
   auto ring_step = [&](auto phi_tag, auto up_tag, int p) {
@@ -469,22 +457,19 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     double rv[2], rc = 0.0;  // ring rows / ring column red(p+1)
     int rco = 0;             // ring column cell offset
     bool rcok = false;
-    if (PROL) {
-      correct_plane(p + 2);
-      __syncthreads();
-    }
     arrive_ring(p + 2, g2);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (RPW > 1 && h != rg) continue;  // narrow tiles: one ring row per row group
       const int b = h ? PHI : 1 - PHI;
       const int row = (h ? TJ + 2 : 1) * PK;
-      const double kn = b ? S1[row + c0 + 2] : S1[row + c0 - 1];
+      const double kn = old(S1, p + 1, b ? row + c0 + 2 : row + c0 - 1);
       const double zm = b ? g1[h][0] : kn;
       const double zp = b ? kn : g1[h][1];
       const double c = g1[h][b];
       const double rb = R1[row - PK + c0 + b];
-      rv[h] = relax(c, rb, lapi(c, g0[h][b], g2[h][b], S1[row - PK + c0 + b], S1[row + PK + c0 + b], zm, zp),
+      rv[h] = relax(c, rb, lapi(c, g0[h][b], g2[h][b], old(S1, p + 1, row - PK + c0 + b), old(S1, p + 1, row + PK + c0 + b),
+                                zm, zp),
                     cf.rgamma);
     }
     if (wk == 0 && lane < TJ + 2) {
@@ -495,8 +480,9 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       const int rr = 1 + 2 * idx + (side ? 1 - PHI : PHI);
       rco = rr * PK + cc;
       AMRB_DCHECK(rr >= 1 && rr <= TJ + 2 && rco - PK >= 0 && rco + PK < LY::PJ * PK);
-      const double c = S1[rco];
-      rc = relax(c, R1[rco - PK], lapi(c, S0[rco], S2[rco], S1[rco - PK], S1[rco + PK], S1[rco - 1], S1[rco + 1]),
+      const double c = old(S1, p + 1, rco);
+      rc = relax(c, R1[rco - PK], lapi(c, old(S0, p, rco), old(S2, p + 2, rco), old(S1, p + 1, rco - PK),
+                                       old(S1, p + 1, rco + PK), old(S1, p + 1, rco - 1), old(S1, p + 1, rco + 1)),
                  cf.rgamma);
       rcok = (side ? rgt_ok : lft_ok) && (rr != 1 || top_ok) && (rr != TJ + 2 || bot_ok);
     }
@@ -514,7 +500,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
       g1[h][0] = g2[h][0];
       g1[h][1] = g2[h][1];
     }
-    if (PROL || p + 1 + NS <= L + 1) fence_proxy_async();
+    if (p + 1 + NS <= L + 1) fence_proxy_async();
   };
 
   // PHI of stream position p: b of strip row 0 = 1 - ((i + j0 + k0) & 1), global

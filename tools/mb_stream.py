@@ -78,6 +78,8 @@ def case(shape, m, reps, rows):
     ops = [("sweep", 1, 0, lambda: S.gsrb_sweep(a, b, rhs, dh))]
     for cfg in CONFIGS:
         ops += [("sweep", 0, cfg, lambda: S.gsrb_sweep(a, b, rhs, dh)),
+                ("sweep_prolong", 0, cfg, lambda: S.gsrb_sweep_prolong(a, b, rhs, dh, c)),
+                ("sweep_norm", 0, cfg, lambda: S.gsrb_sweep_norm(a, b, rhs, dh, nrm)),
                 ("sweep+push", 0, cfg, lambda: S.gsrb_sweep(a, b, rhs, dh, push=tab)),
                 ("sweep_norm+push", 0, cfg, lambda: S.gsrb_sweep_norm(a, b, rhs, dh, nrm, push=tab)),
                 ("sweep_prolong+push", 0, cfg, lambda: S.gsrb_sweep_prolong(a, b, rhs, dh, c, push=tab))]
