@@ -540,13 +540,150 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
 }
 
 // ---------------------------------------------------------------------------
+// k_resid_restrict_stream: crse = average_down(rhs - L(phi)) (coarse_fine.py:
+// 136-163 applied to the residual, the V-cycle's down-leg transfer), streamed
+// like the sweep: phi (+ halo) and rhs plane tiles by TMA, each lane owning a
+// k-pair of RW rows and its column's planes q-1 .. q+1 in registers, j/k
+// neighbours from shared memory (read only: nothing is written back), one
+// barrier per plane for the ring.  A k-pair x row-pair x plane-pair is one
+// coarse cell: the pair sums of plane 2I are kept until plane 2I+1 arrives and
+// the eight residuals are summed in numpy's reshape-mean order
+// ((((c000+c001) + (c010+c011)) + (c100+c101)) + (c110+c111)) * 0.125 (avg8 in
+// stencil.cu).  Segments start on even planes; a downward segment meets the
+// odd plane of a pair first and keeps its pair sums instead.
+// ---------------------------------------------------------------------------
+struct RRArgs {
+  const int* seg;
+  const BoxGeom* geo;
+  const FabView* fc;  // coarse views (box-local coarsening of the fine boxes)
+  double* crse;
+  const int* slot;
+  Coef cf;
+  int a_kc, a_jc, a_ic, r_kc, r_jc, r_ic;
+};
+
+template <int TJ, int TK, int RW, int D>
+__global__ void __launch_bounds__(32 * (TJ / (RW * (TK >= 64 ? 1 : 64 / TK))) * (TK >= 64 ? TK / 64 : 1))
+    k_resid_restrict_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
+                            const __grid_constant__ RRArgs args) {
+  pdl_entry();
+  using LY = StreamLayout<TJ, TK, D, kModePlain>;
+  constexpr int WK = LY::WK, LK = LY::LK, RPW = LY::RPW, NS = LY::NS, PK = LY::PK;
+  static_assert(RW % 2 == 0, "row pairs");
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + LY::BAR);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Coef cf = args.cf;
+  const int* sg = args.seg + 8 * blockIdx.x;
+  const int box = sg[0], j0 = sg[1], k0 = sg[2], i0 = sg[3], i1 = sg[4], dir = sg[5];
+  const int L = i1 - i0;
+  const int istart = dir > 0 ? i0 : i1 - 1;
+  const int bslot = args.slot[box];
+  auto plane = [&](int q) { return istart + dir * q; };
+  // phi position q in slot (q + 1) % NS (q >= -1); rhs position q rides with phi q+1
+  auto slot_base = [&](int q) { return sm + ((q + 1) % NS) * LY::SLOT; };
+  auto phi_s = [&](int q) { return reinterpret_cast<const double*>(slot_base(q)); };
+  auto rhs_s = [&](int q) { return reinterpret_cast<const double*>(slot_base(q + 1) + LY::ROFF); };
+  auto wait_pos = [&](int q) { mbar_wait(&bars[(q + 1) % NS], (unsigned)(((q + 1) / NS) & 1)); };
+  auto issue = [&](int q) {  // phi position q (q = -1 .. L), rhs position q-1 (from q = 1)
+    uint64_t* bar = &bars[(q + 1) % NS];
+    const bool wr = q >= 1;
+    mbar_expect_tx(bar, LY::PB + (wr ? LY::RB : 0));
+    tma_load4(slot_base(q), &tmA, bar, k0 + args.a_kc, j0 + args.a_jc, plane(q) + args.a_ic, bslot);
+    if (wr) tma_load4(slot_base(q) + LY::ROFF, &tmR, bar, k0 + args.r_kc, j0 + args.r_jc, plane(q - 1) + args.r_ic, bslot);
+  };
+  if (tid == 0) {
+    for (int x = 0; x < NS; ++x) mbar_init(&bars[x], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = -1; q <= min(NS - 2, L); ++q) issue(q);
+
+  const int wk = warp % WK;
+  const int rg = lane / LK;
+  const int m = LK * wk + lane % LK;
+  const int c0 = 2 + 2 * m;
+  const int r0 = 2 + ((warp / WK) * RPW + rg) * RW;
+  const FabView Cv = args.fc[box];
+  // coarse row of strip row pair x/2, coarse column of the pair
+  double* cout = args.crse + Cv.off + (int64_t)((j0 + r0 - 2) >> 1) * Cv.s1 + ((k0 + 2 * m) >> 1);
+  double a0[RW][2], a1[RW][2], a2[RW][2], keep[RW / 2][2];
+  auto arrive = [&](int q, double (&dst)[RW][2]) {
+    const double* S = phi_s(q);
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const double2 v = lds2(S + (r0 + x) * PK + c0);
+      dst[x][0] = v.x;
+      dst[x][1] = v.y;
+    }
+  };
+  wait_pos(-1);
+  wait_pos(0);
+  arrive(-1, a0);
+  arrive(0, a1);
+  auto step = [&](auto up_tag, int q) {
+    constexpr bool UP = decltype(up_tag)::value;
+    wait_pos(q + 1);
+    arrive(q + 1, a2);
+    const double* S = phi_s(q);
+    const double* R = rhs_s(q);
+    double r[RW][2];
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      const int row = (r0 + x) * PK;
+      const double2 rh = lds2(R + row - PK + c0);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double c = a1[x][e];
+        const double prev = a0[x][e], next = a2[x][e];
+        const double ym = x > 0 ? a1[x > 0 ? x - 1 : 0][e] : S[row - PK + c0 + e];
+        const double yp = x < RW - 1 ? a1[x < RW - 1 ? x + 1 : 0][e] : S[row + PK + c0 + e];
+        const double zm = e ? a1[x][0] : S[row + c0 - 1];
+        const double zp = e ? S[row + c0 + 2] : a1[x][1];
+        const double lap = UP ? lap7(c, prev, next, ym, yp, zm, zp, cf) : lap7(c, next, prev, ym, yp, zm, zp, cf);
+        r[x][e] = (e ? rh.y : rh.x) - lap;
+      }
+    }
+    const int ip = plane(q);
+    const bool first = UP ? (ip & 1) == 0 : (ip & 1) == 1;  // first plane of its pair in stream order
+#pragma unroll
+    for (int h = 0; h < RW / 2; ++h) {
+      const double pr = r[2 * h][0] + r[2 * h][1];          // pair sum, row 2h
+      const double qr = r[2 * h + 1][0] + r[2 * h + 1][1];  // pair sum, row 2h+1
+      if (first) {
+        keep[h][0] = pr;
+        keep[h][1] = qr;
+      } else {
+        // even plane's (P0, Q0), odd plane's (P1, Q1): ((P0 + Q0) + P1) + Q1
+        const double s = UP ? ((keep[h][0] + keep[h][1]) + pr) + qr : ((pr + qr) + keep[h][0]) + keep[h][1];
+        cout[(int64_t)(ip >> 1) * Cv.s0 + (int64_t)h * Cv.s1] = s * 0.125;
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < RW; ++x) {
+      a0[x][0] = a1[x][0];
+      a0[x][1] = a1[x][1];
+      a1[x][0] = a2[x][0];
+      a1[x][1] = a2[x][1];
+    }
+    __syncthreads();  // everyone is done with phi q-1's slot (and rhs q-1)
+    if (tid == 0 && q + NS - 1 <= L) issue(q + NS - 1);
+  };
+  if (dir > 0)
+    for (int q = 0; q < L; ++q) step(std::true_type{}, q);
+  else
+    for (int q = 0; q < L; ++q) step(std::false_type{}, q);
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 // (column, segment) work items: every resident box cut into TJ x TK columns,
 // each column into nseg near-equal plane ranges; odd segments stream downward.
 // Cached on the Level.
-const SegTable& seg_table(Level& lv, int tj, int tk, int nseg, bool alternate) {
-  auto key = std::make_tuple(tj, tk, alternate ? nseg : -nseg);
+const SegTable& seg_table(Level& lv, int tj, int tk, int nseg, bool alternate, bool even = false) {
+  auto key = std::make_tuple(tj * (even ? -1 : 1), tk, alternate ? nseg : -nseg);
   auto it = lv.segtabs.find(key);
   if (it != lv.segtabs.end()) return *it->second;
   auto* t = new SegTable;
@@ -557,7 +694,11 @@ const SegTable& seg_table(Level& lv, int tj, int tk, int nseg, bool alternate) {
     for (int j = 0; j < gb.n[1]; j += tj)
       for (int k = 0; k < gb.n[2]; k += tk)
         for (int s = 0; s < ns; ++s) {
-          const int a = (int)((long long)gb.n[0] * s / ns), e = (int)((long long)gb.n[0] * (s + 1) / ns);
+          int a = (int)((long long)gb.n[0] * s / ns), e = (int)((long long)gb.n[0] * (s + 1) / ns);
+          if (even) {  // plane pairs stay inside one segment
+            a &= ~1;
+            e = s + 1 == ns ? gb.n[0] : (e & ~1);
+          }
           if (e <= a) continue;
           const int v[8] = {b, j, k, a, e, (alternate && (s & 1)) ? -1 : 1, 0, 0};
           t->host.insert(t->host.end(), v, v + 8);
@@ -656,6 +797,72 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
   return true;
 }
 
+
+template <int TJ, int TK, int RW, int D>
+bool launch_rr_stream(Level& lv, const Field& phi, const double* phi_base, const Field& rhs, const double* rhs_base,
+                      const Field& crse, double* crse_base, const Coef& cf, cudaStream_t st) {
+  using LY = StreamLayout<TJ, TK, D, kModePlain>;
+  constexpr int NW = TJ / (RW * LY::RPW) * LY::WK;
+  int nres = 0;
+  for (int bx = 0; bx < lv.nboxes; ++bx) {
+    if (!lv.resident[bx]) continue;
+    ++nres;
+    const BoxGeom& gg = lv.geo[bx];
+    if (gg.n[1] % TJ || gg.n[2] % TK || gg.n[0] % 2 || gg.lo[0] % 2 || gg.lo[1] % 2 || gg.lo[2] % 2) return false;
+  }
+  if (phi.ngrow < 2 || rhs.ngrow < 1) return false;
+  if (nres == 0) return true;
+  TmaDesc da = describe(lv, phi), dr = describe(lv, rhs);
+  if (!da.ok || !dr.ok || da.slot != lv.slot || dr.slot != lv.slot) return false;
+  CUtensorMap ma, mr;
+  std::memset(&ma, 0, sizeof ma);
+  std::memset(&mr, 0, sizeof mr);
+  if (!make_map(&ma, phi_base, da, nres, LY::PJ, LY::PK)) return false;
+  if (!make_map(&mr, rhs_base, dr, nres, LY::RJ, LY::PK)) return false;
+  RRArgs args;
+  std::memset(&args, 0, sizeof args);
+  args.a_kc = -2 + da.g + da.f;
+  args.a_jc = -2 + da.g;
+  args.a_ic = da.g;
+  args.r_kc = -2 + dr.g + dr.f;
+  args.r_jc = -1 + dr.g;
+  args.r_ic = dr.g;
+  auto kern = k_resid_restrict_stream<TJ, TK, RW, D>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
+    AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NW, LY::BYTES));
+    per_sm = std::max(per_sm, 1);
+  }
+  long long ncols = 0;
+  for (int bx = 0; bx < lv.nboxes; ++bx)
+    if (lv.resident[bx]) ncols += (long long)(lv.geo[bx].n[1] / TJ) * (lv.geo[bx].n[2] / TK);
+  const int nseg = (int)std::max<long long>(1, (long long)per_sm * num_sms() / ncols);
+  const SegTable& t = seg_table(lv, TJ, TK, nseg, option("stream_alternate") != 0, true);
+  args.seg = t.dev.p;
+  args.geo = lv.dgeo.p;
+  args.fc = crse.dev.p;
+  args.crse = crse_base;
+  args.slot = lv.dslot.p;
+  args.cf = cf;
+  launch_k(kern, (unsigned)t.n, 32 * NW, LY::BYTES, st, ma, mr, args);
+  check_launch("k_resid_restrict_stream");
+  return true;
+}
+
+}  // namespace
+
+// crse (on the box-local coarsening of phi's level) = average_down(rhs - L(phi));
+// false (nothing launched) where the layout does not take the streaming kernel
+bool launch_resid_restrict_stream(Level& lv, const Field& phi, const double* phi_base, const Field& rhs,
+                                  const double* rhs_base, const Field& crse, double* crse_base, const Coef& cf,
+                                  cudaStream_t st) {
+  return launch_rr_stream<16, 64, 4, 2>(lv, phi, phi_base, rhs, rhs_base, crse, crse_base, cf, st) ||
+         launch_rr_stream<16, 32, 4, 2>(lv, phi, phi_base, rhs, rhs_base, crse, crse_base, cf, st);
+}
+
+namespace {
 }  // namespace
 
 unsigned int* debug_check_words() {

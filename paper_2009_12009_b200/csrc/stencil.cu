@@ -1300,6 +1300,11 @@ extern "C" int amrb_residual_restrict(const amrb_level* clv_, amrb_field* crse, 
     Level& lv = Lm(clv_);
     need_same_level(F(crse), lv, "residual_restrict");
     need_ghost(F(phi), 1, "residual_restrict");
+    const Field& fphi = F(phi);
+    if (option("sweep_kernel") == 0 && fphi.lv &&
+        launch_resid_restrict_stream(const_cast<Level&>(*fphi.lv), fphi, phi_base, F(rhs), rhs_base, F(crse), crse_base,
+                                     make_coef(dh), (cudaStream_t)stream))
+      return;
     const auto& tt = lv.tiles(pick_ti(lv, kTJ, kTK), kTJ, kTK);
     launch_tiles(tt, k_resid_restrict, (cudaStream_t)stream, dim3(32, 8), lv.dgeo.p, F(crse).dev.p, crse_base,
                  F(rhs).dev.p, rhs_base, F(phi).dev.p, phi_base, make_coef(dh));

@@ -49,6 +49,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // gsrb_stream.cu: mode 0 plain, 1 fused prolongation (clv / c / c_base),
 // 2 plain + max |rhs - L(a)| into *norm (u64 bit pattern, caller zeroes it)
+bool launch_resid_restrict_stream(Level& lv, const Field& phi, const double* phi_base, const Field& rhs,
+                                  const double* rhs_base, const Field& crse, double* crse_base, const Coef& cf,
+                                  cudaStream_t st);
 bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                          const Field& r, const double* r_base, const Coef& cf, const int flo[3], const int fhi[3],
                          cudaStream_t st, const Level* clv, const Field* c, const double* c_base,

@@ -238,3 +238,34 @@ def test_push_table_rejects_irregular_layout():
     dm = A.DistributionMapping.single_rank(len(ba))
     f = A.MultiFab(ba, dm, 1, 2)
     assert push_table(f, A.Box((0, 0, 0), (63, 63, 63)), True, 2) is None
+
+
+@pytest.mark.parametrize("shape,m", [((256, 256, 256), 256), ((128, 128, 128), 64), ((64, 64, 64), 32),
+                                     ((96, 64, 128), 128), ((6, 32, 64), 64)])
+def test_stream_resid_restrict(rng, shape, m):
+    """k_resid_restrict_stream == the tile kernel (k_resid_restrict, sweep_kernel
+    option 1) == the oracle's residual + average_down, bit for bit; several
+    plane segments per column, streamed both ways."""
+    dom, ba, dm, tr, per, a, rhs, g, gr = _setup(rng, 0, m, shape=shape)
+    cba = A.coarsened_layout(ba, 2)
+    out = {}
+    for legacy in (False, True):
+        c = A.MultiFab(cba, dm, 1, 1)
+        with option("sweep_kernel", 1 if legacy else 0):
+            S.residual_restrict(c, rhs, a, DH)
+        torch.cuda.synchronize()
+        out[legacy] = _valid(c)
+    _eq(out[False], out[True])
+    if shape[0] * shape[1] * shape[2] <= 64**3:
+        boxes = tboxes(ba)
+        d = (tuple(dom.lo), tuple(dom.hi))
+        pf = M.make_fabs(boxes, 1, 1)
+        rf = M.make_fabs(boxes, 1, 0)
+        M.load_global(boxes, pf, 1, d, g)
+        M.load_global(boxes, rf, 0, d, gr)
+        M.fill_boundary(boxes, pf, 1, d, per)
+        r = {i: (rf[i][0] - R.laplacian(pf[i][0], DH))[None] for i in pf}
+        cf = M.make_fabs(tboxes(cba), 1, 0)
+        M.average_down(boxes, r, 0, tboxes(cba), cf, 0, (2, 2, 2))
+        for i in cf:
+            assert np.array_equal(out[False][i], cf[i]), i

@@ -1,7 +1,7 @@
 """torchrun: per-op graph timings of the distributed MLMG (C4 layout)."""
 import os, sys, numpy as np, torch, torch.distributed as dist
 sys.path.insert(0, '/root/repo')
-world = int(os.environ["WORLD_SIZE"]); rank = int(os.environ["RANK"]); local = int(os.environ["LOCAL_RANK"])
+world = int(os.environ.get("WORLD_SIZE", "1")); rank = int(os.environ.get("RANK", "0")); local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 import paper_2009_12009_b200 as A
