@@ -663,6 +663,7 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kTailThreads, 
 // ---------------------------------------------------------------------------
 struct GridLevelArgs {
   int n0, n1, n2, lo_par, nsw, up;
+  int l1, l2;  // log2(n1), log2(n2) when powers of two, else -1 (index math by shifts)
   Coef cf;
   double* phi;  // valid lo cell
   int ps0, ps1;  // 32-bit strides: these levels are small (checked on the host)
@@ -672,31 +673,69 @@ struct GridLevelArgs {
   int cs0, cs1;
 };
 
-__global__ void __launch_bounds__(512, 2) k_level_grid(GridLevelArgs a) {
+// e -> (e / n, e % n): shifts when n = 2^l
+__device__ __forceinline__ void divmod(int e, int n, int l, int& q, int& r) {
+  if (l >= 0) {
+    q = e >> l;
+    r = e & (n - 1);
+  } else {
+    q = e / n;
+    r = e - q * n;
+  }
+}
+
+// One single-box periodic level's half V-cycle, cooperative: every phase is a
+// grid-stride loop, phases separated by grid.sync.  The level (<= 2^20 cells)
+// lives in L2, so a phase is bound by gather latency: each thread works on
+// kU cells at once with all their loads issued before any arithmetic.
+constexpr int kU = 4;
+
+__global__ void __launch_bounds__(512, 1) k_level_grid(GridLevelArgs a) {
   pdl_entry();
   namespace cg = cooperative_groups;
   cg::grid_group g = cg::this_grid();
   const int nt = (int)gridDim.x * blockDim.x;
   const int t0 = (int)blockIdx.x * blockDim.x + threadIdx.x;
   const int n0 = a.n0, n1 = a.n1, n2 = a.n2, h = n2 >> 1;
+  const int lh = a.l2 > 0 ? a.l2 - 1 : -1;
   const int ncell = (int)n0 * n1 * n2;
   double* const p = a.phi;
   auto P = [&](int i, int j, int k) -> double& { return p[i * a.ps0 + j * a.ps1 + k]; };
-  auto lapw = [&](int i, int j, int k) {
+  // the 7-point operator at (i, j, k) with periodic wrap; operands first
+  struct Nb {
+    double c, xm, xp, ym, yp, zm, zp;
+  };
+  auto load = [&](int i, int j, int k) {
     const int im = i ? i - 1 : n0 - 1, ip = i + 1 < n0 ? i + 1 : 0;
     const int jm = j ? j - 1 : n1 - 1, jp = j + 1 < n1 ? j + 1 : 0;
     const int km = k ? k - 1 : n2 - 1, kp = k + 1 < n2 ? k + 1 : 0;
-    return lap7(P(i, j, k), P(im, j, k), P(ip, j, k), P(i, jm, k), P(i, jp, k), P(i, j, km), P(i, j, kp), a.cf);
+    return Nb{P(i, j, k), P(im, j, k), P(ip, j, k), P(i, jm, k), P(i, jp, k), P(i, j, km), P(i, j, kp)};
+  };
+  auto lapn = [&](const Nb& n) { return lap7(n.c, n.xm, n.xp, n.ym, n.yp, n.zm, n.zp, a.cf); };
+  auto cell = [&](int e, int& i, int& j, int& k) {
+    int ij;
+    divmod(e, n2, a.l2, ij, k);
+    divmod(ij, n1, a.l1, i, j);
   };
   auto color = [&](int c) {
-    for (int e = t0; e < ncell / 2; e += nt) {
-      const int kq = (int)(e % h);
-      const int ij = e / h;
-      const int j = (int)(ij % n1), i = (int)(ij / n1);
-      const int k = 2 * kq + ((a.lo_par + i + j + c) & 1);
-      const double v = P(i, j, k);
-      const double lap = lapw(i, j, k);
-      P(i, j, k) = relax(v, a.rhs[i * a.rs0 + j * a.rs1 + k], lap, a.cf.rgamma);
+    for (int e0 = t0; e0 < ncell / 2; e0 += kU * nt) {
+      Nb nb[kU];
+      double rh[kU];
+      int off[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = min(e0 + u * nt, ncell / 2 - 1);  // clamped duplicates are not stored
+        int kq, ij, i, j;
+        divmod(e, h, lh, ij, kq);
+        divmod(ij, n1, a.l1, i, j);
+        const int k = 2 * kq + ((a.lo_par + i + j + c) & 1);
+        nb[u] = load(i, j, k);
+        rh[u] = a.rhs[i * a.rs0 + j * a.rs1 + k];
+        off[u] = i * a.ps0 + j * a.ps1 + k;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (e0 + u * nt < ncell / 2) p[off[u]] = relax(nb[u].c, rh[u], lapn(nb[u]), a.cf.rgamma);
     }
   };
   auto smooth = [&]() {
@@ -707,12 +746,6 @@ __global__ void __launch_bounds__(512, 2) k_level_grid(GridLevelArgs a) {
       g.sync();
     }
   };
-  auto cell = [&](int e, int& i, int& j, int& k) {
-    k = (int)(e % n2);
-    const int ij = e / n2;
-    j = (int)(ij % n1);
-    i = (int)(ij / n1);
-  };
   if (!a.up) {
     for (int e = t0; e < ncell; e += nt) {
       int i, j, k;
@@ -722,11 +755,13 @@ __global__ void __launch_bounds__(512, 2) k_level_grid(GridLevelArgs a) {
     g.sync();
     smooth();
     const int c0 = n0 >> 1, c1 = n1 >> 1, c2 = n2 >> 1;
+    const int lc1 = a.l1 > 0 ? a.l1 - 1 : -1, lc2 = a.l2 > 0 ? a.l2 - 1 : -1;
     for (int e = t0; e < ncell / 8; e += nt) {
-      const int K = (int)(e % c2);
-      const int IJ = e / c2;
-      const int J = (int)(IJ % c1), I = (int)(IJ / c1);
-      double v[8];
+      int K, IJ, I, J;
+      divmod(e, c2, lc2, IJ, K);
+      divmod(IJ, c1, lc1, I, J);
+      Nb nb[8];
+      double rh[8];
 #pragma unroll
       for (int di = 0; di < 2; ++di)
 #pragma unroll
@@ -734,10 +769,15 @@ __global__ void __launch_bounds__(512, 2) k_level_grid(GridLevelArgs a) {
 #pragma unroll
           for (int dk = 0; dk < 2; ++dk) {
             const int i = 2 * I + di, j = 2 * J + dj, k = 2 * K + dk;
-            v[di * 4 + dj * 2 + dk] = a.rhs[i * a.rs0 + j * a.rs1 + k] - lapw(i, j, k);
+            nb[di * 4 + dj * 2 + dk] = load(i, j, k);
+            rh[di * 4 + dj * 2 + dk] = a.rhs[i * a.rs0 + j * a.rs1 + k];
           }
+      double v[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) v[x] = rh[x] - lapn(nb[x]);
       a.c[I * a.cs0 + J * a.cs1 + K] = avg8t(v);
     }
+    (void)c0;
     return;
   }
   for (int e = t0; e < ncell; e += nt) {
@@ -956,6 +996,13 @@ extern "C" int amrb_level_grid(int up, const int32_t* lohi, const double* dh, co
     a.c = crse_base + vc.off;
     a.cs0 = vc.s0;
     a.cs1 = vc.s1;
+    auto lg = [](int n) {
+      int l = 0;
+      while ((1 << l) < n) ++l;
+      return (1 << l) == n ? l : -1;
+    };
+    a.l1 = lg(n[1]);
+    a.l2 = lg(n[2]);
     static int max_per_sm = 0;
     if (!max_per_sm) {
       AMRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, k_level_grid, 512, 0));
