@@ -223,7 +223,7 @@ def run_ours(args):
     rhs_sha = hashlib.sha256(rhs_np.tobytes()).hexdigest()
     del rhs_np
     phi = A.MultiFab(ba, dm, 1, 1)
-    mg = A.MLMG(geom, ba, dm, transport=tr, ghost_push={"auto": None, "on": True, "off": False}[args.ghost_push])
+    mg = A.MLMG(geom, ba, dm, transport=tr, ghost_push={"auto": None, "on": True, "off": False, "remote": "remote"}[args.ghost_push])
 
     def barrier():
         torch.cuda.synchronize()
@@ -355,6 +355,27 @@ def run_ours(args):
     e2e_value = mg.cell_updates_per_cycle * sum(p_iters) / t_e2e
     e2e_serial = mg.cell_updates_per_cycle * sum(e_iters) / t_serial
 
+    # what bounds the pipelined loop: the same copies alone (both directions at
+    # once, every rank at once) and the same solves alone, host-timed
+    barrier()
+    t0 = time.perf_counter()
+    for s_ in range(args.steps):
+        with torch.cuda.stream(cs):
+            upload(s_ % 2)
+        with torch.cuda.stream(ds):
+            download(s_ % 2)
+        torch.cuda.synchronize()
+    barrier()
+    t_copies = maxover(time.perf_counter() - t0)
+    barrier()
+    t0 = time.perf_counter()
+    for s_ in range(args.steps):
+        dev_phi[0].setval(0.0)
+        mg.solve(dev_phi[0], dev_rhs[0], rtol=1e-10, max_iter=100)
+    torch.cuda.synchronize()
+    barrier()
+    t_solves = maxover(time.perf_counter() - t0)
+
     # ---- roofline: fine-level fused sweep, events on its launch stream ----------
     top = mg.levels[0]
     a, b = top.phi[0], top.phi[1]
@@ -410,7 +431,9 @@ def run_ours(args):
                     "ms_per_step": 1e3 * t_e2e / args.steps,
                     "mode": "pipelined: double-buffered rhs/phi (FabArray host images), step s+1 upload and step s-1 "
                             "download on two copy streams during step s's solve (all copies inside the timed region)",
-                    "serial": {"value": e2e_serial, "ms_per_step": 1e3 * t_serial / args.steps}},
+                    "serial": {"value": e2e_serial, "ms_per_step": 1e3 * t_serial / args.steps},
+                    "bounds": {"copies_only_ms_per_step": 1e3 * t_copies / args.steps,
+                               "solves_only_ms_per_step": 1e3 * t_solves / args.steps}},
             "roofline": {"bound": "hbm", "kernel": "k_gsrb_stream (fine level, fused red+black, register-streamed, TMA-fed)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
@@ -759,7 +782,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the C1 / C5 microtimings of the C3 line")
-    ap.add_argument("--ghost-push", default="auto", choices=["auto", "on", "off"],
+    ap.add_argument("--ghost-push", default="auto", choices=["auto", "on", "off", "remote"],
                     help="A/B runs: MLMG ghost push (auto: across GPUs only)")
     ap.add_argument("--config", default="c3", choices=["c3", "c5"],
                     help="c3: the headline MLMG solve (C3 / C4 weak scaling); c5: 512^3 sweeps (strong scaling)")

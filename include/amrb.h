@@ -59,15 +59,19 @@ int64_t amrb_launch_count(void);
  * repeats a captured body until its control kernel says stop.  Between
  * amrb_loop_begin and amrb_loop_end every launch on `stream` is captured into
  * the body; the body must end with amrb_loop_control, which appends *norm to
- * the pinned host block's history, zeroes *norm, counts the iteration and
+ * the state block's history, zeroes *norm, counts the iteration and
  * continues while !(norm <= rtol * *r0) and iters < max_iter (the oracle's
- * stopping test, oracle/mlmg_ref.py OracleMLMG.solve).  host_block: pinned
- * host memory {double rtol; int32 max_iter; int32 iters; double hist[capacity]}
- * read and written by the device through UVA; set rtol, max_iter and
- * iters = 0 before amrb_loop_launch, synchronize, then read iters / hist. */
+ * stopping test, oracle/mlmg_ref.py OracleMLMG.solve).  state: DEVICE memory
+ * {double rtol; int32 max_iter; int32 iters; double r0; double
+ * hist[capacity]}; amrb_loop_reset fills rtol / max_iter / r0 and zeroes
+ * iters (a kernel, on the launch stream) before amrb_loop_launch; afterwards
+ * move it to the host (amrb_store_host) and read iters / hist.  Nothing in
+ * the loop touches host memory, so it does not wait behind bulk PCIe copies
+ * running on other streams. */
 typedef struct amrb_loop amrb_loop;
 int amrb_loop_begin(void* stream, amrb_loop** out);
-int amrb_loop_control(amrb_loop* loop, double* norm, const double* r0, void* host_block, int capacity,
+int amrb_loop_reset(void* state, double rtol, int max_iter, const double* r0, void* stream);
+int amrb_loop_control(amrb_loop* loop, double* norm, const double* r0, void* state, int capacity,
                       void* stream);
 int amrb_loop_end(amrb_loop* loop);
 int amrb_loop_launch(amrb_loop* loop, void* stream);
@@ -164,7 +168,11 @@ int amrb_plan_destroy(amrb_plan* p);
 /*     from the owner's storage over NVLink (src_fabtab = every box's layout */
 /*     in its owner's allocation; see amrb_prog_run_p2p).                   */
 /* op: 0 = dst = src (fill / parallel_copy), 1 = dst += src (sum_boundary;   */
-/*     overlapping records are applied in plan order, in waves).             */
+/*     overlapping records are applied in plan order, in waves);            */
+/*     2 = copy only the records whose SOURCE box is resident here (mode 3   */
+/*     only: the local half of a fill whose remote half the producing sweep  */
+/*     pushed over NVLink; run it with amrb_prog_run_p2p_sync, whose fused   */
+/*     barrier then orders the peers' pushes before the consumer).           */
 /* Message payloads are C-order (ncomp, e0, e1, e2) record slices           */
 /* concatenated in plan order -- the reference's message layout (:341-347). */
 /* ------------------------------------------------------------------------ */
@@ -199,14 +207,19 @@ int amrb_prog_run_p2p_sync(amrb_prog* g, const double* src_base, double* dst_bas
  * rank r's pad (>= nranks uint32 slots), epoch = this rank's device counter. */
 /* Failure detection: pinned host memory of 4 uint64 {code, rank, peer, epoch}
  * the device-side peer waits report into (code 1: a peer did not arrive within
- * the "peer_timeout_ms" option; later waits then return at once).  The caller
- * zeroes it, and after synchronising raises TransportError(rank, peer) when
- * code != 0 (comm.py Transport.check_faults).  NULL disables reporting. */
+ * the "peer_timeout_ms" option; later waits then return at once -- the
+ * waits poll a device-memory twin of the code, never the host block).  The
+ * caller zeroes it, and after synchronising raises TransportError(rank, peer)
+ * when code != 0 (comm.py Transport.check_faults).  NULL disables reporting. */
 int amrb_set_fault_mailbox(void* pinned_host);
 int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch,
                       void* stream);
-/* In-place max over ranks of one device double over NVLink (one launch):
- * slot_ptrs[r] = rank r's symmetric buffer of >= nranks doubles. */
+/* In-place max over ranks of one device double >= 0 over NVLink (one launch,
+ * also a device barrier; NaN on any rank wins): slot_ptrs[r] = rank r's
+ * symmetric buffer of >= 2 * nranks uint64 words, zeroed before first use
+ * (epoch-tagged value halves; pad_ptrs is unused, kept for the signature).
+ * Cross-GPU signalling uses gpu-scope fences only (see comm.cu): no
+ * system-scope fence that would wait behind in-flight PCIe copies. */
 int amrb_peer_allmax(const uint64_t* pad_ptrs, const uint64_t* slot_ptrs, int rank,
                      int nranks, uint32_t* epoch, double* val, void* stream);
 

@@ -41,6 +41,7 @@ _SIGS = {
     "amrb_version": (C.c_int, []),
     "amrb_launch_count": (i64, []),
     "amrb_loop_begin": (C.c_int, [vp, P(vp)]),
+    "amrb_loop_reset": (C.c_int, [vp, C.c_double, C.c_int, vp, vp]),
     "amrb_loop_control": (C.c_int, [vp, vp, vp, vp, C.c_int, vp]),
     "amrb_loop_end": (C.c_int, [vp]),
     "amrb_loop_launch": (C.c_int, [vp, vp]),

@@ -109,7 +109,9 @@ class Transport:
             self._bar_buf = symm_mem.empty(64, dtype=torch.int32, device=dev)
             self._bar = symm_mem.rendezvous(self._bar_buf, dist.group.WORLD.group_name)
             self._pads = np.array(self._bar.signal_pad_ptrs, dtype=np.uint64)
+            # peer_allmax: 2 epoch-tagged uint64 words per rank, zero before first use
             self._slots_buf = symm_mem.empty(16, dtype=torch.float64, device=dev)
+            self._slots_buf.zero_()
             self._slots = symm_mem.rendezvous(self._slots_buf, dist.group.WORLD.group_name)
             self._slot_ptrs = np.array(self._slots.buffer_ptrs, dtype=np.uint64)
             self._epoch = torch.zeros(2, dtype=torch.int32, device=dev)  # epoch, CTA ticket
@@ -302,6 +304,8 @@ def _execute(plan, src_fa, dst_fa, transport, op, post_barrier=True):
     src_fa.require_cuda("copy")
     dst_fa.require_cuda("copy")
     p2p = transport.mode == "nccl" and transport.p2p and getattr(src_fa, "symmetric", False)
+    if op == 2 and not p2p:
+        raise ValueError("a local-sources fill needs the p2p transport (symmetric storage)")
     key = (id(plan), src_fa.serial, op, transport.mode, nranks, p2p)
     prog = dst_fa._progs.get(key)
     if prog is None:
@@ -310,12 +314,16 @@ def _execute(plan, src_fa, dst_fa, transport, op, post_barrier=True):
     prog.run(src_fa, dst_fa, transport, post_barrier=post_barrier)
 
 
-def fill_boundary(fa, transport, domain, periodic=None, ngrow=None, _post_barrier=True):
+def fill_boundary(fa, transport, domain, periodic=None, ngrow=None, _post_barrier=True, _local_sources=False):
     """Fill every in-domain (or periodic-image) ghost cell from the valid cell it
     shadows; out-of-domain non-periodic ghosts are untouched (fabarray.py:364).
 
     ``ngrow`` (<= fa.ngrow) limits the exchange to the first ``ngrow`` ghost
     layers (AMReX FillBoundary(nghost)); default is all of them.
+    ``_local_sources`` (p2p transport only; the MLMG's remote ghost push) copies
+    only the ghost cells whose source box lives on this GPU -- peers already
+    stored the rest -- and is the device barrier that makes those stores
+    visible before the next kernel.
     """
     ng = fa.ngrow if ngrow is None else int(ngrow)
     if ng > fa.ngrow:
@@ -323,7 +331,7 @@ def fill_boundary(fa, transport, domain, periodic=None, ngrow=None, _post_barrie
     if ng == 0:
         return
     plan = build_plan_fill_boundary(fa.ba, ng, domain, periodic)
-    _execute(plan, fa, fa, transport, 0, post_barrier=_post_barrier)
+    _execute(plan, fa, fa, transport, 2 if _local_sources else 0, post_barrier=_post_barrier)
 
 
 def parallel_copy(dst_fa, src_fa, transport, domain=None, periodic=None):

@@ -63,6 +63,7 @@ struct PeerPtrs {
 // mailbox after its next synchronisation (Transport.check_faults).
 struct Fault {
   unsigned long long* box;  // [0] code (0 none, 1 peer wait timed out), [1] rank, [2] peer, [3] epoch
+  unsigned long long* dev;  // device twin of box[0]: what the waits poll (never host memory, see signal_store)
   unsigned long long timeout_ns;
 };
 
@@ -72,31 +73,58 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// Cross-GPU signals.  Every exchange here is a PULL: what a peer reads after
+// a signal lives in the signalling GPU's own HBM, written by earlier kernels,
+// and the owner's L2 serves the peer's NVLink loads -- so a gpu-scope release
+// fence orders it before the signal store, and the waiting side needs a
+// gpu-scope acquire fence after it sees the signal.  No system-scope fence:
+// fence.sc.sys / MEMBAR.SYS also drains this GPU's outstanding PCIe traffic,
+// and with bulk host copies in flight on side streams (the e2e pipeline) one
+// barrier measured 200 us instead of 6 (tools/mb_interfere.py, 4 GPUs).
+__device__ __forceinline__ void signal_store(uint32_t* slot, uint32_t v) {
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;\n" ::"l"(slot), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void record_fault(const Fault& f, int rank, int peer, uint32_t target) {
+  if (f.dev && atomicCAS(f.dev, 0ull, 1ull) == 0ull && f.box) {
+    f.box[1] = (unsigned long long)rank;
+    f.box[2] = (unsigned long long)peer;
+    f.box[3] = (unsigned long long)target;
+    __threadfence_system();  // failure path only
+    f.box[0] = 1ull;
+  }
+}
+
+__device__ __forceinline__ bool faulted(const Fault& f) {
+  return f.dev && *reinterpret_cast<volatile unsigned long long*>(f.dev) != 0;
+}
+
 // spin until *pad (wrap-safe) reaches `target`; false (and a fault recorded) on timeout
 __device__ bool peer_wait(const uint32_t* pad, uint32_t target, int rank, int peer, const Fault& f) {
-  if (f.box && *reinterpret_cast<volatile unsigned long long*>(f.box) != 0) return false;
+  if (faulted(f)) return false;
   const unsigned long long t0 = global_ns();
   for (unsigned it = 0;; ++it) {
     uint32_t x;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(pad) : "memory");
-    if ((int32_t)(x - target) >= 0) return true;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(pad) : "memory");
+    if ((int32_t)(x - target) >= 0) {
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+      return true;
+    }
     if ((it & 255) == 255 && f.timeout_ns && global_ns() - t0 > f.timeout_ns) {
-      if (f.box && atomicCAS(f.box, 0ull, 1ull) == 0ull) {
-        f.box[1] = (unsigned long long)rank;
-        f.box[2] = (unsigned long long)peer;
-        f.box[3] = (unsigned long long)target;
-        __threadfence_system();
-      }
+      record_fault(f, rank, peer, target);
       return false;
     }
   }
 }
 
 unsigned long long* g_fault_box = nullptr;  // amrb_set_fault_mailbox
+unsigned long long* g_fault_dev = nullptr;
 
 Fault current_fault() {
   Fault f;
   f.box = g_fault_box;
+  f.dev = g_fault_box ? g_fault_dev : nullptr;
   const int64_t ms = option("peer_timeout_ms");
   f.timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
   return f;
@@ -175,10 +203,7 @@ __global__ void __launch_bounds__(kCopyThreads)
         for (int q = 0; q < bl.y && !wait; ++q) wait |= recs[-bl.x - 1 + q].src_peer != sy.rank;
       }
       if (p < sy.nranks && p != sy.rank) {
-        if (blockIdx.x == 0) {
-          __threadfence_system();
-          asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(sy.pads[p] + sy.rank), "r"(ep) : "memory");
-        }
+        if (blockIdx.x == 0) signal_store(sy.pads[p] + sy.rank, ep);
         if (wait) peer_wait(sy.pads[sy.rank] + p, ep, sy.rank, p, sy.fault);
       }
     }
@@ -350,12 +375,17 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
                                 amrb_prog** out) {
   return amrb::guarded([&] {
     using namespace amrb;
-    if (!plan_ || !out || ncomp < 1 || nranks < 1 || my_rank < 0 || my_rank >= nranks || (op != 0 && op != 1) ||
+    if (!plan_ || !out || ncomp < 1 || nranks < 1 || my_rank < 0 || my_rank >= nranks || op < 0 || op > 2 ||
+        (op == 2 && mode != 3) ||
         mode < 0 || mode > 3 || (mode == 3 && nranks > kMaxPeers))
       throw Error(AMRB_EINVAL, "amrb_prog_create: bad arguments");
     const int sim_ranks = mode == 1;
     const bool local_only = mode == 2;
     const bool p2p = mode == 3;  // src_fabtab = each box's layout in its OWNER's storage
+    // op 2: copy only the records whose source is resident here (p2p: the
+    // local half of a fill whose remote half the producing kernel pushed)
+    const bool local_src = op == 2;
+    if (local_src) op = 0;
     const Plan& plan = *reinterpret_cast<const Plan*>(plan_);
     Tab st{src_fabtab}, dt{dst_fabtab};
     auto* g = new Prog;
@@ -376,6 +406,7 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
       if (sr[r] < 0 || sr[r] >= nranks || dr[r] < 0 || dr[r] >= nranks)
         throw Error(AMRB_EINVAL, "owner rank out of range");
       if (local_only && !(sr[r] == my_rank && dr[r] == my_rank)) sr[r] = dr[r] = -1;  // dropped
+      if (local_src && sr[r] != my_rank) sr[r] = dr[r] = -1;
     }
     // ---- message segments: ordered (src, dst) pairs, plan order inside ------
     // buffer offset of each remote record (elements)
@@ -630,8 +661,7 @@ __global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nra
   const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch) + 1;
   __syncwarp();
   if (p < nranks && p != rank) {
-    __threadfence_system();
-    asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
+    amrb::signal_store(pads.p[p] + rank, e);
     amrb::peer_wait(my_pad + p, e, rank, p, fault);
   }
   __syncwarp();
@@ -640,7 +670,16 @@ __global__ void k_peer_barrier(uint32_t* my_pad, PadPtrs pads, int rank, int nra
 }  // namespace
 
 extern "C" int amrb_set_fault_mailbox(void* pinned_host) {
-  return amrb::guarded([&] { amrb::g_fault_box = reinterpret_cast<unsigned long long*>(pinned_host); });
+  return amrb::guarded([&] {
+    if (pinned_host && !amrb::g_fault_dev) {
+      void* d = nullptr;
+      AMRB_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+      AMRB_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+      AMRB_CUDA(cudaDeviceSynchronize());
+      amrb::g_fault_dev = reinterpret_cast<unsigned long long*>(d);
+    }
+    amrb::g_fault_box = reinterpret_cast<unsigned long long*>(pinned_host);
+  });
 }
 
 extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch, void* stream) {
@@ -659,36 +698,60 @@ extern "C" int amrb_peer_barrier(const uint64_t* pad_ptrs, int rank, int nranks,
 
 using amrb::PeerPtrs;
 namespace {
-// Max-all-reduce of one double over NVLink: publish the local value into slot
-// [rank] of every peer's symmetric buffer, run the signal barrier, then take
-// the max over the local slots.  One launch, graph-replay safe (device epoch).
-__global__ void k_peer_allmax(uint32_t* my_pad, PadPtrs pads, amrb::Fault fault, int rank, int nranks, uint32_t* epoch,
-                              double* val, double* my_slots, PeerPtrs peer_slots) {
+// Max-all-reduce of one double over NVLink, as tagged words (no flag, no
+// fence on the data): rank r stores its value into slot r of every peer's
+// symmetric buffer as two 64-bit words (epoch << 32 | low half, epoch << 32 |
+// high half) -- each store single-copy atomic -- and each rank polls its own
+// slots until both words of every peer carry this epoch.  Arriving there also
+// means every peer finished the kernels before this one (the gpu-scope fence
+// before the stores orders them), so the call doubles as the device barrier.
+__global__ void k_peer_allmax(PadPtrs pads, amrb::Fault fault, int rank, int nranks, uint32_t* epoch, double* val,
+                              unsigned long long* my_slots, PeerPtrs peer_slots) {
   amrb::pdl_entry();
-  // one warp; lane p serves peer p (value store, publish, poll) concurrently
+  (void)pads;
+  // one warp; lane p serves peer p (stores, poll) concurrently
   const int p = threadIdx.x;
   const double v = *val;
   const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch) + 1;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long tag = (unsigned long long)e << 32;
+  double got = v;
   __syncwarp();
-  if (p < nranks) {
-    double* dst = const_cast<double*>(peer_slots.p[p]) + rank;
-    *dst = v;
-    if (p != rank) {
-      __threadfence_system();
-      asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pads.p[p] + rank), "r"(e) : "memory");
-      amrb::peer_wait(my_pad + p, e, rank, p, fault);
+  if (p < nranks && p != rank) {
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(const_cast<double*>(peer_slots.p[p])) + 2 * rank;
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;\n" ::"l"(dst), "l"(tag | (bits & 0xffffffffull)) : "memory");
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;\n" ::"l"(dst + 1), "l"(tag | (bits >> 32)) : "memory");
+    const unsigned long long* src = my_slots + 2 * p;
+    const unsigned long long t0 = amrb::global_ns();
+    bool dead = amrb::faulted(fault);
+    for (unsigned it = 0; !dead; ++it) {
+      unsigned long long lo, hi;
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];\n" : "=l"(lo) : "l"(src) : "memory");
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];\n" : "=l"(hi) : "l"(src + 1) : "memory");
+      if ((uint32_t)(lo >> 32) == e && (uint32_t)(hi >> 32) == e) {
+        got = __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+        break;
+      }
+      if ((it & 255) == 255 && fault.timeout_ns && amrb::global_ns() - t0 > fault.timeout_ns) {
+        amrb::record_fault(fault, rank, p, e);
+        dead = true;
+      }
     }
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }
-  __syncwarp();
-  if (p != 0) return;
-  *epoch = e;
-  double m = my_slots[0];
-  for (int p = 1; p < nranks; ++p) {
-    double x;
-    asm volatile("ld.acquire.sys.global.f64 %0, [%1];\n" : "=d"(x) : "l"(my_slots + p) : "memory");
-    m = fmax(m, x);
+  // max over lanes on the bit patterns: the operands are norms (>= 0), which
+  // order like their bits, and a NaN (above +inf) on any rank wins -- a
+  // diverged rank cannot look converged
+  unsigned long long gb = (unsigned long long)__double_as_longlong(got);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, gb, o);
+    gb = x > gb ? x : gb;
   }
-  *val = m;
+  if (p == 0) {
+    *epoch = e;
+    *val = __longlong_as_double((long long)gb);
+  }
 }
 }  // namespace
 
@@ -704,8 +767,8 @@ extern "C" int amrb_peer_allmax(const uint64_t* pad_ptrs, const uint64_t* slot_p
       pads.p[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
       slots.p[r] = reinterpret_cast<const double*>(slot_ptrs[r]);
     }
-    launch_k(k_peer_allmax, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream),
-        pads.p[rank], pads, current_fault(), rank, nranks, epoch, val, const_cast<double*>(slots.p[rank]), slots);
+    launch_k(k_peer_allmax, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream), pads, current_fault(), rank, nranks,
+             epoch, val, reinterpret_cast<unsigned long long*>(const_cast<double*>(slots.p[rank])), slots);
     check_launch("k_peer_allmax");
   });
 }

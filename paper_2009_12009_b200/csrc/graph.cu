@@ -3,12 +3,19 @@
 // The MLMG solve (paper_2009_12009_b200/mlmg.py) captures ONE iteration --
 // the V-cycle and the residual norm that decides whether to go on -- into the
 // body of a WHILE node; the body ends with k_loop_control, which appends the
-// norm to the residual history (pinned host memory), counts the iteration and
-// sets the node's condition to "not converged and under max_iter".  A whole
-// solve is then one graph launch and one host synchronisation, instead of a
-// replay + stream sync + host test per cycle.  The stopping test is the
-// oracle's (oracle/mlmg_ref.py OracleMLMG.solve): stop once
-// norm <= rtol * r0, evaluated in the same fp64 operations.
+// norm to the residual history, counts the iteration and sets the node's
+// condition to "not converged and under max_iter".  A whole solve is then one
+// graph launch and one host synchronisation, instead of a replay + stream sync
+// + host test per cycle.  The stopping test is the oracle's
+// (oracle/mlmg_ref.py OracleMLMG.solve): stop once norm <= rtol * r0,
+// evaluated in the same fp64 operations.
+//
+// The loop state lives in DEVICE memory: k_loop_reset writes it from kernel
+// arguments before a launch and the caller moves it to the host once after
+// (amrb_store_host).  Nothing inside the loop touches host memory -- a kernel
+// store to pinned memory, or a system-scope fence, waits behind whatever bulk
+// PCIe copies are in flight on other streams (measured 2 -> 70 us per store
+// with the e2e pipeline's copies running, tools/mb_interfere.py).
 #include <cuda_runtime.h>
 
 #include "device.h"
@@ -17,25 +24,30 @@ namespace amrb {
 
 namespace {
 
-// Pinned host block shared with the control kernel (UVA): the host writes
-// rtol / max_iter / iters = 0 before each launch and reads iters / hist after.
-struct LoopHost {
+struct LoopState {
   double rtol;
   int32_t max_iter;
   int32_t iters;
+  double r0;
   double hist[1];  // [capacity]
 };
 
-__global__ void k_loop_control(cudaGraphConditionalHandle h, double* norm, const double* r0, LoopHost* host,
+__global__ void k_loop_reset(LoopState* st, double rtol, int max_iter, const double* r0) {
+  st->rtol = rtol;
+  st->max_iter = max_iter;
+  st->iters = 0;
+  st->r0 = *r0;
+}
+
+__global__ void k_loop_control(cudaGraphConditionalHandle h, double* norm, const double* r0, LoopState* st,
                                int capacity) {
   pdl_entry();
   const double rn = *norm;
-  int it = host->iters;
-  if (it < capacity) host->hist[it] = rn;
-  host->iters = ++it;
+  int it = st->iters;
+  if (it < capacity) st->hist[it] = rn;
+  st->iters = ++it;
   *norm = 0.0;  // the next iteration's norm accumulates from zero
-  const bool done = rn <= host->rtol * *r0 || it >= host->max_iter;
-  __threadfence_system();
+  const bool done = rn <= st->rtol * *r0 || it >= st->max_iter;
   cudaGraphSetConditional(h, done ? 0u : 1u);
 }
 
@@ -87,15 +99,24 @@ extern "C" int amrb_loop_begin(void* stream, amrb_loop** out) {
   });
 }
 
-extern "C" int amrb_loop_control(amrb_loop* loop, double* norm, const double* r0, void* host_block, int capacity,
+extern "C" int amrb_loop_reset(void* state, double rtol, int max_iter, const double* r0, void* stream) {
+  return guarded([&] {
+    if (!state || !r0 || max_iter < 0) throw Error(AMRB_EINVAL, "amrb_loop_reset: bad arguments");
+    amrb::launch_k(amrb::k_loop_reset, 1, 1, 0, reinterpret_cast<cudaStream_t>(stream),
+                   reinterpret_cast<amrb::LoopState*>(state), rtol, max_iter, r0);
+    amrb::check_launch("k_loop_reset");
+  });
+}
+
+extern "C" int amrb_loop_control(amrb_loop* loop, double* norm, const double* r0, void* state, int capacity,
                                  void* stream) {
   return guarded([&] {
     Loop* L = reinterpret_cast<Loop*>(loop);
-    if (!L || !norm || !r0 || !host_block || capacity < 1) throw Error(AMRB_EINVAL, "amrb_loop_control: bad arguments");
+    if (!L || !norm || !r0 || !state || capacity < 1) throw Error(AMRB_EINVAL, "amrb_loop_control: bad arguments");
     if (!L->capturing || reinterpret_cast<cudaStream_t>(stream) != L->capture)
       throw Error(AMRB_EINVAL, "amrb_loop_control: not inside this loop's capture");
     amrb::launch_k(amrb::k_loop_control, 1, 1, 0, L->capture, L->handle, norm, r0,
-                   reinterpret_cast<amrb::LoopHost*>(host_block), capacity);
+                   reinterpret_cast<amrb::LoopState*>(state), capacity);
     amrb::check_launch("k_loop_control");
   });
 }

@@ -914,7 +914,8 @@ __global__ void k_store_host(const double* __restrict__ src, double* dst, int64_
   pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
-  __threadfence_system();
+  // (no system fence: the stores are visible to the host once the kernel has
+  // completed and the host synchronised with the stream)
 }
 }  // namespace
 }  // namespace amrb

@@ -23,6 +23,14 @@ other GPUs after a device barrier) and the copy-program fill disappears.
 destination lives on another GPU whose storage is not mapped here (no
 symmetric memory); callers then keep the copy-program fill.  The table is
 checked against the fill plan: the cells it covers must be exactly the plan's.
+
+``remote_only`` keeps only the destinations on other GPUs: the sweep stores
+the ghost faces its peers need over NVLink while it writes them, and the
+consumer's fill copies just the local-source records, as one launch that is
+also the device barrier (comm.fill_boundary(_local_sources=True)).  Only the
+cross-GPU part of the exchange moves into the kernel -- the part that costs a
+barrier plus NVLink round trips when pulled -- and the same-GPU ghosts stay a
+bulk copy (pushing those from the sweep's edge warps measured slower).
 """
 
 from __future__ import annotations
@@ -73,19 +81,20 @@ def _wrap(p, domain, periodic):
     return tuple(out)
 
 
-def push_table(fa, domain, periodic, width=2):
+def push_table(fa, domain, periodic, width=2, remote_only=False):
     """The push table of FabArray ``fa`` for ghost width ``width`` (see the
-    module docstring), cached on ``fa``; None if unsupported."""
+    module docstring), cached on ``fa``; None if unsupported (or, with
+    ``remote_only``, when no destination is on another GPU)."""
     periodic = normalize_periodic(periodic, fa.dim)
-    key = ("push", width, tuple(domain.lo), tuple(domain.hi), periodic)
+    key = ("push", width, tuple(domain.lo), tuple(domain.hi), periodic, bool(remote_only))
     if key in fa._native:
         return fa._native[key]
-    tab = _build(fa, domain, periodic, width)
+    tab = _build(fa, domain, periodic, width, bool(remote_only))
     fa._native[key] = tab
     return tab
 
 
-def _build(fa, domain, periodic, width):
+def _build(fa, domain, periodic, width, remote_only=False):
     if fa.dim != 3 or fa.ncomp != 1 or fa.ngrow < width or width < 1:
         return None
     ba = fa.ba
@@ -144,6 +153,8 @@ def _build(fa, domain, periodic, width):
                     return None  # would land on N's valid cells: not a lattice
                 if d[a] == 0 and (lo_t != N.lo[a] or hi_t != N.hi[a]):
                     return None  # faces must match box to box
+            if remote_only and owner[nb] == me:
+                continue  # same-GPU ghosts: the consumer's local fill
             covered += int(np.prod([h - l + 1 for l, h in zip(src_lo, src_hi)]))
             # element offset of the destination of B's local cell (0, 0, 0)
             rel = [B.lo[a] + t[a] - N.lo[a] for a in range(3)]
@@ -151,11 +162,15 @@ def _build(fa, domain, periodic, width):
             host[b, (d[0] + 1) * 9 + (d[1] + 1) * 3 + (d[2] + 1)] = bases[owner[nb]] + 8 * off
             remote |= owner[nb] != me
     # the table must cover exactly the fill plan's ghost cells of the resident boxes
+    if remote_only and not remote:
+        return None
     plan = build_plan_fill_boundary(ba, width, domain, periodic)
     if dist or n != int(np.count_nonzero(fa.resident)):
         table = plan.table()
         res = np.asarray(fa.resident)
         mine = res[table[:, 0]]  # records whose SOURCE box is resident here
+        if remote_only:
+            mine &= np.asarray(owner)[table[:, 1]] != me
         ext = table[:, 5:8] - table[:, 2:5] + 1
         want = int(np.prod(ext[mine], axis=1).sum())
     else:

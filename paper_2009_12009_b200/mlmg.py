@@ -267,14 +267,31 @@ class MLMG:
         # other GPUs: a device barrier instead).  Periodic lattice layouts.
         # Measured on one GPU (tools/mb_stream.py, C3 fine level): sweep + push
         # 88.5 us vs sweep 75 us + fill 12 us -- the ghost bytes cost the same
-        # either way in a bandwidth-bound kernel; on two GPUs the pushed solve
-        # measured 8.77 ms vs 8.44 ms with p2p fills (bench.py --ghost-push).
-        # So fills stay the default (ghost_push=True forces the push).
+        # either way in a bandwidth-bound kernel, and the same-GPU j / k faces
+        # are pushed by few edge warps.  ghost_push="remote" pushes only the
+        # faces other GPUs need (coalesced NVLink stores from the CTAs that own
+        # them); the consumer's fill then copies the same-GPU records and is the
+        # device barrier -- no NVLink round trips on its critical path.  Both
+        # push modes end the pushing CTAs with a system-scope fence (remote
+        # stores before the consumer's barrier), which waits behind in-flight
+        # PCIe copies (tools/mb_interfere.py: sweep 97 -> 263 us with the e2e
+        # pipeline's copies running), and on 2 GPUs they measured 8.65 ms
+        # ("remote") and 8.33 ms (True) vs 8.03 ms with p2p fills (bench.py
+        # --ghost-push, tools/r2x.sh).  So the default is the fill.
+        # ghost_push: None / False = fills, True = push everything, "remote".
         self.p2p = self.dist and self.transport.p2p
+        if ghost_push is None:
+            ghost_push = False
+        if ghost_push not in (False, True, "remote"):
+            raise ValueError("ghost_push must be None, False, True or 'remote'")
+        if ghost_push == "remote" and not self.p2p:
+            ghost_push = False  # nothing lives on another GPU
+        self.ghost_push = ghost_push
         for lv in self.levels:
             lv.push = None
             if ghost_push and self.all_periodic:
-                tabs = [push_table(f, lv.domain, self.periodic, 2) for f in lv.phi]
+                tabs = [push_table(f, lv.domain, self.periodic, 2, remote_only=ghost_push == "remote")
+                        for f in lv.phi]
                 if all(t is not None for t in tabs):
                     lv.push = tabs
         # up-leg: prolongation fused into the first post-smoothing sweep
@@ -289,6 +306,7 @@ class MLMG:
             lv.fuse = (fuse_prolong and l < len(self.levels) - 1 and lv.boxlocal_next
                        and self.nu2 >= 1 and self.all_periodic)
         self._ghost = {}  # id(field) -> ghost width known to be current
+        self._partial = set()  # fields whose cross-GPU ghosts were pushed, same-GPU ones stale
         self._pending = False  # pushes to peers since the last device barrier
         self._reads = set()  # fields whose ghosts were read since the last barrier
         top = self.levels[0]
@@ -300,7 +318,10 @@ class MLMG:
         self.r0_dev = torch.zeros(1, dtype=torch.float64, device=top.rhs.device)
         # pinned block shared with the loop's control kernel (csrc/graph.cu):
         # rtol, (max_iter, iters), history
-        self.loop_host = torch.zeros(2 + self._HIST, dtype=torch.float64).pin_memory()
+        # and its device twin the loop works on (nothing inside the loop touches
+        # host memory): rtol, (max_iter, iters), r0, history
+        self.loop_host = torch.zeros(3 + self._HIST, dtype=torch.float64).pin_memory()
+        self.loop_dev = torch.zeros(3 + self._HIST, dtype=torch.float64, device=top.rhs.device)
         self.lag = None  # decided by the first _prime()
         self._loop = None
         self.graph_replays = 0
@@ -320,6 +341,15 @@ class MLMG:
 
     def _need_ghosts(self, lv, fa, width):
         """Before a kernel reads fa's ghosts (width cells)."""
+        if id(fa) in self._partial:
+            # peers pushed the cross-GPU ghosts (to the table's width 2): copy
+            # the same-GPU ones; the launch is also the device barrier
+            fill_boundary(fa, self.transport, lv.domain, self.periodic, ngrow=2, _post_barrier=False,
+                          _local_sources=True)
+            self._partial.discard(id(fa))
+            self._ghost[id(fa)] = 2
+            self._pending = False
+            self._reads.clear()
         if self._ghost.get(id(fa), 0) >= width:
             if self._pending:
                 self._barrier()
@@ -335,8 +365,19 @@ class MLMG:
     def _produced(self, fa, width, pushed_to_peers=False):
         """After a kernel rewrote fa's valid cells; width = ghosts it filled."""
         self._ghost[id(fa)] = width
+        self._partial.discard(id(fa))
         if pushed_to_peers:
             self._pending = True
+
+    def _pushed(self, fa, tab):
+        """After a sweep wrote fa through push table ``tab``."""
+        if tab is None:
+            self._produced(fa, 0)
+        elif self.ghost_push == "remote":
+            self._produced(fa, 0, pushed_to_peers=True)
+            self._partial.add(id(fa))
+        else:
+            self._produced(fa, tab.width, pushed_to_peers=tab.remote)
 
     def _before_push(self, tab, fa):
         """Before a kernel stores into peers' ghosts of fa: no peer may still be
@@ -410,7 +451,7 @@ class MLMG:
             if rc == AMRB_ENOTSUP:
                 raise NotImplementedError("level does not take the streaming sweep")
             check(rc)
-        self._produced(b, 0 if tab is None else 2, pushed_to_peers=tab is not None and tab.remote)
+        self._pushed(b, tab)
         lv.cur = 1 - lv.cur
 
     def _smooth(self, lv, n):
@@ -488,7 +529,7 @@ class MLMG:
         except NotImplementedError:
             lv.fuse = False
             return False
-        self._produced(b, 0 if tab is None else 2, pushed_to_peers=tab is not None and tab.remote)
+        self._pushed(b, tab)
         lv.cur = 1 - lv.cur
         return True
 
@@ -675,7 +716,7 @@ class MLMG:
                 self._body()
                 check(lib().amrb_loop_control(loop, C.c_void_p(self.norm.data_ptr()),
                                               C.c_void_p(self.r0_dev.data_ptr()),
-                                              C.c_void_p(self.loop_host.data_ptr()), self._HIST, stream_ptr()))
+                                              C.c_void_p(self.loop_dev.data_ptr()), self._HIST, stream_ptr()))
                 self.launches_per_cycle = int(lib().amrb_launch_count()) - l0  # incl. the control kernel
             except BaseException:
                 lib().amrb_loop_destroy(loop)
@@ -744,20 +785,18 @@ class MLMG:
         if self._loop is not None:
             for lv, c in zip(self.levels, self._loop_cur):
                 lv.cur = c
-            h = self.loop_host
-            h[0] = float(rtol)
-            hi = h.view(torch.int32)
-            hi[2] = max_iter
-            hi[3] = 0
+            check(lib().amrb_loop_reset(C.c_void_p(self.loop_dev.data_ptr()), float(rtol), max_iter,
+                                        C.c_void_p(self.r0_dev.data_ptr()), stream_ptr()))
             check(lib().amrb_loop_launch(self._loop, stream_ptr()))
             self.graph_replays += 1
-            check(lib().amrb_store_host(C.c_void_p(self.r0_dev.data_ptr()), C.c_void_p(self.norm_host.data_ptr()),
-                                        1, stream_ptr()))
+            h = self.loop_host
+            check(lib().amrb_store_host(C.c_void_p(self.loop_dev.data_ptr()), C.c_void_p(h.data_ptr()),
+                                        3 + max_iter, stream_ptr()))
             torch.cuda.current_stream().synchronize()
             self._check_faults()
-            self.r0 = float(self.norm_host[0])
-            self.iterations = int(hi[3])
-            self.history = [float(x) for x in h[2:2 + self.iterations].tolist()]
+            self.r0 = float(h[2])
+            self.iterations = int(h.view(torch.int32)[3])
+            self.history = [float(x) for x in h[3:3 + self.iterations].tolist()]
             rn = self.history[-1]
         else:
             self.r0 = r0 = self._host_scalar(self.r0_dev)

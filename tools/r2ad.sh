@@ -1,0 +1,7 @@
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29594 tools/mb_interfere.py 2>&1 | grep -E "world=|Error" | head -30
+for n in 2 4; do
+cmd="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2959$n"
+timeout 900 $cmd bench.py --gpus $n --steps 10 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/r2ad_bench$n.json 2> gpurun_out/r2ad_bench$n.err; echo "bench $n rc=$?"
+python -c "
+import json; d=json.loads(open('gpurun_out/r2ad_bench$n.json').read().strip().splitlines()[-1]); e=d['e2e']; print('$n solve ms', d['ms_per_step'], 'e2e ms', e['ms_per_step'], 'serial', e['serial']['ms_per_step'], e['bounds'])"
+done

@@ -1,0 +1,7 @@
+for rep in 1 2; do
+for gp in auto off on; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 bench.py --gpus 2 --steps 20 --warmup 3 --no-cpu-baseline --no-other-configs --ghost-push $gp > gpurun_out/r2x_bench2_$gp.json 2> gpurun_out/r2x_bench2_$gp.err; echo "bench $gp rc=$?"
+python -c "
+import json; d=json.loads(open('gpurun_out/r2x_bench2_$gp.json').read().strip().splitlines()[-1]); print('$gp solve ms', d['ms_per_step'], 'e2e ms', d['e2e']['ms_per_step'], 'iters', d['config']['iterations'][:2])"
+done
+done
