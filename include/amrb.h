@@ -291,6 +291,22 @@ int amrb_gsrb_sweep_norm(const amrb_level* lv, const amrb_field* a, const double
                          const int32_t* fixed_lohi, uint64_t* norm, const uint64_t* push,
                          void* stream);
 
+/* amrb_gsrb_sweep (norm == NULL) / amrb_gsrb_sweep_norm with FillBoundary
+ * fused in: every CTA first copies the width-2 ghost cells of its input
+ * footprint through `pull` (27 entries per box, ghosts.pull_table: the source
+ * address of ghost cell (0, 0, 0) of each direction's slab, bit 0 set when the
+ * source box is on another GPU; 0 = not filled, e.g. a non-periodic side), so
+ * a's ghosts need not be current and are current afterwards.  nranks > 1: the
+ * launch is also the device barrier of amrb_prog_run_p2p_sync (same pads and
+ * epoch): CTA 0 publishes, the CTAs that read another GPU's cells (and CTA 0)
+ * wait for every peer -- the rest start at once.  Periodic levels only (no
+ * fixed cells). */
+int amrb_gsrb_sweep_pull(const amrb_level* lv, const amrb_field* a, double* a_base,
+                         amrb_field* b, double* b_base, const amrb_field* rhs,
+                         const double* rhs_base, const double dh[3], const uint64_t* pull,
+                         const uint64_t* pad_ptrs, int rank, int nranks, uint32_t* epoch,
+                         uint64_t* norm, void* stream);
+
 /* Prolongation fused into the first post-smoothing sweep of the V-cycle up-leg:
  * b = GSRB(a + P(c)), P = piecewise-constant interpolation of the coarse
  * correction c (interp_to_fine(..., "pc"), coarse_fine.py:166-185, then

@@ -87,6 +87,7 @@ _SIGS = {
     "amrb_gsrb_color": (C.c_int, [vp, vp, vp, vp, vp, P(f64), C.c_int, vp]),
     "amrb_gsrb_sweep": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, vp]),
     "amrb_gsrb_sweep_norm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), P(i32), vp, vp, vp]),
+    "amrb_gsrb_sweep_pull": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp, vp, C.c_int, C.c_int, vp, vp, vp]),
     "amrb_gsrb_sweep_prolong": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp, vp, vp, vp, vp]),
     "amrb_restrict": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, P(i32), C.c_int, vp]),
     "amrb_residual_restrict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(f64), vp]),

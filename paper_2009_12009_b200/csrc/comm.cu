@@ -26,8 +26,21 @@
 #include <memory>
 
 #include "device.h"
+#include "peer.cuh"
 
 namespace amrb {
+
+unsigned long long* g_fault_box = nullptr;  // amrb_set_fault_mailbox
+unsigned long long* g_fault_dev = nullptr;
+
+Fault current_fault() {
+  Fault f;
+  f.box = g_fault_box;
+  f.dev = g_fault_box ? g_fault_dev : nullptr;
+  const int64_t ms = option("peer_timeout_ms");
+  f.timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
+  return f;
+}
 
 namespace {
 
@@ -53,82 +66,7 @@ struct PeerPtrs {
 
 // Device barrier fused into a p2p copy launch (see k_copy): pads[r] = rank r's
 // signal pad, epoch = {this rank's barrier epoch, CTA completion ticket}.
-// Failure detection for the NVLink signalling (transport.py:20-24,37-38: a
-// failed message raises TransportError(src, dst, why)).  Every device-side
-// wait for a peer is bounded: after `timeout_ns` of %globaltimer the waiting
-// lane records (code, waiting rank, missing peer, epoch) in the fault mailbox
-// -- pinned host memory the Transport registered -- and gives up; once a fault
-// is recorded every later wait returns at once, so a dead peer costs one
-// timeout, not one per barrier.  The host raises TransportError from the
-// mailbox after its next synchronisation (Transport.check_faults).
-struct Fault {
-  unsigned long long* box;  // [0] code (0 none, 1 peer wait timed out), [1] rank, [2] peer, [3] epoch
-  unsigned long long* dev;  // device twin of box[0]: what the waits poll (never host memory, see signal_store)
-  unsigned long long timeout_ns;
-};
 
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Cross-GPU signals.  Every exchange here is a PULL: what a peer reads after
-// a signal lives in the signalling GPU's own HBM, written by earlier kernels,
-// and the owner's L2 serves the peer's NVLink loads -- so a gpu-scope release
-// fence orders it before the signal store, and the waiting side needs a
-// gpu-scope acquire fence after it sees the signal.  No system-scope fence:
-// fence.sc.sys / MEMBAR.SYS also drains this GPU's outstanding PCIe traffic,
-// and with bulk host copies in flight on side streams (the e2e pipeline) one
-// barrier measured 200 us instead of 6 (tools/mb_interfere.py, 4 GPUs).
-__device__ __forceinline__ void signal_store(uint32_t* slot, uint32_t v) {
-  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-  asm volatile("st.relaxed.sys.global.u32 [%0], %1;\n" ::"l"(slot), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void record_fault(const Fault& f, int rank, int peer, uint32_t target) {
-  if (f.dev && atomicCAS(f.dev, 0ull, 1ull) == 0ull && f.box) {
-    f.box[1] = (unsigned long long)rank;
-    f.box[2] = (unsigned long long)peer;
-    f.box[3] = (unsigned long long)target;
-    __threadfence_system();  // failure path only
-    f.box[0] = 1ull;
-  }
-}
-
-__device__ __forceinline__ bool faulted(const Fault& f) {
-  return f.dev && *reinterpret_cast<volatile unsigned long long*>(f.dev) != 0;
-}
-
-// spin until *pad (wrap-safe) reaches `target`; false (and a fault recorded) on timeout
-__device__ bool peer_wait(const uint32_t* pad, uint32_t target, int rank, int peer, const Fault& f) {
-  if (faulted(f)) return false;
-  const unsigned long long t0 = global_ns();
-  for (unsigned it = 0;; ++it) {
-    uint32_t x;
-    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];\n" : "=r"(x) : "l"(pad) : "memory");
-    if ((int32_t)(x - target) >= 0) {
-      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-      return true;
-    }
-    if ((it & 255) == 255 && f.timeout_ns && global_ns() - t0 > f.timeout_ns) {
-      record_fault(f, rank, peer, target);
-      return false;
-    }
-  }
-}
-
-unsigned long long* g_fault_box = nullptr;  // amrb_set_fault_mailbox
-unsigned long long* g_fault_dev = nullptr;
-
-Fault current_fault() {
-  Fault f;
-  f.box = g_fault_box;
-  f.dev = g_fault_box ? g_fault_dev : nullptr;
-  const int64_t ms = option("peer_timeout_ms");
-  f.timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
-  return f;
-}
 
 struct SyncArgs {
   uint32_t* pads[kMaxPeers];
@@ -508,7 +446,21 @@ extern "C" int amrb_prog_create(const amrb_plan* plan_, int ncomp, const int64_t
       }
       return d;
     };
-    if (op == 0) {
+    if (op == 0 && p2p) {
+      // one wave: a copy's records never share a destination cell, and in
+      // the pull model nothing waits for a receive buffer -- the CTAs reading
+      // a peer wait for the fused barrier while the local ones run (k_copy).
+      // Peer records first, so their CTAs are scheduled (and start waiting)
+      // first.
+      auto* w = new Wave;
+      g->apply.push_back(w);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int64_t r : mine)
+          if ((sr[r] == dr[r]) == (pass == 1)) w->host.push_back(make_apply(r));
+      for (int64_t r : mine)
+        if (sr[r] == dr[r]) g->local_records++;
+      g->local_waves = 0;
+    } else if (op == 0) {
       auto* local = new Wave;
       auto* remote = new Wave;
       g->apply.push_back(local);

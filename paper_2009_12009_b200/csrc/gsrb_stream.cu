@@ -41,6 +41,7 @@
 #include <type_traits>
 
 #include "tma.cuh"
+#include "peer.cuh"
 
 namespace amrb {
 
@@ -137,6 +138,21 @@ struct StreamArgs {
   // the ghost copy of output cell (i, j, k) of box b toward direction
   // (dx, dy, dz) is at push[27 b + 9 (dx+1) + 3 (dy+1) + (dz+1)] + i s0 + j s1 + k
   const long long* push;
+  // in-kernel ghost pull (ghosts.pull_table): per box 27 source addresses (0:
+  // none; bit 0 set: the source box is on another GPU); the INPUT's ghost cell
+  // (i, j, k) (box-local, inside direction d's width-2 slab) is copied from
+  // (pull[27 b + d] & ~1) + i s0 + j s1 + k (elements, the input's strides)
+  // before the CTA's first TMA load -- the copy-program fill disappears.  The
+  // CTAs whose footprint reaches a remote slab (and CTA 0) first wait for
+  // every peer to reach this launch: k_copy's fused device barrier, same pads
+  // and epoch (comm.cu).
+  const long long* pull;
+  double* a;          // the input's allocation (ghost destinations)
+  const FabView* fa;  // the input's views
+  uint32_t* pads[kMaxPeers];
+  uint32_t* epoch;
+  int rank, nranks;
+  Fault fault;
 };
 
 constexpr int r128(int x) { return (x + 127) / 128 * 128; }
@@ -154,7 +170,7 @@ struct StreamLayout {
   static constexpr int COFF = ROFF + r128(RB);
   static constexpr int SLOT = COFF + (MODE == kModeProl ? r128(CB) : 0);
   static constexpr int BAR = NS * SLOT;
-  static constexpr int PTAB = BAR + 8 * NS;  // PUSH: this box's 27 destination addresses
+  static constexpr int PTAB = BAR + 8 * NS;  // PUSH / PULL: this box's 27 table entries
   static constexpr int BYTES = PTAB + 8 * 27;
   // lanes per tile row: 32 k-pairs per warp for TK >= 64 (WK warps across k),
   // else TK/2 lanes per row and RPW = 32 / LK row groups per warp
@@ -171,7 +187,96 @@ __host__ __device__ constexpr int stream_warps() {
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double x, double y) { *reinterpret_cast<double2*>(p) = make_double2(x, y); }
 
-template <int TJ, int TK, int RW, int D, int MODE, int MINB, bool PUSH>
+// x / d for 0 <= x < 2^22 through a float reciprocal (off by at most one,
+// corrected): the pull's index math without the ~20-instruction integer
+// division chain per cell
+__device__ __forceinline__ int quick_div(int x, int d, float rcp) {
+  int q = __float2int_rz(__int2float_rz(x) * rcp);
+  const int r = x - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
+// In-kernel ghost pull of one CTA's input footprint (planes fi0..fi1, rows
+// fj0..fj1, cols fk0..fk1, box-local; see StreamArgs::pull).  Every CTA whose
+// footprint holds a ghost cell copies that cell itself, so a CTA's TMA only
+// ever reads ghost values it (or a neighbour, with the same value) wrote.
+template <int NT>
+__device__ __forceinline__ void pull_ghosts(const StreamArgs& args, long long* tab, int box, const BoxGeom& g, int fi0,
+                                            int fi1, int fj0, int fj1, int fk0, int fk1) {
+  const int tid = threadIdx.x;
+  if (tid < 27) tab[tid] = args.pull[27 * box + tid];
+  __syncthreads();
+  const int flo[3] = {fi0, fj0, fk0}, fhi[3] = {fi1, fj1, fk1};
+  // the footprint's part of direction d's ghost slab (width 2)
+  auto part = [&](int d, int lo[3], int hi[3]) {
+    const int dd[3] = {d / 9 - 1, (d / 3) % 3 - 1, d % 3 - 1};
+    bool any = true;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int slo = dd[ax] < 0 ? -2 : (dd[ax] > 0 ? g.n[ax] : 0);
+      const int shi = dd[ax] < 0 ? -1 : (dd[ax] > 0 ? g.n[ax] + 1 : g.n[ax] - 1);
+      lo[ax] = max(flo[ax], slo);
+      hi[ax] = min(fhi[ax], shi);
+      any &= lo[ax] <= hi[ax];
+    }
+    return any;
+  };
+  if (args.nranks > 1) {
+    const uint32_t ep = *reinterpret_cast<volatile uint32_t*>(args.epoch) + 1;
+    if (tid < 32) {
+      bool wait = blockIdx.x == 0;
+      int lo[3], hi[3];
+      for (int d = 0; d < 27 && !wait; ++d)
+        if (d != 13 && (tab[d] & 1)) wait = part(d, lo, hi);
+      const int p = tid;
+      if (p < args.nranks && p != args.rank) {
+        if (blockIdx.x == 0) signal_store(args.pads[p] + args.rank, ep);
+        if (wait) peer_wait(args.pads[args.rank] + p, ep, args.rank, p, args.fault);
+      }
+      // every CTA has read the old epoch once all have taken a ticket
+      if (tid == 0 && atomicAdd(args.epoch + 1, 1u) == gridDim.x - 1) {
+        args.epoch[0] = ep;
+        args.epoch[1] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  const FabView A = args.fa[box];
+  double* dst = args.a + A.off;
+  for (int d = 0; d < 27; ++d) {
+    const long long e = tab[d];
+    int lo[3], hi[3];
+    if (d == 13 || !e || !part(d, lo, hi)) continue;
+    const int e1 = hi[1] - lo[1] + 1, e2 = hi[2] - lo[2] + 1;
+    const int total = (hi[0] - lo[0] + 1) * e1 * e2;
+    const float r1 = 1.0f / (float)e1, r2 = 1.0f / (float)e2;
+    const double* src = reinterpret_cast<const double*>(e & ~1ll);
+    constexpr int U = 16;  // loads in flight per thread (NVLink latency)
+    for (int base = 0; base < total; base += U * NT) {
+      double v[U];
+      int64_t o[U];  // box-local offsets: negative for the low ghost slabs
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = base + u * NT + tid;
+        if (x < total) {
+          const int r = quick_div(x, e2, r2), i = quick_div(r, e1, r1);
+          const int k = x - r * e2, j = r - i * e1;
+          o[u] = (int64_t)(lo[0] + i) * A.s0 + (int64_t)(lo[1] + j) * A.s1 + (lo[2] + k);
+          v[u] = src[o[u]];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * NT + tid < total) dst[o[u]] = v[u];
+    }
+  }
+  // generic-proxy stores before this CTA's TMA (async proxy) reads of them
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// XCH: 0 = plain, 1 = ghost push (args.push), 2 = ghost pull (args.pull)
+template <int TJ, int TK, int RW, int D, int MODE, int MINB, int XCH>
 __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     k_gsrb_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ StreamArgs args) {
@@ -181,6 +286,7 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
   constexpr int WK = LY::WK, LK = LY::LK, RPW = LY::RPW, NS = LY::NS, PK = LY::PK, CK = LY::CK;
   constexpr int NSW = TJ / (RW * RPW) * WK;  // strip warps (then WK ring warps)
   constexpr bool PROL = MODE == kModeProl, NORM = MODE == kModeNorm;
+  constexpr bool PUSH = XCH == 1, PULL = XCH == 2;
   static_assert((TK % 64 == 0 || TK == 32) && TJ % (RW * RPW) == 0 && RW % 2 == 0 && TJ + 2 <= 32, "tile shape");
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + LY::BAR);
@@ -234,6 +340,8 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
     fence_barrier_init();
   }
   if (PUSH && tid < 27) reinterpret_cast<long long*>(sm + LY::PTAB)[tid] = args.push[27 * box + tid];
+  if (PULL) pull_ghosts<32 * stream_warps<TJ, TK, RW>()>(args, reinterpret_cast<long long*>(sm + LY::PTAB), box, g,
+                                                         i0 - 2, i1 + 1, j0 - 2, j0 + TJ + 1, k0 - 2, k0 + TK + 1);
   __syncthreads();
   if (tid == producer)
     for (int q = -2; q <= min(NS - 3, L + 1); ++q) issue(q);
@@ -710,11 +818,11 @@ const SegTable& seg_table(Level& lv, int tj, int tk, int nseg, bool alternate, b
   return *t;
 }
 
-template <int TJ, int TK, int RW, int D, int MODE, int MINB, bool PUSH>
+template <int TJ, int TK, int RW, int D, int MODE, int MINB, int XCH>
 bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
                    const double* r_base, const Coef& cf, const int flo[3], const int fhi[3], cudaStream_t st,
                    const Level* clv, const Field* c, const double* c_base, unsigned long long* norm,
-                   const long long* push) {
+                   const long long* push, const StreamPull* pull) {
   using LY = StreamLayout<TJ, TK, D, MODE>;
   constexpr int NW = stream_warps<TJ, TK, RW>();
   int nres = 0;
@@ -753,7 +861,7 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
   } else {
     mc = ma;
   }
-  auto kern = k_gsrb_stream<TJ, TK, RW, D, MODE, MINB, PUSH>;
+  auto kern = k_gsrb_stream<TJ, TK, RW, D, MODE, MINB, XCH>;
   static int per_sm = 0;
   if (!per_sm) {
     AMRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::BYTES));
@@ -792,6 +900,16 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
   }
   args.norm = norm;
   args.push = push;
+  if (XCH == 2) {
+    args.pull = pull->tab;
+    args.a = const_cast<double*>(a_base);
+    args.fa = a.dev.p;
+    for (int x = 0; x < pull->nranks; ++x) args.pads[x] = pull->pads[x];
+    args.epoch = pull->epoch;
+    args.rank = pull->rank;
+    args.nranks = pull->nranks;
+    args.fault = pull->nranks > 1 ? current_fault() : Fault{};
+  }
   launch_k(kern, (unsigned)t.n, 32 * NW, LY::BYTES, st, ma, mr, mc, args);
   check_launch("k_gsrb_stream");
   return true;
@@ -876,15 +994,33 @@ unsigned int* debug_check_words() {
 }
 
 // mode 0: plain, 1: PROL (clv/c/c_base), 2: NORM (norm)
+template <int TJ, int TK, int RW, int D, int M, int B>
+bool dispatch_stream(Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base, const Field& r,
+                     const double* r_base, const Coef& cf, const int flo[3], const int fhi[3], cudaStream_t st,
+                     const Level* clv, const Field* c, const double* c_base, unsigned long long* norm,
+                     const long long* push, const StreamPull* pull) {
+  if (push)
+    return launch_stream<TJ, TK, RW, D, M, B, 1>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, c_base,
+                                                 norm, push, pull);
+  if (pull) {
+    if constexpr (M == kModeProl) {
+      return false;  // the up-leg input's ghosts come from the restriction's fill
+    } else {
+      return launch_stream<TJ, TK, RW, D, M, B, 2>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c,
+                                                   c_base, norm, push, pull);
+    }
+  }
+  return launch_stream<TJ, TK, RW, D, M, B, 0>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, c_base,
+                                               norm, push, pull);
+}
+
 bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                          const Field& r, const double* r_base, const Coef& cf, const int flo[3], const int fhi[3],
                          cudaStream_t st, const Level* clv, const Field* c, const double* c_base,
-                         unsigned long long* norm, const long long* push) {
-#define AMRB_STREAM(TJ, TK, RW, D, M, B)                                                                     \
-  (push ? launch_stream<TJ, TK, RW, D, M, B, true>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, \
-                                                    c_base, norm, push)                                          \
-        : launch_stream<TJ, TK, RW, D, M, B, false>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, \
-                                                     c_base, norm, push))
+                         unsigned long long* norm, const long long* push, const StreamPull* pull) {
+#define AMRB_STREAM(TJ, TK, RW, D, M, B)                                                                            \
+  dispatch_stream<TJ, TK, RW, D, M, B>(lv, a, a_base, b, b_base, r, r_base, cf, flo, fhi, st, clv, c, c_base, norm, \
+                                       push, pull)
   // variants (library option "stream_config" forces one; measured on the C3 fine
   // level, tools/mb_stream.py): 1 = 16x64 tiles, 4-row strips (the fastest plain
   // sweep); 2 = 16x64, 2-row strips (two CTAs/SM even with the ghost push);

@@ -1240,6 +1240,34 @@ extern "C" int amrb_gsrb_sweep_norm(const amrb_level* lv_, const amrb_field* a, 
   });
 }
 
+extern "C" int amrb_gsrb_sweep_pull(const amrb_level* lv_, const amrb_field* a, double* a_base, amrb_field* b,
+                                    double* b_base, const amrb_field* rhs, const double* rhs_base, const double dh[3],
+                                    const uint64_t* pull, const uint64_t* pad_ptrs, int rank, int nranks,
+                                    uint32_t* epoch, uint64_t* norm, void* stream) {
+  return guarded([&] {
+    Level& lv = Lm(lv_);
+    need_ghost(F(a), 2, "gsrb_sweep_pull (phi in)");
+    need_ghost(F(rhs), 1, "gsrb_sweep_pull (rhs)");
+    for (auto* f : {a, (const amrb_field*)b, rhs}) need_same_level(F(f), lv, "gsrb_sweep_pull");
+    if (!pull) throw Error(AMRB_EINVAL, "gsrb_sweep_pull: null pull table");
+    if (nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks || (nranks > 1 && (!pad_ptrs || !epoch)))
+      throw Error(AMRB_EINVAL, "gsrb_sweep_pull: bad peer arguments");
+    if (!lv.all_even()) throw Error(AMRB_EINVAL, "gsrb_sweep needs even box extents");
+    StreamPull pl;
+    pl.tab = reinterpret_cast<const long long*>(pull);
+    pl.rank = rank;
+    pl.nranks = nranks;
+    pl.epoch = epoch;
+    for (int r = 0; r < nranks && pad_ptrs; ++r) pl.pads[r] = reinterpret_cast<uint32_t*>(pad_ptrs[r]);
+    const int flo[3] = {-(1 << 30), -(1 << 30), -(1 << 30)}, fhi[3] = {1 << 30, 1 << 30, 1 << 30};
+    if (option("sweep_kernel") != 0 ||
+        !launch_sweep_stream(norm ? 2 : 0, lv, F(a), a_base, F(b), b_base, F(rhs), rhs_base, make_coef(dh), flo, fhi,
+                             (cudaStream_t)stream, nullptr, nullptr, nullptr,
+                             reinterpret_cast<unsigned long long*>(norm), nullptr, &pl))
+      throw Error(AMRB_ENOTSUP, "gsrb_sweep_pull: level does not take the k_gsrb_stream path");
+  });
+}
+
 extern "C" int amrb_gsrb_sweep_prolong(const amrb_level* lv_, const amrb_field* a, const double* a_base,
                                           amrb_field* b, double* b_base, const amrb_field* rhs, const double* rhs_base,
                                           const double dh[3], const amrb_level* clv_, const amrb_field* c,

@@ -52,10 +52,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 bool launch_resid_restrict_stream(Level& lv, const Field& phi, const double* phi_base, const Field& rhs,
                                   const double* rhs_base, const Field& crse, double* crse_base, const Coef& cf,
                                   cudaStream_t st);
+// in-kernel ghost pull of the input (modes 0 and 2): table + device barrier
+struct StreamPull {
+  const long long* tab;  // 27 per box (ghosts.pull_table)
+  uint32_t* pads[kMaxPeers];
+  uint32_t* epoch;
+  int rank = 0, nranks = 1;
+};
 bool launch_sweep_stream(int mode, Level& lv, const Field& a, const double* a_base, const Field& b, double* b_base,
                          const Field& r, const double* r_base, const Coef& cf, const int flo[3], const int fhi[3],
                          cudaStream_t st, const Level* clv, const Field* c, const double* c_base,
-                         unsigned long long* norm, const long long* push = nullptr);
+                         unsigned long long* norm, const long long* push = nullptr,
+                         const StreamPull* pull = nullptr);
 
 
 }  // namespace amrb

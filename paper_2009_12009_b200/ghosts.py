@@ -43,7 +43,7 @@ import torch
 from .multifab import world_size
 from .plans import build_plan_fill_boundary, normalize_periodic
 
-__all__ = ["PushTable", "push_table"]
+__all__ = ["PushTable", "push_table", "pull_table"]
 
 DIRECTIONS = [d for d in itertools.product((-1, 0, 1), repeat=3) if d != (0, 0, 0)]
 
@@ -94,7 +94,26 @@ def push_table(fa, domain, periodic, width=2, remote_only=False):
     return tab
 
 
-def _build(fa, domain, periodic, width, remote_only=False):
+def pull_table(fa, domain, periodic, width=2):
+    """The pull table of FabArray ``fa`` (csrc/gsrb_stream.cu StreamArgs::pull),
+    cached on ``fa``; None if unsupported.
+
+    tab[b, (dx+1)*9 + (dy+1)*3 + (dz+1)] = Q | remote  such that box b's ghost
+    cell (i, j, k) (box-local, inside direction (dx, dy, dz)'s width-``width``
+    slab) is a copy of the valid cell at  Q + 8*(i*s0 + j*s1 + k)  -- the same
+    cells the fill plan copies into b's ghosts, read by the sweep itself.  Bit 0
+    marks a source box on another GPU.
+    """
+    periodic = normalize_periodic(periodic, fa.dim)
+    key = ("pull", width, tuple(domain.lo), tuple(domain.hi), periodic)
+    if key in fa._native:
+        return fa._native[key]
+    tab = _build(fa, domain, periodic, width, pull=True)
+    fa._native[key] = tab
+    return tab
+
+
+def _build(fa, domain, periodic, width, remote_only=False, pull=False):
     if fa.dim != 3 or fa.ncomp != 1 or fa.ngrow < width or width < 1:
         return None
     ba = fa.ba
@@ -131,6 +150,35 @@ def _build(fa, domain, periodic, width, remote_only=False):
         if int(fa.fabtab[b][2]) != s0 or int(fa.fabtab[b][3]) != s1:
             return None
         B = ba[b]
+        if pull:
+            for d in DIRECTIONS:
+                probe = tuple(B.lo[a] - 1 if d[a] < 0 else (B.hi[a] + 1 if d[a] > 0 else B.lo[a]) for a in range(3))
+                img = _wrap(probe, domain, periodic)
+                if img is None:
+                    continue  # boundary-condition ghosts: not filled
+                nb = ba.owner_at(img)
+                if nb is None:
+                    return None
+                N = ba[nb]
+                if int(gtab[nb][2]) != s0 or int(gtab[nb][3]) != s1:
+                    return None
+                t = tuple(img[a] - probe[a] for a in range(3))
+                # B's ghost slab toward d, shifted, must be N's valid cells
+                g_lo = [B.lo[a] - width if d[a] < 0 else (B.hi[a] + 1 if d[a] > 0 else B.lo[a]) for a in range(3)]
+                g_hi = [B.lo[a] - 1 if d[a] < 0 else (B.hi[a] + width if d[a] > 0 else B.hi[a]) for a in range(3)]
+                for a in range(3):
+                    lo_t, hi_t = g_lo[a] + t[a], g_hi[a] + t[a]
+                    if lo_t < N.lo[a] or hi_t > N.hi[a]:
+                        return None
+                    if d[a] == 0 and (lo_t != N.lo[a] or hi_t != N.hi[a]):
+                        return None
+                covered += int(np.prod([h - l + 1 for l, h in zip(g_lo, g_hi)]))
+                rel = [B.lo[a] + t[a] - N.lo[a] for a in range(3)]
+                off = origin(nb) + rel[0] * s0 + rel[1] * s1 + rel[2]
+                far = owner[nb] != me
+                host[b, (d[0] + 1) * 9 + (d[1] + 1) * 3 + (d[2] + 1)] = (bases[owner[nb]] + 8 * off) | int(far)
+                remote |= far
+            continue
         for d in DIRECTIONS:
             # the first cell beyond B's d-face (inside B along axes with d = 0)
             probe = tuple(B.lo[a] - 1 if d[a] < 0 else (B.hi[a] + 1 if d[a] > 0 else B.lo[a]) for a in range(3))
@@ -168,7 +216,8 @@ def _build(fa, domain, periodic, width, remote_only=False):
     if dist or n != int(np.count_nonzero(fa.resident)):
         table = plan.table()
         res = np.asarray(fa.resident)
-        mine = res[table[:, 0]]  # records whose SOURCE box is resident here
+        # push: records whose SOURCE box is resident here; pull: DESTINATION
+        mine = res[table[:, 1 if pull else 0]]
         if remote_only:
             mine &= np.asarray(owner)[table[:, 1]] != me
         ext = table[:, 5:8] - table[:, 2:5] + 1

@@ -38,7 +38,7 @@ from .device import dh_array, field_of, level_of, stream_ptr
 from .geometry import BoundaryRecord, Geometry, apply_domain_boundary
 from .interlevel import coarsened_layout, prolong_from
 from .layout import BoxArray, DistributionMapping
-from .ghosts import push_table
+from .ghosts import pull_table, push_table
 from .stencil import gsrb_sweep_prolong
 from .multifab import FabArray, MultiFab, world_size
 
@@ -136,7 +136,7 @@ class MLMG:
 
     def __init__(self, geom, ba, dm, transport=None, nu1=2, nu2=2, bottom_sweeps=32, use_graph=True,
                  ghost_push=None, agg_cells=128**3, fuse_prolong=None, cluster_tail=None,
-                 grid_level_cells=None, bc=None):
+                 grid_level_cells=None, bc=None, ghost_pull=None):
         if geom.dim != 3:
             raise ValueError("MLMG is implemented for 3-D domains")
         # boundary conditions: 'periodic' dimensions, or 'external' sides (a
@@ -294,6 +294,27 @@ class MLMG:
                         for f in lv.phi]
                 if all(t is not None for t in tabs):
                     lv.push = tabs
+        # ghost pull (ghosts.pull_table, csrc/gsrb_stream.cu): a sweep whose
+        # input's ghosts are stale copies them itself -- every CTA the ghost
+        # cells of its own footprint, before its first TMA load -- instead of
+        # a copy-program fill launched before it; across GPUs the launch is
+        # also the fill's device barrier, and only the CTAs that read another
+        # GPU's cells wait for it.  The fill's launch, its barrier wait and its
+        # NVLink round trips leave the critical path of the other CTAs.
+        # Measured slower than the fills it replaces (tools/mb_pull2.py, C3 fine
+        # level: sweep 75 us, fill + sweep 85 us, pull sweep 132 us; the edge
+        # CTAs' copies run at loaded-HBM latency on their critical path while
+        # every other CTA streams), so it is opt-in.
+        # ghost_pull: None / False = fills, True = pull.
+        if ghost_pull is None:
+            ghost_pull = False
+        self.ghost_pull = bool(ghost_pull) and not ghost_push
+        for lv in self.levels:
+            lv.pull = None
+            if self.ghost_pull and self.all_periodic:
+                tabs = [pull_table(f, lv.domain, self.periodic, 2) for f in lv.phi]
+                if all(t is not None for t in tabs):
+                    lv.pull = tabs
         # up-leg: prolongation fused into the first post-smoothing sweep
         # (k_gsrb_sweep5<PROL>, box-local level pairs): no separate read+write
         # pass over the fine phi and no fill after it; the restriction fills the
@@ -422,6 +443,9 @@ class MLMG:
         level does not take the streaming kernel)."""
         a = lv.phi[lv.cur]
         b = lv.phi[1 - lv.cur]
+        if lv.pull is not None and id(a) not in self._partial and self._ghost.get(id(a), 0) < 2:
+            if self._sweep_pull(lv, a, b, norm):
+                return
         self._need_ghosts(lv, a, 2)
         self._need_ghosts(lv, lv.rhs, 1)
         tab = self._push_for(lv, b)
@@ -453,6 +477,44 @@ class MLMG:
             check(rc)
         self._pushed(b, tab)
         lv.cur = 1 - lv.cur
+
+    def _sweep_pull(self, lv, a, b, norm):
+        """_sweep with the input's ghost fill done by the sweep itself
+        (amrb_gsrb_sweep_pull); False (nothing launched) where the level does
+        not take the streaming kernel."""
+        self._need_ghosts(lv, lv.rhs, 1)
+        tab = lv.pull[0] if a is lv.phi[0] else lv.pull[1]
+        tr = self.transport
+        peers = self.p2p
+        rc = lib().amrb_gsrb_sweep_pull(
+            level_of(a).handle,
+            field_of(a).handle,
+            C.c_void_p(a.storage.data_ptr()),
+            field_of(b).handle,
+            C.c_void_p(b.storage.data_ptr()),
+            field_of(lv.rhs).handle,
+            C.c_void_p(lv.rhs.storage.data_ptr()),
+            lv.dhc,
+            C.c_void_p(tab.ptr),
+            tr._pads.ctypes.data_as(C.POINTER(C.c_uint64)) if peers else None,
+            tr.rank if peers else 0,
+            tr.nranks if peers else 1,
+            C.c_void_p(tr._epoch.data_ptr()) if peers else None,
+            None if norm is None else C.c_void_p(norm.data_ptr()),
+            stream_ptr(),
+        )
+        if rc == AMRB_ENOTSUP:
+            lv.pull = None
+            return False
+        check(rc)
+        self._ghost[id(a)] = 2  # every ghost cell of a was copied by some CTA
+        if peers:  # the launch was the device barrier
+            self._pending = False
+            self._reads.clear()
+            self._reads.add(id(a))
+        self._produced(b, 0)
+        lv.cur = 1 - lv.cur
+        return True
 
     def _smooth(self, lv, n):
         for _ in range(n):

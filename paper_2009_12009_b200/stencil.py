@@ -114,6 +114,30 @@ def gsrb_sweep_norm(a, b, rhs, dh, norm, fixed=None, push=None):
     check(rc)
 
 
+def gsrb_sweep_pull(a, b, rhs, dh, table, norm=None, transport=None):
+    """gsrb_sweep (norm None) / gsrb_sweep_norm with a's width-2 ghost fill
+    done inside the sweep through ``table`` (ghosts.pull_table(a, ...)): a's
+    ghosts need not be current before and are after -- the same cells as
+    fill_boundary(a, ngrow=2) followed by the sweep.  With a p2p ``transport``
+    the launch is also the device barrier of a p2p fill.  Raises
+    NotImplementedError (nothing launched) when the level does not take the
+    streaming sweep path."""
+    _same_layout(a, b, rhs)
+    if table is None:
+        raise ValueError("gsrb_sweep_pull needs a pull table (ghosts.pull_table)")
+    peers = transport is not None and transport.nranks > 1 and getattr(transport, "p2p", False)
+    rc = lib().amrb_gsrb_sweep_pull(
+        level_of(a).handle, field_of(a).handle, _p(a), field_of(b).handle, _p(b), field_of(rhs).handle, _p(rhs),
+        dh_array(dh), C.c_void_p(table.ptr),
+        transport._pads.ctypes.data_as(C.POINTER(C.c_uint64)) if peers else None,
+        transport.rank if peers else 0, transport.nranks if peers else 1,
+        C.c_void_p(transport._epoch.data_ptr()) if peers else None,
+        None if norm is None else C.c_void_p(norm.data_ptr()), stream_ptr())
+    if rc == AMRB_ENOTSUP:
+        raise NotImplementedError("gsrb_sweep_pull: level does not take the streaming sweep path")
+    check(rc)
+
+
 def gsrb_sweep_prolong(a, b, rhs, dh, crse, push=None):
     """b = one fused red+black sweep of (a + pc-interpolated crse), periodic;
     crse on the box-local coarsened layout of a (ghosts width 1), a's ghosts

@@ -231,6 +231,45 @@ def test_push_equals_fill(rng, n, m, per):
             assert torch.equal(b1.fab(i).data, b2.fab(i).data), (name, i)
 
 
+@pytest.mark.parametrize("n,m", [(64, 32), (128, 64), (64, 64), (96, 32)])
+def test_pull_equals_fill(rng, n, m):
+    """Ghost pull (ghosts.pull_table): the sweep and its NORM variant, run on
+    an input whose ghosts hold garbage, produce the bits of fill_boundary(width
+    2) + the sweep, and leave the input's ghosts exactly as that fill does."""
+    from paper_2009_12009_b200.ghosts import pull_table
+
+    dom, ba, dm, tr, p3, a, rhs, g, gr = _setup(rng, n, m)
+    for name in ("sweep", "norm"):
+        ref_b = A.MultiFab(ba, dm, 1, 2)
+        n1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        if name == "sweep":
+            S.gsrb_sweep(a, ref_b, rhs, DH)
+        else:
+            S.gsrb_sweep_norm(a, ref_b, rhs, DH, n1)
+        a2 = A.MultiFab(ba, dm, 1, 2)
+        a2.setval(-7777.0)
+        a2.load_valid_from(dom, g)
+        tab = pull_table(a2, dom, p3, 2)
+        assert tab is not None and not tab.remote
+        b2 = A.MultiFab(ba, dm, 1, 2)
+        n2 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        S.gsrb_sweep_pull(a2, b2, rhs, DH, tab, norm=None if name == "sweep" else n2)
+        torch.cuda.synchronize()
+        _eq(_valid(ref_b), _valid(b2))
+        for i in a.fabs:
+            assert torch.equal(a.fab(i).data, a2.fab(i).data), (name, i)
+        assert torch.equal(n1, n2), name
+
+
+def test_pull_table_rejects_irregular_layout():
+    from paper_2009_12009_b200.ghosts import pull_table
+
+    ba = A.BoxArray([A.Box((0, 0, 0), (63, 63, 31)), A.Box((0, 0, 32), (31, 63, 63)), A.Box((32, 0, 32), (63, 63, 63))])
+    dm = A.DistributionMapping.single_rank(len(ba))
+    f = A.MultiFab(ba, dm, 1, 2)
+    assert pull_table(f, A.Box((0, 0, 0), (63, 63, 63)), True, 2) is None
+
+
 def test_push_table_rejects_irregular_layout():
     from paper_2009_12009_b200.ghosts import push_table
 
