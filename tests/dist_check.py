@@ -105,16 +105,20 @@ def main():
     # (default: p2p fills; True: every ghost pushed by the sweeps; "remote":
     # cross-GPU faces pushed, same-GPU records copied by the barrier fill)
     if tr.p2p:
-        for variant in (True, "remote"):
+        for variant in (True, "remote", "pull"):
             phi2 = A.MultiFab(ba, dmw, 1, 1)
-            mg2 = A.MLMG(geom, ba, dmw, transport=tr, ghost_push=variant)
-            pushing = any(lv.push is not None and lv.push[0].remote for lv in mg2.levels)
+            if variant == "pull":  # sweeps copy their input's ghosts themselves
+                mg2 = A.MLMG(geom, ba, dmw, transport=tr, ghost_pull=True)
+            else:
+                mg2 = A.MLMG(geom, ba, dmw, transport=tr, ghost_push=variant)
+            pushing = any((lv.push is not None and lv.push[0].remote) or (lv.pull is not None and lv.pull[0].remote)
+                          for lv in mg2.levels)
             mg2.solve(phi2, rhs, rtol=1e-10, max_iter=60)
             same2 = all(torch.equal(phi.fab(i).valid(), phi2.fab(i).valid()) for i in phi.fabs)
             flag = torch.tensor([1 if (same2 and mg2.history == mg.history) else 0], device="cuda")
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
             if rank == 0:
-                print(f"ghost_push={variant}: remote={pushing} identical={bool(flag.item())}", flush=True)
+                print(f"ghost exchange {variant}: remote={pushing} identical={bool(flag.item())}", flush=True)
                 ok = ok and bool(flag.item())
 
     # -- failure detection: a peer that never arrives ---------------------------------

@@ -115,6 +115,23 @@ def test_ghost_push_solve_matches_oracle_bitwise(n, m):
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
 
 
+@pytest.mark.parametrize("n,m", [(64, 32), (128, 128)])
+def test_ghost_pull_solve_matches_oracle_bitwise(n, m):
+    """MLMG(ghost_pull=True): sweeps whose input ghosts are stale copy them
+    themselves (amrb_gsrb_sweep_pull, no copy-program fill before them) --
+    same iterations, history and solution as the oracle."""
+    dom, ba, dm, geom, rhs = _problem(n, m, seed=4)
+    ref = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), tboxes(ba)).solve(rhs, rtol=1e-10, max_iter=100)
+    phi = A.MultiFab(ba, dm, 1, 1)
+    b = A.MultiFab(ba, dm, 1, 0)
+    b.load_valid_from(dom, rhs)
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), ghost_pull=True)
+    assert any(lv.pull for lv in mg.levels)
+    mg.solve(phi, b, rtol=1e-10, max_iter=100)
+    assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
+    assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
+
+
 @pytest.mark.parametrize("n,m", [(128, 64), (256, 64)])
 def test_fused_prolong_sweep_solve_identical(n, m):
     """MLMG(fuse_prolong=True) (default: prolongation inside the first
