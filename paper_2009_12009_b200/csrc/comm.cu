@@ -57,7 +57,7 @@ struct DevRec {
   int32_t e0, e1, e2;
   int32_t from_buf;  // 1: source is the receive/staging buffer
   int32_t src_peer = -1;  // >= 0: source lives in that peer's storage (p2p mode)
-  int32_t pad_ = 0;
+  int32_t vec = 0;  // 1: moved as 16-byte pairs (even row length, even offsets and strides; large records)
 };
 
 struct PeerPtrs {
@@ -113,6 +113,24 @@ __device__ __forceinline__ void rec_cell(const DevRec& r, int64_t loc, int64_t c
   dofs = r.dst + c * r.dcs + (int64_t)i * r.ds0 + (int64_t)j * r.ds1 + k;
 }
 
+// rec_cell for a vec record: loc indexes cell PAIRS (comp, i, j, k/2)
+__device__ __forceinline__ void rec_pair(const DevRec& r, int64_t loc, int64_t units, int ncomp, int64_t& so,
+                                         int64_t& dofs) {
+  int c = 0;
+  unsigned t = (unsigned)loc;
+  if (ncomp > 1) {
+    c = (int)(loc / units);
+    t = (unsigned)(loc - (int64_t)c * units);
+  }
+  const unsigned e2h = (unsigned)r.e2 >> 1, e1 = (unsigned)r.e1;
+  const unsigned row = t / e2h;
+  const unsigned k = 2 * (t - row * e2h);
+  const unsigned i = row / e1;
+  const unsigned j = row - i * e1;
+  so = r.src + c * r.scs + (int64_t)i * r.ss0 + (int64_t)j * r.ss1 + k;
+  dofs = r.dst + c * r.dcs + (int64_t)i * r.ds0 + (int64_t)j * r.ds1 + k;
+}
+
 // With sy.on (p2p fills) the launch also is the cross-rank barrier that used to
 // precede it: CTA 0 publishes this rank's next epoch in every peer's pad; CTA 0
 // and every CTA that reads a peer's storage wait until all peers published
@@ -122,7 +140,7 @@ __device__ __forceinline__ void rec_cell(const DevRec& r, int64_t loc, int64_t c
 // peer's earlier pulls from this rank before whatever follows it here.
 template <bool kAdd>
 __global__ void __launch_bounds__(kCopyThreads)
-    k_copy(const DevRec* __restrict__ recs, const int2* __restrict__ blocks, int ncomp,
+    k_copy(const DevRec* __restrict__ recs, const int2* __restrict__ blocks, int ncomp, int aligned,
            const double* __restrict__ src, const double* __restrict__ buf, double* __restrict__ dst,
            const __grid_constant__ PeerPtrs peers, const __grid_constant__ SyncArgs sy) {
   amrb::pdl_entry();
@@ -149,7 +167,47 @@ __global__ void __launch_bounds__(kCopyThreads)
   }
   double v[kCopyItems];
   int64_t dofs[kCopyItems];
-  if (bl.x >= 0) {  // one large record, chunk starting at flat index bl.y
+  bool paired = false;
+  if (bl.x >= 0 && recs[bl.x].vec) {  // one large record moved as 16-byte pairs
+    paired = true;
+    const DevRec r = recs[bl.x];
+    const int64_t units = (int64_t)r.e0 * r.e1 * (r.e2 >> 1);
+    const int64_t end = min(units * ncomp, (int64_t)bl.y + kChunk);
+    const double* s = r.from_buf ? buf : (r.src_peer >= 0 ? peers.p[r.src_peer] : src);
+    double2 w2[kCopyItems];
+#pragma unroll
+    for (int u = 0; u < kCopyItems; ++u) {
+      const int64_t loc = (int64_t)bl.y + u * kCopyThreads + threadIdx.x;
+      dofs[u] = -1;
+      if (loc < end) {
+        int64_t so, dof;
+        rec_pair(r, loc, units, ncomp, so, dof);
+        dofs[u] = dof;
+        if (aligned) {
+          w2[u] = *reinterpret_cast<const double2*>(s + so);
+        } else {  // a base pointer off 16 bytes: same pairs, scalar accesses
+          w2[u].x = s[so];
+          w2[u].y = s[so + 1];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCopyItems; ++u) {
+      if (dofs[u] < 0) continue;
+      double* q = dst + dofs[u];
+      double2 o = w2[u];
+      if (kAdd) {
+        o.x = q[0] + o.x;
+        o.y = q[1] + o.y;
+      }
+      if (aligned) {
+        *reinterpret_cast<double2*>(q) = o;
+      } else {
+        q[0] = o.x;
+        q[1] = o.y;
+      }
+    }
+  } else if (bl.x >= 0) {  // one large record, chunk starting at flat index bl.y
     const DevRec r = recs[bl.x];
     const int64_t cells = (int64_t)r.e0 * r.e1 * r.e2;
     const int64_t end = min(cells * ncomp, (int64_t)bl.y + kChunk);
@@ -200,7 +258,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     }
   }
 #pragma unroll
-  for (int u = 0; u < kCopyItems; ++u) {
+  for (int u = 0; u < kCopyItems && !paired; ++u) {
     if (dofs[u] < 0) continue;
     if (kAdd)
       dst[dofs[u]] = dst[dofs[u]] + v[u];
@@ -268,7 +326,13 @@ void prepare_wave(Wave& w, int ncomp) {
     w.total += n;
     if (n >= kSmall) {
       close_pack();  // packs hold consecutive records only
-      for (int64_t o = 0; o < n; o += kChunk) w.blocks.push_back(make_int2((int)i, (int)o));
+      // 16-byte pairs when every row starts 16-byte aligned on both sides
+      // (allocations are 256-byte aligned; offsets and strides in elements)
+      auto even = [](int64_t x) { return (x & 1) == 0; };
+      r.vec = even(r.e2) && even(r.src) && even(r.dst) && even(r.ss0) && even(r.ss1) && even(r.ds0) &&
+              even(r.ds1) && (ncomp == 1 || (even(r.scs) && even(r.dcs)));
+      const int64_t units = r.vec ? n / 2 : n;
+      for (int64_t o = 0; o < units; o += kChunk) w.blocks.push_back(make_int2((int)i, (int)o));
       continue;
     }
     if (packn && (packc + n > kChunk || packn == kPackMax)) close_pack();
@@ -285,10 +349,15 @@ bool run_wave(const Wave& w, int ncomp, bool add, const double* src, const doubl
               cudaStream_t st, const PeerPtrs& peers = PeerPtrs{}, const SyncArgs& sy = SyncArgs{}) {
   if (w.blocks.empty()) return false;
   const unsigned nb = (unsigned)w.blocks.size();
+  // 16-byte accesses for the pair records need every base 16-byte aligned
+  uintptr_t bases = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(buf) |
+                    reinterpret_cast<uintptr_t>(dst);
+  for (int r = 0; r < kMaxPeers; ++r) bases |= reinterpret_cast<uintptr_t>(peers.p[r]);
+  const int aligned = (bases & 15) == 0;
   if (add)
-    launch_k(k_copy<true>, nb, kCopyThreads, 0, st, w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
+    launch_k(k_copy<true>, nb, kCopyThreads, 0, st, w.recs.p, w.dblocks.p, ncomp, aligned, src, buf, dst, peers, sy);
   else
-    launch_k(k_copy<false>, nb, kCopyThreads, 0, st, w.recs.p, w.dblocks.p, ncomp, src, buf, dst, peers, sy);
+    launch_k(k_copy<false>, nb, kCopyThreads, 0, st, w.recs.p, w.dblocks.p, ncomp, aligned, src, buf, dst, peers, sy);
   check_launch("k_copy");
   return true;
 }
