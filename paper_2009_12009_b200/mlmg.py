@@ -208,13 +208,14 @@ class MLMG:
         # a 32^3 single-box level above a 16^3 .. tail joins it: the cluster
         # variant of the tail kernel (8 CTAs, the 32^3 level split in slabs
         # across their shared memory) runs it too.  cluster_tail: 0 / False
-        # off, 1 / True / None (default) cubic chains, 2 also 32 x n1 x n2 top
+        # off, 1 / True cubic chains, 2 / None (default) also 32 x n1 x n2 top
         # levels (n1, n2 powers of two <= 32: the multi-GPU weak-scaling chains
-        # 32x16x16 .. and 32x32x16 ..; bit-identical but measured slower than
-        # the one-CTA non-cubic tail).  The library picks the kernel
-        # from the same shape test and reports the ghost width it wrote.
+        # 32x16x16 .. and 32x32x16 ..; at 4 GPUs the cluster tail from
+        # 32x32x16 takes 47.5 us against 29 us of grid level + 35.7 us of
+        # one-CTA tail, tools/r2aj.sh).  The library picks the kernel from the
+        # same shape test and reports the ghost width it wrote.
         self.cluster_tail = False
-        self.cluster_mode = 1 if cluster_tail is None else int(cluster_tail)
+        self.cluster_mode = 2 if cluster_tail is None else int(cluster_tail)
         if self.cluster_mode not in (0, 1, 2):
             raise ValueError("cluster_tail must be 0, 1, 2 or a bool")
         noncubic = self.cluster_mode == 2

@@ -235,7 +235,7 @@ def test_noncubic_pow2_tail_matches_oracle(shape, mode):
     b.load_valid_from(dom, rhs)
     mg = A.MLMG(geom, ba, dm, transport=A.Transport(1), cluster_tail=mode)
     assert mg.tail < len(mg.levels)
-    # the non-cubic cluster tail is opt-in (cluster_tail=2)
+    # the non-cubic cluster tail needs cluster_tail=2 (the default); 1 = cubic only
     assert mg.cluster_tail == (mode == 2 and shape[0] == 64)
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]

@@ -13,7 +13,8 @@ ba = A.BoxArray([dom]).max_size(64)
 dm = A.sfc_distribute(ba, A.default_costs(ba), world)
 tr = A.Transport.distributed()
 geom = A.Geometry(dom, (0.0,) * 3, tuple(e / 256.0 for e in ext), True)
-mg = A.MLMG(geom, ba, dm, transport=tr)
+mg = A.MLMG(geom, ba, dm, transport=tr, cluster_tail=int(os.environ.get('MB_CLUSTER', '2')),
+           grid_level_cells=int(os.environ['MB_GRID']) if 'MB_GRID' in os.environ else None)
 for lv in mg.levels:
     for fa in lv.phi: fa.storage.normal_()
     lv.rhs.storage.normal_()
