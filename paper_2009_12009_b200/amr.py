@@ -22,6 +22,7 @@ import ctypes as C
 import numpy as np
 import torch
 
+from . import counters
 from ._native import check, lib
 from .boxes import Box, IntVect, box_diff
 from .comm import Transport, copy_into, fill_boundary, parallel_copy
@@ -522,14 +523,24 @@ class AdvectionSolver:
         dt = self.dt_coarse()
         if self._graph is not None:
             self._graph.replay()
+            self._replay_counts()
         elif self.use_graph and self.step_count >= 2:
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
+            # the step's message / byte tallies are accounted on the host while
+            # the launches are captured; a replay adds the same amounts
+            # (counters.py names, transport.py:40-58 counts per step)
+            before = counters.snapshot()
+            # NCCL send/recv inside a capture need the relaxed mode
+            mode = "relaxed" if self.transport.mode == "nccl" else "global"
             with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
+                with torch.cuda.graph(g, stream=s, capture_error_mode=mode):
                     self._advance(dt, check=False)
             torch.cuda.current_stream().wait_stream(s)
+            after = counters.snapshot()
+            self._step_counts = {k: after[k] - before.get(k, 0) for k in ("transport_messages", "transport_bytes")
+                                 if after.get(k, 0) != before.get(k, 0)}
             self._graph = g
             g.replay()  # capture records the launches without running them
         else:
@@ -537,6 +548,10 @@ class AdvectionSolver:
         self.time += dt
         self.step_count += 1
         return dt
+
+    def _replay_counts(self):
+        for k, v in getattr(self, "_step_counts", {}).items():
+            counters.incr(k, v)
 
     def _advance(self, dt, check):
         dim = self.dim
