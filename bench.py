@@ -784,11 +784,19 @@ def main():
     ap.add_argument("--no-other-configs", action="store_true", help="skip the C1 / C5 microtimings of the C3 line")
     ap.add_argument("--ghost-push", default="auto", choices=["auto", "on", "off", "remote"],
                     help="A/B runs: MLMG ghost push (auto: across GPUs only)")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="A/B runs: set a library option (amrb_set_option) before building")
     ap.add_argument("--config", default="c3", choices=["c3", "c5"],
                     help="c3: the headline MLMG solve (C3 / C4 weak scaling); c5: 512^3 sweeps (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.option:
+        from paper_2009_12009_b200._native import set_option
+
+        for kv in args.option:
+            name, _, value = kv.partition("=")
+            set_option(name, int(value))
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "c5":

@@ -438,6 +438,14 @@ int amrb_level_grid(int up, const int32_t* lohi, const double* dh, const amrb_fi
 int amrb_reduce(const amrb_level* lv, const amrb_field* x, const double* x_base,
                 int comp, int kind, double* dev_out, void* stream);
 
+/* FillBoundary (fabarray.py:364) of a level that is ONE periodic box equal to
+ * its domain: every ghost cell within `width` is copied from its periodic
+ * image, as the fill plan's records would (same bits), in one launch without
+ * a record table.  AMRB_ENOTSUP unless the level has exactly one resident box
+ * and width <= both the field's ghost width and the box extent on each axis
+ * (3-D).  ncomp = the field's component count. */
+int amrb_fill_wrap(const amrb_level* lv, amrb_field* f, double* base, int ncomp, int width,
+                   void* stream);
 /* setval (fabarray.py:119-122, Fab.setval :58-65): components [comp0, comp1)
  * of box `box` (-1: every resident box) = value: ghosts 0 the valid cells,
  * 1 the grown box, 2 the ghost cells only. */

@@ -51,6 +51,7 @@ _SIGS = {
     "amrb_get_option": (C.c_int, [C.c_char_p, P(i64)]),
     "amrb_zero": (C.c_int, [vp, i64, vp]),
     "amrb_fill": (C.c_int, [vp, i64, f64, vp]),
+    "amrb_fill_wrap": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
     "amrb_setval": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, f64, vp]),
     "amrb_store_host": (C.c_int, [vp, vp, i64, vp]),
     "amrb_morton_key": (C.c_int, [C.c_int, P(i32), P(i32), P(C.c_uint64)]),

@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import counters
-from ._native import check, i32p, i64p, lib, ptr
+from ._native import AMRB_ENOTSUP, check, i32p, i64p, lib, ptr
 from .boxes import box_diff
 from .device import field_of, level_of, stream_ptr
 from .plans import (
@@ -35,6 +35,7 @@ from .plans import (
     build_plan_copy_grown,
     build_plan_fill_boundary,
     build_plan_sum_boundary,
+    normalize_periodic,
 )
 
 __all__ = [
@@ -330,8 +331,27 @@ def fill_boundary(fa, transport, domain, periodic=None, ngrow=None, _post_barrie
         raise ValueError("fill width exceeds the FabArray's ghost width")
     if ng == 0:
         return
+    if _single_periodic_box(fa, transport, domain, periodic, _local_sources):
+        # one box that is the whole periodic domain: every ghost is a wrapped
+        # copy of the box itself -- one record-free launch (amrb_fill_wrap)
+        fa.require_cuda("fill_boundary")
+        rc = lib().amrb_fill_wrap(level_of(fa).handle, field_of(fa).handle, C.c_void_p(fa.storage.data_ptr()),
+                                  fa.ncomp, ng, stream_ptr())
+        if rc == 0:
+            return
+        if rc != AMRB_ENOTSUP:
+            check(rc)
     plan = build_plan_fill_boundary(fa.ba, ng, domain, periodic)
     _execute(plan, fa, fa, transport, 2 if _local_sources else 0, post_barrier=_post_barrier)
+
+
+def _single_periodic_box(fa, transport, domain, periodic, local_sources):
+    if local_sources or transport.nranks != 1 or fa.dim != 3 or len(fa.ba) != 1 or domain is None:
+        return False
+    if not all(normalize_periodic(periodic, fa.dim)):
+        return False
+    b = fa.ba[0]
+    return tuple(b.lo) == tuple(domain.lo) and tuple(b.hi) == tuple(domain.hi) and bool(fa.resident[0])
 
 
 def parallel_copy(dst_fa, src_fa, transport, domain=None, periodic=None):

@@ -138,6 +138,7 @@ struct StreamArgs {
   // the ghost copy of output cell (i, j, k) of box b toward direction
   // (dx, dy, dz) is at push[27 b + 9 (dx+1) + 3 (dy+1) + (dz+1)] + i s0 + j s1 + k
   const long long* push;
+  int push_fence;
   // in-kernel ghost pull (ghosts.pull_table): per box 27 source addresses (0:
   // none; bit 0 set: the source box is on another GPU); the INPUT's ghost cell
   // (i, j, k) (box-local, inside direction d's width-2 slab) is copied from
@@ -640,7 +641,12 @@ __global__ void __launch_bounds__(32 * stream_warps<TJ, TK, RW>(), MINB)
   }
 
 #undef AMRB_DCHECK
-  if (PUSH && pushed) __threadfence_system();  // pushes to peers before the consumer's device barrier
+  // Pushes to peers before the consumer's device barrier: the barrier is
+  // signalled by a LATER kernel on this stream, and a kernel completes only
+  // once its stores (NVLink ones included) are acknowledged, so no fence is
+  // needed here; a system-scope fence would also wait behind in-flight PCIe
+  // copies.  (Library option "push_fence" = 1 restores it, for A/B runs.)
+  if (PUSH && pushed && args.push_fence) __threadfence_system();
   if (NORM) {
     for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
     if (strip && lane == 0 && nmax) atomicMax(args.norm, nmax);
@@ -900,6 +906,7 @@ bool launch_stream(Level& lv, const Field& a, const double* a_base, const Field&
   }
   args.norm = norm;
   args.push = push;
+  args.push_fence = (int)option("push_fence");
   if (XCH == 2) {
     args.pull = pull->tab;
     args.a = const_cast<double*>(a_base);

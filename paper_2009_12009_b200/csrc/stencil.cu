@@ -37,7 +37,7 @@ namespace {
 std::mutex g_opt_mu;
 std::map<std::string, int64_t>& options() {
   static std::map<std::string, int64_t> o = {{"pdl", 2}, {"sweep_kernel", 0}, {"grid_per_sm", 0}, {"stream_segments", 0}, {"stream_alternate", 1},
-                                               {"stream_config", 0},
+                                               {"stream_config", 0}, {"push_fence", 0},
                                                {"peer_timeout_ms", 30000}};
   return o;
 }
@@ -955,6 +955,93 @@ extern "C" int amrb_setval(const amrb_level* lv_, amrb_field* f, double* base, i
     amrb::launch_k(amrb::k_setval, dim3(box >= 0 ? 64 : 16, box >= 0 ? 1 : lv.nboxes), 256, 0, (cudaStream_t)stream,
                    lv.dgeo.p, fld.dev.p, base, lv.nboxes, box, gw, comp0, comp1, value, ghosts == 2 ? 1 : 0);
     amrb::check_launch("k_setval");
+  });
+}
+
+namespace amrb {
+namespace {
+// FillBoundary of a single periodic box (the box is the whole domain): every
+// ghost cell within w of the box is a copy of the valid cell its periodic
+// image names -- the records fabarray.py:254-277 builds for this layout, as
+// one kernel without a record table.  Warps take whole grown rows (rows of
+// the ghost planes, ghost rows of the valid planes), threads the 2w ghost
+// cells at the two ends of each valid row (16-byte pairs when w = 2).
+__device__ __forceinline__ int wrap_idx(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+
+__global__ void __launch_bounds__(256) k_wrap_fill(double* base, FabView v, int n0, int n1, int n2, int w, int ncomp,
+                                                   int blocks_a, int pairs) {
+  pdl_entry();
+  const int rows_a = 2 * w * (n1 + 2 * w) + n0 * 2 * w;
+  const int segs = (n2 + 2 * w + 31) / 32;  // 32-cell segments per grown row: one per warp
+  if ((int)blockIdx.x < blocks_a) {
+    const int item = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const int ra = item / segs;
+    if (ra >= rows_a) return;
+    const int k = (item - ra * segs) * 32 + lane - w;
+    int ip, j;
+    const int ga = 2 * w * (n1 + 2 * w);
+    if (ra < ga) {
+      const int pl = ra / (n1 + 2 * w);
+      ip = pl < w ? pl - w : n0 + (pl - w);
+      j = ra - pl * (n1 + 2 * w) - w;
+    } else {
+      const int r2 = ra - ga;
+      ip = r2 / (2 * w);
+      const int t = r2 - ip * 2 * w;
+      j = t < w ? t - w : n1 + (t - w);
+    }
+    const int64_t drow = v.off + (int64_t)ip * v.s0 + (int64_t)j * v.s1;
+    const int64_t srow = v.off + (int64_t)wrap_idx(ip, n0) * v.s0 + (int64_t)wrap_idx(j, n1) * v.s1;
+    if (k < n2 + w)
+      for (int c = 0; c < ncomp; ++c) base[drow + c * v.cs + k] = base[srow + c * v.cs + wrap_idx(k, n2)];
+    return;
+  }
+  const int rb = (blockIdx.x - blocks_a) * 256 + threadIdx.x;
+  if (rb >= n0 * n1) return;
+  const int ip = rb / n1, j = rb - ip * n1;
+  const int64_t row = v.off + (int64_t)ip * v.s0 + (int64_t)j * v.s1;
+  for (int c = 0; c < ncomp; ++c) {
+    double* r = base + row + c * v.cs;
+    if (pairs) {  // w = 2: cols -2, -1 <- n2-2, n2-1 and n2, n2+1 <- 0, 1
+      const double2 lo = *reinterpret_cast<const double2*>(r + n2 - 2);
+      const double2 hi = *reinterpret_cast<const double2*>(r);
+      *reinterpret_cast<double2*>(r - 2) = lo;
+      *reinterpret_cast<double2*>(r + n2) = hi;
+    } else {
+      for (int k = 1; k <= w; ++k) {
+        r[-k] = r[n2 - k];
+        r[n2 + k - 1] = r[k - 1];
+      }
+    }
+  }
+}
+}  // namespace
+}  // namespace amrb
+
+extern "C" int amrb_fill_wrap(const amrb_level* lv_, amrb_field* f, double* base, int ncomp, int width,
+                              void* stream) {
+  return amrb::guarded([&] {
+    const amrb::Level& lv = amrb::L(lv_);
+    const amrb::Field& fld = amrb::F(f);
+    amrb::need_same_level(fld, lv, "fill_wrap");
+    if (lv.nboxes != 1 || !lv.resident[0]) throw amrb::Error(AMRB_ENOTSUP, "fill_wrap: one resident box only");
+    const amrb::BoxGeom& g = lv.geo[0];
+    if (ncomp < 1) throw amrb::Error(AMRB_EINVAL, "fill_wrap: ncomp < 1");
+    if (width < 1) return;
+    for (int a = 0; a < 3; ++a)
+      if (fld.ng3[a] < width || g.n[a] < width) throw amrb::Error(AMRB_ENOTSUP, "fill_wrap: ghost width exceeds box");
+    const amrb::FabView v = fld.host[0];
+    const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+    const int rows_a = 2 * width * (n1 + 2 * width) + n0 * 2 * width;
+    const long long items_a = (long long)rows_a * ((n2 + 2 * width + 31) / 32);
+    const int blocks_a = (int)((items_a + 7) / 8);
+    const long long rows_b = (long long)n0 * n1;
+    const int blocks_b = (int)((rows_b + 255) / 256);
+    const bool even = !(v.off & 1) && !(v.s0 & 1) && !(v.s1 & 1) && !(v.cs & 1) && !(n2 & 1);
+    const int pairs = width == 2 && even && !(reinterpret_cast<uintptr_t>(base) & 15);
+    amrb::launch_k(amrb::k_wrap_fill, blocks_a + blocks_b, 256, 0, (cudaStream_t)stream, base, v, n0, n1, n2, width,
+                   ncomp, blocks_a, pairs);
+    amrb::check_launch("k_wrap_fill");
   });
 }
 

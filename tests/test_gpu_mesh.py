@@ -54,6 +54,42 @@ def test_fill_boundary_matches_dense_wrap_oracle(rng):
                         assert np.array_equal(got, g[(slice(None),) + src])
 
 
+@pytest.mark.parametrize("shape,ngrow,width,ncomp", [((16, 16, 16), 2, 2, 1), ((16, 12, 20), 2, 1, 2),
+                                                     ((8, 10, 6), 3, 3, 1), ((32, 8, 64), 2, 2, 2),
+                                                     ((6, 6, 6), 1, 1, 3)])
+def test_single_periodic_box_fill_matches_plan_and_oracle(rng, shape, ngrow, width, ncomp):
+    """One box = the whole periodic domain takes the record-free wrap kernel
+    (amrb_fill_wrap); it leaves every cell -- ghosts beyond the fill width
+    included -- exactly as the fill-plan copy program and as the dense-wrap
+    oracle."""
+    from paper_2009_12009_b200 import comm
+    from paper_2009_12009_b200.plans import build_plan_fill_boundary
+
+    dom = A.Box((0, 0, 0), tuple(e - 1 for e in shape))
+    ba = A.BoxArray([dom])
+    dm = A.DistributionMapping.single_rank(1)
+    g = rng.normal(size=(ncomp,) + shape)
+    tr = A.Transport(1)
+    a = A.MultiFab(ba, dm, ncomp, ngrow)
+    b = A.MultiFab(ba, dm, ncomp, ngrow)
+    for f in (a, b):
+        _sentinel_load(f, dom, g)
+    assert comm._single_periodic_box(a, tr, dom, True, False)
+    A.fill_boundary(a, tr, dom, True, ngrow=width)
+    comm._execute(build_plan_fill_boundary(ba, width, dom, True), b, b, tr, 0)  # the copy program
+    torch.cuda.synchronize()
+    assert torch.equal(a.fab(0).data, b.fab(0).data)
+    data = a.fab(0).data.cpu().numpy()
+    fab = a.fab(0)
+    for cell in fab.gbox.cells():
+        loc = tuple(cell[d] - fab.gbox.lo[d] for d in range(3))
+        if all(-width <= cell[d] < shape[d] + width for d in range(3)):
+            src = tuple(cell[d] % shape[d] for d in range(3))
+            assert np.array_equal(data[(slice(None),) + loc], g[(slice(None),) + src])
+        else:
+            assert np.all(data[(slice(None),) + loc] == -7777.0)
+
+
 def test_fill_boundary_equals_oracle_executor(rng):
     for dim in (1, 2, 3):
         for _ in range(3):
