@@ -346,7 +346,11 @@ def fill_boundary(fa, transport, domain, periodic=None, ngrow=None, _post_barrie
 
 
 def _single_periodic_box(fa, transport, domain, periodic, local_sources):
-    if local_sources or transport.nranks != 1 or fa.dim != 3 or len(fa.ba) != 1 or domain is None:
+    # one process, or a replicated FabArray (every rank holds the whole box:
+    # the fill involves no peer)
+    if local_sources or fa.dim != 3 or len(fa.ba) != 1 or domain is None:
+        return False
+    if transport.nranks != 1 and not getattr(fa, "replicated", False):
         return False
     if not all(normalize_periodic(periodic, fa.dim)):
         return False
