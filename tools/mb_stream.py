@@ -83,17 +83,23 @@ def case(shape, m, reps, rows):
                 ("sweep+push", 0, cfg, lambda: S.gsrb_sweep(a, b, rhs, dh, push=tab)),
                 ("sweep_norm+push", 0, cfg, lambda: S.gsrb_sweep_norm(a, b, rhs, dh, nrm, push=tab)),
                 ("sweep_prolong+push", 0, cfg, lambda: S.gsrb_sweep_prolong(a, b, rhs, dh, c, push=tab))]
+    want = os.environ.get("MB_OPS")
+    segs_list = [int(x) for x in os.environ.get("MB_SEGS", "0").split(",")]
     for name, kern, cfg, fn in ops:
-        try:
-            with option("sweep_kernel", kern), option("stream_config", cfg):
-                us = timeit(fn, reps)
-        except (NotImplementedError, ValueError) as e:
-            rows.append({"shape": shape, "box": m, "op": name, "kernel": kern, "error": str(e)})
+        if want and name not in want.split(","):
             continue
-        row = {"shape": list(shape), "box": m, "op": name, "kernel": ["stream", "legacy"][kern], "cfg": cfg,
-               "us": round(us, 2), "alg_GBs": round(alg / us / 1e3, 1), "frac": round(alg / us / 1e3 / PEAK, 3)}
-        rows.append(row)
-        print(json.dumps(row), flush=True)
+        for segs in segs_list:
+            try:
+                with option("sweep_kernel", kern), option("stream_config", cfg), option("stream_segments", segs):
+                    us = timeit(fn, reps)
+            except (NotImplementedError, ValueError) as e:
+                rows.append({"shape": shape, "box": m, "op": name, "kernel": kern, "error": str(e)})
+                continue
+            row = {"shape": list(shape), "box": m, "op": name, "kernel": ["stream", "legacy"][kern], "cfg": cfg,
+                   "segs": segs, "us": round(us, 2), "alg_GBs": round(alg / us / 1e3, 1),
+                   "frac": round(alg / us / 1e3 / PEAK, 3)}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
 
 
 def main():
