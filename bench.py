@@ -56,6 +56,11 @@ def _golden_iterations(case):
         return json.load(f)[case]["iterations"]
 
 
+def _golden(case):
+    with open(os.path.join(ROOT, "tests", "golden", "mlmg_golden.json")) as f:
+        return json.load(f)[case]
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -261,6 +266,18 @@ def run_ours(args):
     barrier()
     clk.__exit__(None, None, None)
     t_dev = maxover(e0.elapsed_time(e1) / 1e3)
+    # the last timed solve against the CPU oracle's solve of the same rhs bits
+    # (tests/golden/mlmg_golden.json; C3 only -- outside the timed region)
+    parity = None
+    if world == 1:
+        gold = _golden("c3")
+        out = A.gather_global(phi, dom)
+        parity = {
+            "history_equals_oracle": [float(x).hex() for x in mg.history] == gold["history"],
+            "phi_sha256_equals_oracle": hashlib.sha256(np.ascontiguousarray(out).tobytes()).hexdigest()
+            == gold["phi_sha256"],
+            "solves_checked": "the last of the timed solves (the same MLMG object solved every step)",
+        }
     # eager launches (uploads, priming sweep, copies) + the captured iteration's
     # launches times the iterations the device loop ran
     launches = (lib().amrb_launch_count() - launches0) + sum(iters) * mg.launches_per_cycle
@@ -423,6 +440,7 @@ def run_ours(args):
                        "(sha256 %s...)" % (2 if world == 1 else 3, rhs_sha[:16]),
                 # the CPU oracle's iteration count on the same rhs bits (tests/golden/mlmg_golden.json)
                 "oracle_iterations": _golden_iterations("c3") if world == 1 else None,
+                "oracle_parity": parity,
                 "mlmg_solve_ms": ms, "global_batch": 1, "seq_len": dom.num_cells(),
                 "parallelism": f"dp{world} (boxes by Morton SFC)",
                 "l2": "working set (phi x2 + rhs, 256^3 fp64 per GPU = 0.4 GB) exceeds the 126 MB L2",

@@ -791,6 +791,7 @@ class MLMG:
             raise RuntimeError("captured iteration does not return the level buffers to their start state")
         self._loop = loop
         self._loop_cur = start
+        self._loop_entry = saved  # buffer state set_phi / _prime start from
         for lv, c in zip(self.levels, saved):
             lv.cur = c
 
@@ -834,6 +835,12 @@ class MLMG:
         top = self.levels[0]
         if self.use_graph and self._loop is None:
             self._capture()
+        if self._loop is not None:
+            # the captured loop expects the primed sweep's output where the
+            # capture left it: start every solve from the capture's entry
+            # state (a previous solve leaves lv.cur at the loop's state)
+            for lv, c in zip(self.levels, self._loop_entry):
+                lv.cur = c
         self.set_rhs(rhs)
         self.set_phi(phi)
         device_reduce(top.rhs, "absmax", 0, out=self.r0_dev)

@@ -121,6 +121,21 @@ def main():
                 print(f"ghost exchange {variant}: remote={pushing} identical={bool(flag.item())}", flush=True)
                 ok = ok and bool(flag.item())
 
+    # -- max-all-reduce over NVLink: values and NaN propagation -----------------------
+    if tr.p2p:
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64, device="cuda")
+        tr.peer_allmax(t)
+        nan = torch.tensor([float("nan") if rank == world - 1 else 1.0], dtype=torch.float64, device="cuda")
+        tr.peer_allmax(nan)
+        torch.cuda.synchronize()
+        good = t.item() == float(world) and bool(torch.isnan(nan).item())
+        flag = torch.tensor([1 if good else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"peer_allmax: max={t.item()} nan_propagates={bool(torch.isnan(nan).item())} ok={bool(flag.item())}",
+                  flush=True)
+            ok = ok and bool(flag.item())
+
     # -- failure detection: a peer that never arrives ---------------------------------
     if tr.p2p:
         from paper_2009_12009_b200._native import set_option

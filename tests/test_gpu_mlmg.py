@@ -280,3 +280,30 @@ def test_mlmg_boundary_arguments():
     with pytest.raises(ValueError):  # record disagrees with the geometry's periodic flags
         A.MLMG(A.Geometry(dom, (0.0,) * 3, (1.0,) * 3, True), ba, dm,
                bc=A.BoundaryRecord(("external",) * 3, ("external",) * 3))
+
+
+def test_max_iter_and_repeated_solves_follow_the_oracle():
+    """The WHILE-graph loop's state (device memory, reset by a kernel before
+    each launch): max_iter stops it exactly where the oracle stops, a second
+    solve of the same problem replays the same bits, max_iter=0 only returns
+    ||rhs|| and out-of-range max_iter is rejected."""
+    n, m = 64, 32
+    dom, ba, dm, geom, rhs = _problem(n, m, seed=21)
+    ref3 = R.OracleMLMG(((0, 0, 0), (n - 1,) * 3), tboxes(ba)).solve(rhs, rtol=1e-10, max_iter=3)
+    b = A.MultiFab(ba, dm, 1, 0)
+    b.load_valid_from(dom, rhs)
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1))
+    out = []
+    for _ in range(2):
+        phi = A.MultiFab(ba, dm, 1, 1)
+        rn = mg.solve(phi, b, rtol=1e-10, max_iter=3)
+        out.append((mg.iterations, list(mg.history), rn, A.gather_global(phi, dom)))
+    assert mg.graph_replays == 2
+    for it, hist, rn, phi in out:
+        assert it == 3 == ref3["iterations"] and hist == ref3["history"] and rn == hist[-1]
+        assert np.array_equal(phi, ref3["phi"])
+    phi = A.MultiFab(ba, dm, 1, 1)
+    r0 = mg.solve(phi, b, rtol=1e-10, max_iter=0)
+    assert mg.iterations == 0 and mg.history == [] and r0 == float(np.abs(rhs).max())
+    with pytest.raises(ValueError):
+        mg.solve(phi, b, max_iter=mg._HIST + 1)
