@@ -82,6 +82,17 @@ def main():
     say("mlmg built", [(lv.kind, len(lv.ba)) for lv in mg.levels], "tail", mg.tail)
     rn = mg.solve(phi, rhs, rtol=1e-10, max_iter=60)
     say("solve done", mg.iterations)
+    # a second solve on the same solver (graph replay) reproduces the first
+    hist1 = list(mg.history)
+    phi_again = A.MultiFab(ba, dmw, 1, 1)
+    mg.solve(phi_again, rhs, rtol=1e-10, max_iter=60)
+    same_again = mg.history == hist1 and all(torch.equal(phi.fab(i).valid(), phi_again.fab(i).valid())
+                                             for i in phi.fabs)
+    flag = torch.tensor([1 if same_again else 0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(f"repeated solve identical={bool(flag.item())}", flush=True)
+    ok = ok and bool(flag.item())
     mine = {i: f.valid().cpu().numpy() for i, f in phi.fabs.items()}
     allv = [None] * world
     dist.all_gather_object(allv, mine)
