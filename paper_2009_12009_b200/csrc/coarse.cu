@@ -738,8 +738,8 @@ __global__ void __launch_bounds__(512, 1) k_level_grid(GridLevelArgs a) {
         if (e0 + u * nt < ncell / 2) p[off[u]] = relax(nb[u].c, rh[u], lapn(nb[u]), a.cf.rgamma);
     }
   };
-  auto smooth = [&]() {
-    for (int q = 0; q < a.nsw; ++q) {
+  auto smooth = [&](int first) {
+    for (int q = first; q < a.nsw; ++q) {
       color(0);
       g.sync();
       color(1);
@@ -747,13 +747,25 @@ __global__ void __launch_bounds__(512, 1) k_level_grid(GridLevelArgs a) {
     }
   };
   if (!a.up) {
+    // the correction starts from zero: the first red half-sweep sees only
+    // zeros around its cells, so it is fused with the zeroing pass -- the same
+    // operations on the same (zero) operands, one pass and one grid sync less
     for (int e = t0; e < ncell; e += nt) {
       int i, j, k;
       cell(e, i, j, k);
-      P(i, j, k) = 0.0;
+      const bool red = (k & 1) == ((a.lo_par + i + j) & 1);
+      P(i, j, k) = red && a.nsw > 0 ? relax(0.0, a.rhs[i * a.rs0 + j * a.rs1 + k],
+                                            lap7(0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, a.cf), a.cf.rgamma)
+                                     : 0.0;
     }
-    g.sync();
-    smooth();
+    if (a.nsw > 0) {
+      g.sync();
+      color(1);
+      g.sync();
+      smooth(1);
+    } else {
+      g.sync();
+    }
     const int c0 = n0 >> 1, c1 = n1 >> 1, c2 = n2 >> 1;
     const int lc1 = a.l1 > 0 ? a.l1 - 1 : -1, lc2 = a.l2 > 0 ? a.l2 - 1 : -1;
     for (int e = t0; e < ncell / 8; e += nt) {
@@ -786,7 +798,7 @@ __global__ void __launch_bounds__(512, 1) k_level_grid(GridLevelArgs a) {
     P(i, j, k) = P(i, j, k) + a.c[(i >> 1) * a.cs0 + (j >> 1) * a.cs1 + (k >> 1)];
   }
   g.sync();
-  smooth();
+  smooth(0);
   // width-1 ghost layer of the grown box (valid cells are final)
   const int E1 = n1 + 2, E2 = n2 + 2, ng = (int)(n0 + 2) * E1 * E2;
   for (int e = t0; e < ng; e += nt) {
