@@ -96,6 +96,9 @@ int amrb_debug_checks(int64_t* failures, int64_t* line, int reset);
  *   "stream_config"    0  k_gsrb_stream tile / strip / depth variant (A/B runs)
  *   "peer_timeout_ms" 30000  bound on every device-side wait for a peer
  *                     (NVLink signal pads); 0 waits forever
+ *   "push_fence"   0  1: a ghost-pushing sweep ends with a system-scope
+ *                     fence (A/B runs; the consumer's barrier is signalled
+ *                     by a later kernel, after this one's stores completed)
  * AMRB_EINVAL for an unknown name. */
 int amrb_set_option(const char* name, int64_t value);
 int amrb_get_option(const char* name, int64_t* value);
