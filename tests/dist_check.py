@@ -116,10 +116,12 @@ def main():
     # (default: p2p fills; True: every ghost pushed by the sweeps; "remote":
     # cross-GPU faces pushed, same-GPU records copied by the barrier fill)
     if tr.p2p:
-        for variant in (True, "remote", "pull"):
+        for variant in (True, "remote", "pull", "nogrid"):
             phi2 = A.MultiFab(ba, dmw, 1, 1)
             if variant == "pull":  # sweeps copy their input's ghosts themselves
                 mg2 = A.MLMG(geom, ba, dmw, transport=tr, ghost_pull=True)
+            elif variant == "nogrid":  # replicated levels as streaming sweeps + wrap fills (the 8-GPU 128^3 level)
+                mg2 = A.MLMG(geom, ba, dmw, transport=tr, grid_level_cells=0)
             else:
                 mg2 = A.MLMG(geom, ba, dmw, transport=tr, ghost_push=variant)
             pushing = any((lv.push is not None and lv.push[0].remote) or (lv.pull is not None and lv.pull[0].remote)
