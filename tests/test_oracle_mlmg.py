@@ -110,3 +110,22 @@ def test_threaded_oracle_is_bit_identical():
     assert a["iterations"] == b["iterations"]
     assert a["history"] == b["history"]
     assert np.array_equal(a["phi"], b["phi"])
+
+
+@pytest.mark.parametrize("ext,m,nranks", [((256, 256, 256), 64, 1), ((128, 128, 128), 32, 1), ((512, 256, 256), 64, 2),
+                                          ((512, 512, 256), 64, 4), ((512, 512, 512), 64, 8), ((96, 64, 128), 32, 1),
+                                          ((64, 32, 32), 32, 1), ((48, 48, 48), 16, 1)])
+def test_device_hierarchy_has_the_oracle_resolutions(ext, m, nranks):
+    """mlmg.mg_hierarchy (the device solver's levels: it agglomerates earlier,
+    into replicated or one-box levels) keeps the oracle's level RESOLUTIONS
+    (oracle/mlmg_ref.py mg_levels) -- the box decomposition of a level does not
+    change its values, so the V-cycles stay bit-identical."""
+    import paper_2009_12009_b200 as A
+    from paper_2009_12009_b200.mlmg import mg_hierarchy
+
+    dom = A.Box((0, 0, 0), tuple(e - 1 for e in ext))
+    ba = A.BoxArray([dom]).max_size(m)
+    dev = [tuple(d.extents()) for d, _, _ in mg_hierarchy(dom, ba, nranks)]
+    boxes = [(tuple(b.lo), tuple(b.hi)) for b in ba]
+    ref = [tuple(M.ext(d)) for d, _, _ in R.mg_levels(((0, 0, 0), tuple(e - 1 for e in ext)), boxes)]
+    assert dev == ref
