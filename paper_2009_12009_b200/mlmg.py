@@ -25,6 +25,7 @@ runs the identical bottom solve.  Results are bit-identical for any GPU count.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 
@@ -341,8 +342,12 @@ class MLMG:
         # pinned block shared with the loop's control kernel (csrc/graph.cu):
         # rtol, (max_iter, iters), history
         # and its device twin the loop works on (nothing inside the loop touches
-        # host memory): rtol, (max_iter, iters), r0, history
-        self.loop_host = torch.zeros(3 + self._HIST, dtype=torch.float64).pin_memory()
+        # host memory): rtol, (max_iter, iters), r0, history.  Two host slots:
+        # solve(wait=False) lets the caller queue the next solve before
+        # reading this one's results (finish())
+        self.loop_host = [torch.zeros(3 + self._HIST, dtype=torch.float64).pin_memory() for _ in range(2)]
+        self._host_slot = 0
+        self._queued = collections.deque()  # solves queued by solve(wait=False), oldest first
         self.loop_dev = torch.zeros(3 + self._HIST, dtype=torch.float64, device=top.rhs.device)
         self.lag = None  # decided by the first _prime()
         self._loop = None
@@ -825,10 +830,18 @@ class MLMG:
         top = self.levels[0]
         parallel_copy(phi, top.phi[self._solution_index()], self.transport)
 
-    def solve(self, phi, rhs, rtol=1e-10, max_iter=200):
+    def solve(self, phi, rhs, rtol=1e-10, max_iter=200, wait=True):
         """Solve L(phi) = rhs to ||r||_inf <= rtol * ||rhs||_inf; phi is the
         initial guess and receives the solution.  Returns the final ||r||_inf;
-        ``iterations``, ``history`` and ``r0`` are left on the solver."""
+        ``iterations``, ``history`` and ``r0`` are left on the solver.
+
+        ``wait=False`` (graph solves): everything is queued on the current
+        stream and the call returns None at once; ``finish()`` waits for the
+        oldest queued solve and returns what solve() would have (so a caller
+        can queue the next solve before reading this one: no idle device
+        between solves).  At most two solves may be queued."""
+        if len(self._queued) >= 2:
+            raise RuntimeError("two solves already queued: call finish() first")
         max_iter = int(max_iter)
         if max_iter < 0 or max_iter > self._HIST:
             raise ValueError(f"max_iter must be in [0, {self._HIST}]")
@@ -848,9 +861,10 @@ class MLMG:
         self.history = []
         self.iterations = 0
         if max_iter == 0:
+            self._drain()
             self.r0 = self._host_scalar(self.r0_dev)
             self.get_phi(phi)
-            return self.r0
+            return self._done(self.r0, wait)
         self._prime()
         if self._loop is not None:
             for lv, c in zip(self.levels, self._loop_cur):
@@ -859,16 +873,17 @@ class MLMG:
                                         C.c_void_p(self.r0_dev.data_ptr()), stream_ptr()))
             check(lib().amrb_loop_launch(self._loop, stream_ptr()))
             self.graph_replays += 1
-            h = self.loop_host
+            h = self.loop_host[self._host_slot]
+            self._host_slot ^= 1
             check(lib().amrb_store_host(C.c_void_p(self.loop_dev.data_ptr()), C.c_void_p(h.data_ptr()),
                                         3 + max_iter, stream_ptr()))
-            torch.cuda.current_stream().synchronize()
-            self._check_faults()
-            self.r0 = float(h[2])
-            self.iterations = int(h.view(torch.int32)[3])
-            self.history = [float(x) for x in h[3:3 + self.iterations].tolist()]
-            rn = self.history[-1]
+            self.get_phi(phi)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._queued.append(("graph", h, ev))
+            return self.finish() if wait else None
         else:
+            self._drain()
             self.r0 = r0 = self._host_scalar(self.r0_dev)
             rn = r0
             while self.iterations < max_iter:
@@ -880,7 +895,34 @@ class MLMG:
                 if rn <= rtol * r0:
                     break
         self.get_phi(phi)
-        return rn
+        return self._done(rn, wait)
+
+    def _done(self, rn, wait):
+        """A solve that finished synchronously: queue its result for finish()."""
+        if wait:
+            return rn
+        self._queued.append(("done", (rn, self.r0, self.iterations, list(self.history)), None))
+        return None
+
+    def _drain(self):
+        while self._queued:
+            self.finish()
+
+    def finish(self):
+        """Wait for the oldest solve queued with solve(wait=False); sets r0,
+        iterations and history from it and returns its final ||r||_inf."""
+        if not self._queued:
+            raise RuntimeError("no queued solve")
+        kind, h, ev = self._queued.popleft()
+        if kind == "done":
+            rn, self.r0, self.iterations, self.history = h
+            return rn
+        ev.synchronize()
+        self._check_faults()
+        self.r0 = float(h[2])
+        self.iterations = int(h.view(torch.int32)[3])
+        self.history = [float(x) for x in h[3:3 + self.iterations].tolist()]
+        return self.history[-1]
 
 
 class _LocalView:

@@ -331,3 +331,36 @@ def test_noncubic_single_box_solve_matches_oracle(shape):
     mg.solve(phi, b, rtol=1e-10, max_iter=100)
     assert mg.iterations == ref["iterations"] and mg.history == ref["history"]
     assert np.array_equal(A.gather_global(phi, dom), ref["phi"])
+
+
+def test_queued_solves_equal_synchronous_solves():
+    """solve(wait=False) queues a solve on the stream; finish() returns the
+    oldest one's ||r|| and sets its iterations / history.  Two queued solves
+    of different right-hand sides give the synchronous solves' bits."""
+    n, m = 64, 32
+    dom, ba, dm, geom, rhs1 = _problem(n, m, seed=31)
+    rhs2 = np.random.default_rng(32).standard_normal((n, n, n))
+    rhs2 -= rhs2.mean()
+    mg = A.MLMG(geom, ba, dm, transport=A.Transport(1))
+    sync = []
+    for r in (rhs1, rhs2):
+        b = A.MultiFab(ba, dm, 1, 0)
+        b.load_valid_from(dom, r)
+        phi = A.MultiFab(ba, dm, 1, 1)
+        rn = mg.solve(phi, b, rtol=1e-10, max_iter=100)
+        sync.append((rn, mg.iterations, list(mg.history), A.gather_global(phi, dom)))
+    bs, phis = [], []
+    for r in (rhs1, rhs2):
+        b = A.MultiFab(ba, dm, 1, 0)
+        b.load_valid_from(dom, r)
+        bs.append(b)
+        phis.append(A.MultiFab(ba, dm, 1, 1))
+    assert mg.solve(phis[0], bs[0], rtol=1e-10, max_iter=100, wait=False) is None
+    assert mg.solve(phis[1], bs[1], rtol=1e-10, max_iter=100, wait=False) is None
+    with pytest.raises(RuntimeError):
+        mg.solve(phis[1], bs[1], wait=False)  # at most two queued
+    for (rn, it, hist, phi_ref), phi in zip(sync, phis):
+        assert mg.finish() == rn and mg.iterations == it and mg.history == hist
+        assert np.array_equal(A.gather_global(phi, dom), phi_ref)
+    with pytest.raises(RuntimeError):
+        mg.finish()
