@@ -453,6 +453,8 @@ def run_ours(args):
                 # the CPU oracle's iteration count on the same rhs bits (tests/golden/mlmg_golden.json)
                 "oracle_iterations": _golden_iterations("c3") if world == 1 else None,
                 "oracle_parity": parity,
+                "solves": "back to back: step s+1 is queued before step s's result is read "
+                          "(MLMG.solve(wait=False) / finish()); each runs its own device-side convergence test",
                 "mlmg_solve_ms": ms, "global_batch": 1, "seq_len": dom.num_cells(),
                 "parallelism": f"dp{world} (boxes by Morton SFC)",
                 "l2": "working set (phi x2 + rhs, 256^3 fp64 per GPU = 0.4 GB) exceeds the 126 MB L2",
