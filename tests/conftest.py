@@ -46,3 +46,23 @@ def amrkit():
     import amrkit as ak
 
     return ak
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Under the checked build (AMRB_LIBRARY=checked) report the device-side
+    invariant checks the whole session recorded (csrc/device.h AMRB_DCHECK)."""
+    if os.environ.get("AMRB_LIBRARY") != "checked":
+        return
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return
+        from paper_2009_12009_b200._native import debug_checks
+
+        fails, line = debug_checks(reset=False)
+        print(f"\nlibamrb_checked.so: session DCHECK failures {fails} (first at line {line})")
+        if fails:
+            session.exitstatus = 1
+    except Exception as e:  # report, do not mask the test outcome
+        print(f"\nchecked-build report unavailable: {e}")
